@@ -1,0 +1,247 @@
+/*
+ * hetserve_b200.h -- C ABI of the B200-native engine for the data-parallel
+ * core of arXiv 2504.15303 (reference package `hetserve`).
+ *
+ * Every entry point replaces one reference Python function on the hot path
+ * (paths relative to /root/reference/pkg/src/hetserve):
+ *
+ *   hs_search_tables   planner.py:143-181 estimate_system_throughput, one
+ *                      machine at a time, for every (machine, tp degree):
+ *                      capacity.py:72-95 kv_budget/check_memory_constraint,
+ *                      planner.py:51-87 plan_static_batches,
+ *                      planner.py:90-118 estimate_batch_time/time_batches/
+ *                      estimate_instance_throughput.
+ *   hs_search_best     planner.py:213-228 search_optimal_config product loop,
+ *                      reduced to (best total, lowest index) over an index
+ *                      range of the mixed-radix candidate space.
+ *   hs_search_rank     planner.py:213-228 again, full ranking (ranked.sort
+ *                      key (-total, tp tuple)) for spaces small enough to
+ *                      materialise.
+ *   hs_replay          simulator.py:272-363 run_continuous with
+ *                      scheduling.py:216-346 Scheduler.evaluate/choose/
+ *                      complete, for a batch of independent traces.
+ *
+ * Conventions: plain pointers and sizes, caller-owned host buffers, calls are
+ * synchronous (the reference API is synchronous).  One context per thread.
+ * Return value: HS_OK or an hs_status code; hs_last_error() gives text.
+ * Domain-level failures that the reference raises as exceptions are NOT call
+ * failures: they are reported per table entry (hs_entry.status) or per trace
+ * (hs_trace_result.error) so the Python shim can raise the same exception
+ * type with the same fields.
+ */
+#ifndef HETSERVE_B200_H
+#define HETSERVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_ABI_VERSION 1
+#define HS_MAX_DEGREES 32   /* power-of-two divisors of an accelerator count  */
+#define HS_MAX_MACHINES 64
+#define HS_MAX_INSTANCES 32 /* one warp lane per instance (round-1 kernel)    */
+
+/* call status */
+enum hs_status {
+  HS_OK = 0,
+  HS_ERR_ARG = 1,          /* bad argument (null pointer, size out of range) */
+  HS_ERR_CUDA = 2,         /* CUDA runtime failure                           */
+  HS_ERR_UNSUPPORTED = 3,  /* valid input the engine does not handle yet     */
+  HS_ERR_NOMEM = 4
+};
+
+/* Per-(machine, degree) outcome: which exception estimate_system_throughput
+ * (planner.py:143-181) raises for that machine, if any. */
+enum hs_entry_status {
+  HS_ENTRY_OK = 0,
+  HS_ENTRY_INFEASIBLE_CONFIG = 1,  /* planner.py:156-163 InfeasibleConfigError */
+  HS_ENTRY_MISSING_PARAMS = 2,     /* planner.py:164-166 SpecError             */
+  HS_ENTRY_INFEASIBLE_REQUEST = 3, /* planner.py:78-84 InfeasibleRequestError  */
+  HS_ENTRY_ZERO_DIVISION = 4,      /* planner.py:118 ZeroDivisionError (NOT caught
+                                      by search_optimal_config: aborts it)     */
+  HS_ENTRY_BAD_DEGREE = 5          /* capacity.py:79-83 SpecError (degree does
+                                      not divide the named machine's count)    */
+};
+
+/* scheduling policies, scheduling.py:41 POLICIES */
+enum hs_policy_kind { HS_POLICY_OS = 0, HS_POLICY_RR = 1, HS_POLICY_WRR = 2, HS_POLICY_SI = 3, HS_POLICY_MB = 4 };
+
+/* Per-trace outcome of a replay: the exception run_continuous would raise. */
+enum hs_trace_error {
+  HS_TRACE_OK = 0,
+  HS_TRACE_INFEASIBLE_REQUEST = 1, /* simulator.py:304-309 admit()                 */
+  HS_TRACE_NONPOSITIVE_COST = 2,   /* scheduling.py:143-146 per_request_cost SpecError */
+  HS_TRACE_EXP_OVERFLOW = 3,       /* scheduling.py:154 math.exp OverflowError      */
+  HS_TRACE_NO_INSTANCE = 4,        /* scheduling.py:310-311 SchedulingError         */
+  HS_TRACE_NEGATIVE_RUNNING = 5,   /* capacity.py:50-52 SpecError                   */
+  HS_TRACE_CAPACITY = 6            /* engine limit: active-set bound exceeded        */
+};
+
+/* core.py:45-56 ModelSpec */
+typedef struct {
+  int64_t layers, hidden_dim, param_count, bytes_per_param;
+} hs_model;
+
+/* core.py:75-88 EngineOverheads */
+typedef struct {
+  double mem_utilization_fraction;
+  int64_t static_overhead_bytes;
+} hs_engine;
+
+/* core.py:91-100 WorkloadLimits */
+typedef struct {
+  int64_t max_input_len, max_output_len;
+} hs_limits;
+
+/* core.py:59-72 MachineSpec, plus the index of the machine whose spec
+ * cluster.machine(name) resolves to (core.py:161-165: first machine with that
+ * name; == own index when names are unique).  fixed_degree = 0 enumerates
+ * the machine's degrees (core.py:363-371); > 0 evaluates that one degree
+ * (an explicit DeploymentConfig placement, planner.py:143-181). */
+typedef struct {
+  int64_t accelerator_count;
+  int64_t accelerator_mem_bytes;
+  int32_t spec_index;
+  int32_t fixed_degree;
+} hs_machine;
+
+/* One (machine, degree) table entry = planner.py:167-179 MachineEstimate
+ * plus the failure that replaces it. */
+typedef struct {
+  double contribution;   /* machine_tokens_per_sec = rate * instance_count */
+  double rate;           /* instance_tokens_per_sec                      */
+  double budget;         /* KV budget bytes (may be <= 0)                */
+  double slack;          /* budget - required bytes                      */
+  int64_t instance_count;
+  int64_t bad_request;   /* request index for HS_ENTRY_INFEASIBLE_REQUEST */
+  int64_t token_count;   /* sum(I + O) over the trace                      */
+  int32_t tp_degree;
+  int32_t status;        /* hs_entry_status */
+  int32_t zero_div_int;  /* 1 when total_time was the int 0 (empty plan)   */
+  int32_t _pad;
+} hs_entry;
+
+/* One candidate: (total, mixed-radix index; machine 0 most significant). */
+typedef struct {
+  double total;
+  int64_t index;
+} hs_cand;
+
+/* Schedulable instance (scheduling.py:44-52 InstanceHandle). */
+typedef struct {
+  double p[8];           /* LatencyParams p1..p8 (latency.py:36-51)         */
+  double budget;         /* KvBudget.total_bytes (> 0)                       */
+  double wrr_weight;     /* PolicyConfig.wrr_weights[i] (WRR only)           */
+  int32_t type;          /* class id: instances with bit-identical (p, budget)
+                            share one; 0 <= type < n_instances              */
+  int32_t _pad;
+} hs_instance;
+
+/* scheduling.py:98-116 PolicyConfig (predictor is applied host-side: the
+ * engine consumes the predicted lengths as an array). */
+typedef struct {
+  int32_t policy;        /* hs_policy_kind */
+  int32_t n_instances;
+  double theta;
+  int64_t per_token;     /* capacity.py:67-69 kv_bytes_per_token */
+} hs_policy;
+
+/* simulator.py:82-88 InstanceMetrics + scheduler.loads() residual. */
+typedef struct {
+  double completion_time;
+  double peak_kv_usage;
+  double residual_load;
+  int64_t request_count;
+  int64_t token_count;
+} hs_inst_metrics;
+
+typedef struct {
+  int32_t error;         /* hs_trace_error */
+  int32_t err_instance;  /* instance index involved (or -1) */
+  int64_t err_request;   /* request index within the trace (or -1) */
+  double err_value;      /* offending value (e.g. non-positive batch time) */
+  int64_t n_steps;       /* step events executed (statistics) */
+} hs_trace_result;
+
+/* A batch of traces laid out back to back (SoA).  Trace t owns requests
+ * [offsets[t], offsets[t+1]).  arrival == NULL means rate = inf (all 0.0,
+ * simulator.py:117-118). */
+typedef struct {
+  int64_t n_traces;
+  const int64_t* offsets;
+  const int32_t* input_len;
+  const int32_t* output_len;
+  const int32_t* pred_output_len;
+  const double* arrival;
+} hs_trace_batch;
+
+typedef struct hs_ctx hs_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+int hs_abi_version(void);
+int hs_ctx_create(int device, hs_ctx** out);
+int hs_ctx_destroy(hs_ctx* ctx);
+const char* hs_last_error(void);
+/* Kernel launches issued by this context since creation (evidence counter). */
+int64_t hs_ctx_launch_count(const hs_ctx* ctx);
+/* Device milliseconds of the last call's kernels (CUDA events on the
+ * context's stream, excluding host<->device copies). */
+double hs_ctx_last_kernel_ms(const hs_ctx* ctx);
+
+/* ---- deployment search ------------------------------------------------ */
+/* Fill table[i * HS_MAX_DEGREES + d] for d < n_degrees[i] (degree list =
+ * core.py:363-371 enumerate_tp_degrees of machines[i]).  params is
+ * [M][HS_MAX_DEGREES][8] and params_present [M][HS_MAX_DEGREES], indexed by
+ * the same degree position.  I/O are the trace's input/output lengths. */
+int hs_search_tables(hs_ctx* ctx, const hs_model* model, const hs_engine* engine,
+                     const hs_limits* limits, const hs_machine* machines, int32_t n_machines,
+                     const double* params, const uint8_t* params_present,
+                     const int32_t* input_len, const int32_t* output_len, int64_t n_requests,
+                     hs_entry* table, int32_t* n_degrees);
+
+/* Exhaustive argmax over candidate indices [begin, end) of the product
+ * space defined by (table, n_degrees): best = max total, ties -> lowest
+ * index (planner.py:227).  *n_feasible receives the number of feasible
+ * candidates in the range.  best->index = -1 when none is feasible. */
+int hs_search_best(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees, int32_t n_machines,
+                   int64_t begin, int64_t end, hs_cand* best, int64_t* n_feasible);
+
+/* Rank every candidate of the space (size <= 2^26): feasible ones into
+ * ranked[0 .. *n_ranked) ordered by (-total, index); for every candidate,
+ * first_bad[c] = index of the first machine (config order) whose entry is
+ * not OK, or -1 when feasible. */
+int hs_search_rank(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees, int32_t n_machines,
+                   hs_cand* ranked, int64_t* n_ranked, int8_t* first_bad);
+
+/* ---- batched scheduler replay ------------------------------------------ */
+/* Replay every trace of the batch on the same instance set.  assign
+ * ([total requests], may be NULL) receives the chosen instance per request;
+ * depart ([total requests], may be NULL) the departure time; metrics is
+ * [n_traces][n_instances]; result is [n_traces]. */
+int hs_replay(hs_ctx* ctx, const hs_instance* instances, const hs_policy* policy,
+              const hs_trace_batch* batch, uint8_t* assign, double* depart,
+              hs_inst_metrics* metrics, hs_trace_result* result);
+
+/* Device-resident variant for throughput measurement: every pointer in
+ * batch / assign / depart / metrics / result is a DEVICE pointer (allocated
+ * with hs_device_alloc); instances and policy are host structs. */
+int hs_replay_device(hs_ctx* ctx, const hs_instance* instances, const hs_policy* policy,
+                     const hs_trace_batch* batch, uint8_t* assign, double* depart,
+                     hs_inst_metrics* metrics, hs_trace_result* result);
+
+/* Device buffers for hs_replay_device. */
+int hs_device_alloc(hs_ctx* ctx, int64_t bytes, void** out);
+int hs_device_free(hs_ctx* ctx, void* ptr);
+int hs_memcpy_h2d(hs_ctx* ctx, void* dst, const void* src, int64_t bytes);
+int hs_memcpy_d2h(hs_ctx* ctx, void* dst, const void* src, int64_t bytes);
+int hs_device_synchronize(hs_ctx* ctx);
+/* Page-locked host buffers (for end-to-end transfers at full PCIe rate). */
+int hs_host_alloc(hs_ctx* ctx, int64_t bytes, void** out);
+int hs_host_free(hs_ctx* ctx, void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETSERVE_B200_H */

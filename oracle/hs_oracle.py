@@ -1,0 +1,141 @@
+"""ctypes binding of oracle/build/libhs_oracle.so -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+--impl reference) may import this module.  See hs_oracle.h.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import pathlib
+import subprocess
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+LIB = HERE / "build" / "libhs_oracle.so"
+
+
+def build() -> pathlib.Path:
+    gcc = "/usr/bin/gcc" if pathlib.Path("/usr/bin/gcc").exists() else "gcc"
+    subprocess.run(["make", "-s", "-C", str(HERE), f"CC={gcc}"], check=True)
+    return LIB
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            build()
+        L = C.CDLL(str(LIB))
+        vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.hs_oracle_exp.argtypes = [dbl, C.POINTER(C.c_int)]
+        L.hs_oracle_exp.restype = dbl
+        L.hs_oracle_floordiv.argtypes = [dbl, dbl]
+        L.hs_oracle_floordiv.restype = dbl
+        L.hs_oracle_pysum.argtypes = [vp, i64]
+        L.hs_oracle_pysum.restype = dbl
+        L.hs_oracle_tables.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, vp]
+        L.hs_oracle_tables.restype = C.c_int
+        L.hs_oracle_candidate_literal.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, i64,
+                                                  C.POINTER(i32), C.POINTER(i32)]
+        L.hs_oracle_candidate_literal.restype = dbl
+        L.hs_oracle_best.argtypes = [vp, vp, i32, i64, i64, C.c_int, vp, vp]
+        L.hs_oracle_best.restype = C.c_int
+        L.hs_oracle_rank.argtypes = [vp, vp, i32, vp, vp, vp]
+        L.hs_oracle_rank.restype = C.c_int
+        L.hs_oracle_replay.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, vp]
+        L.hs_oracle_replay.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def exp(x: float):
+    of = C.c_int()
+    y = lib().hs_oracle_exp(float(x), C.byref(of))
+    return y, bool(of.value)
+
+
+def floordiv(a: float, b: float) -> float:
+    return lib().hs_oracle_floordiv(float(a), float(b))
+
+
+def pysum(xs) -> float:
+    a = np.ascontiguousarray(xs, np.float64)
+    return lib().hs_oracle_pysum(_p(a), len(a))
+
+
+def tables(model, engine, limits, machines, params, present, I, O):
+    """Same layout as hs_search_tables; structs from paper_2504_15303_b200._native."""
+    from paper_2504_15303_b200 import _native as nat
+    M = len(machines)
+    table = np.zeros(M * nat.HS_MAX_DEGREES, nat.ENTRY_DTYPE)
+    nd = np.zeros(M, np.int32)
+    I = np.ascontiguousarray(I, np.int32)
+    O = np.ascontiguousarray(O, np.int32)
+    rc = lib().hs_oracle_tables(C.byref(model), C.byref(engine), C.byref(limits), C.cast(machines, C.c_void_p), M,
+                                _p(params), _p(present), _p(I), _p(O), len(I), _p(table), _p(nd))
+    assert rc == 0
+    return table.reshape(M, nat.HS_MAX_DEGREES), nd
+
+
+def candidate_literal(model, engine, limits, machines, params, present, I, O, index: int):
+    fb, st = C.c_int32(), C.c_int32()
+    I = np.ascontiguousarray(I, np.int32)
+    O = np.ascontiguousarray(O, np.int32)
+    t = lib().hs_oracle_candidate_literal(C.byref(model), C.byref(engine), C.byref(limits),
+                                          C.cast(machines, C.c_void_p), len(machines), _p(params), _p(present),
+                                          _p(I), _p(O), len(I), int(index), C.byref(fb), C.byref(st))
+    return t, fb.value, st.value
+
+
+def best(table, nd, begin, end, nthreads=1):
+    from paper_2504_15303_b200 import _native as nat
+    out = np.zeros(1, nat.CAND_DTYPE)
+    nf = np.zeros(1, np.int64)
+    t = np.ascontiguousarray(table.reshape(-1))
+    rc = lib().hs_oracle_best(_p(t), _p(np.ascontiguousarray(nd, np.int32)), len(nd), int(begin), int(end),
+                              int(nthreads), _p(out), _p(nf))
+    assert rc == 0
+    return float(out["total"][0]), int(out["index"][0]), int(nf[0])
+
+
+def rank(table, nd):
+    from paper_2504_15303_b200 import _native as nat
+    P = int(np.prod(np.asarray(nd, np.int64)))
+    ranked = np.zeros(max(P, 1), nat.CAND_DTYPE)
+    fb = np.zeros(max(P, 1), np.int8)
+    n = np.zeros(1, np.int64)
+    t = np.ascontiguousarray(table.reshape(-1))
+    rc = lib().hs_oracle_rank(_p(t), _p(np.ascontiguousarray(nd, np.int32)), len(nd), _p(ranked), _p(n), _p(fb))
+    assert rc == 0
+    return ranked[: n[0]], fb[:P]
+
+
+def replay(instances, policy, offsets, I, O, P, arrival=None, nthreads=1, want_depart=True):
+    from paper_2504_15303_b200 import _native as nat
+    T = len(offsets) - 1
+    N = policy.n_instances
+    total = int(offsets[-1])
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    I = np.ascontiguousarray(I, np.int32)
+    O = np.ascontiguousarray(O, np.int32)
+    P = np.ascontiguousarray(P, np.int32)
+    arrival = None if arrival is None else np.ascontiguousarray(arrival, np.float64)
+    batch = nat.hs_trace_batch(T, offsets.ctypes.data, I.ctypes.data, O.ctypes.data, P.ctypes.data,
+                               None if arrival is None else arrival.ctypes.data)
+    assign = np.zeros(max(total, 1), np.uint8)
+    depart = np.zeros(max(total, 1), np.float64) if want_depart else None
+    metrics = np.zeros(max(T * N, 1), nat.METRICS_DTYPE)
+    result = np.zeros(max(T, 1), nat.RESULT_DTYPE)
+    rc = lib().hs_oracle_replay(C.cast(instances, C.c_void_p), C.byref(policy), C.byref(batch), int(nthreads),
+                                _p(assign), _p(depart), _p(metrics), _p(result))
+    assert rc == 0
+    return assign[:total], (None if depart is None else depart[:total]), metrics[: T * N].reshape(T, N), result[:T]

@@ -1,0 +1,272 @@
+"""ctypes binding of libhetserve_b200.so (include/hetserve_b200.h).
+
+The engine has no CPU fallback: if the library cannot be loaded, or no CUDA
+device is present, every call raises EngineUnavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+import threading
+
+import numpy as np
+
+HS_MAX_DEGREES = 32
+HS_MAX_MACHINES = 64
+HS_MAX_INSTANCES = 32
+
+# enums (hetserve_b200.h)
+HS_OK, HS_ERR_ARG, HS_ERR_CUDA, HS_ERR_UNSUPPORTED, HS_ERR_NOMEM = 0, 1, 2, 3, 4
+ENTRY_OK, ENTRY_INFEASIBLE_CONFIG, ENTRY_MISSING_PARAMS, ENTRY_INFEASIBLE_REQUEST, ENTRY_ZERO_DIVISION, \
+    ENTRY_BAD_DEGREE = range(6)
+POLICY_CODE = {"OS": 0, "RR": 1, "WRR": 2, "SI": 3, "MB": 4}
+TRACE_OK, TRACE_INFEASIBLE_REQUEST, TRACE_NONPOSITIVE_COST, TRACE_EXP_OVERFLOW, TRACE_NO_INSTANCE, \
+    TRACE_NEGATIVE_RUNNING, TRACE_CAPACITY = range(7)
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "libhetserve_b200.so"
+
+
+class EngineUnavailable(RuntimeError):
+    """The CUDA engine cannot run here (library missing or no GPU)."""
+
+
+class EngineError(RuntimeError):
+    """A call into the engine failed (CUDA error, unsupported input, ...)."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[hs status {code}] {message}")
+        self.code = code
+
+
+class hs_model(C.Structure):
+    _fields_ = [("layers", C.c_int64), ("hidden_dim", C.c_int64), ("param_count", C.c_int64),
+                ("bytes_per_param", C.c_int64)]
+
+
+class hs_engine(C.Structure):
+    _fields_ = [("mem_utilization_fraction", C.c_double), ("static_overhead_bytes", C.c_int64)]
+
+
+class hs_limits(C.Structure):
+    _fields_ = [("max_input_len", C.c_int64), ("max_output_len", C.c_int64)]
+
+
+class hs_machine(C.Structure):
+    _fields_ = [("accelerator_count", C.c_int64), ("accelerator_mem_bytes", C.c_int64), ("spec_index", C.c_int32),
+                ("fixed_degree", C.c_int32)]
+
+
+class hs_entry(C.Structure):
+    _fields_ = [("contribution", C.c_double), ("rate", C.c_double), ("budget", C.c_double), ("slack", C.c_double),
+                ("instance_count", C.c_int64), ("bad_request", C.c_int64), ("token_count", C.c_int64),
+                ("tp_degree", C.c_int32), ("status", C.c_int32), ("zero_div_int", C.c_int32), ("_pad", C.c_int32)]
+
+
+class hs_cand(C.Structure):
+    _fields_ = [("total", C.c_double), ("index", C.c_int64)]
+
+
+class hs_instance(C.Structure):
+    _fields_ = [("p", C.c_double * 8), ("budget", C.c_double), ("wrr_weight", C.c_double), ("type", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class hs_policy(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("n_instances", C.c_int32), ("theta", C.c_double), ("per_token", C.c_int64)]
+
+
+class hs_inst_metrics(C.Structure):
+    _fields_ = [("completion_time", C.c_double), ("peak_kv_usage", C.c_double), ("residual_load", C.c_double),
+                ("request_count", C.c_int64), ("token_count", C.c_int64)]
+
+
+class hs_trace_result(C.Structure):
+    _fields_ = [("error", C.c_int32), ("err_instance", C.c_int32), ("err_request", C.c_int64),
+                ("err_value", C.c_double), ("n_steps", C.c_int64)]
+
+
+class hs_trace_batch(C.Structure):
+    _fields_ = [("n_traces", C.c_int64), ("offsets", C.c_void_p), ("input_len", C.c_void_p),
+                ("output_len", C.c_void_p), ("pred_output_len", C.c_void_p), ("arrival", C.c_void_p)]
+
+
+# numpy views of the structs (same layout) for bulk results
+ENTRY_DTYPE = np.dtype([("contribution", "<f8"), ("rate", "<f8"), ("budget", "<f8"), ("slack", "<f8"),
+                        ("instance_count", "<i8"), ("bad_request", "<i8"), ("token_count", "<i8"),
+                        ("tp_degree", "<i4"), ("status", "<i4"), ("zero_div_int", "<i4"), ("_pad", "<i4")])
+CAND_DTYPE = np.dtype([("total", "<f8"), ("index", "<i8")])
+METRICS_DTYPE = np.dtype([("completion_time", "<f8"), ("peak_kv_usage", "<f8"), ("residual_load", "<f8"),
+                          ("request_count", "<i8"), ("token_count", "<i8")])
+RESULT_DTYPE = np.dtype([("error", "<i4"), ("err_instance", "<i4"), ("err_request", "<i8"), ("err_value", "<f8"),
+                         ("n_steps", "<i8")])
+
+# every symbol include/hetserve_b200.h declares
+EXPORTS = (
+    "hs_abi_version", "hs_ctx_create", "hs_ctx_destroy", "hs_last_error", "hs_ctx_launch_count",
+    "hs_ctx_last_kernel_ms", "hs_search_tables", "hs_search_best", "hs_search_rank", "hs_replay",
+    "hs_replay_device", "hs_device_alloc", "hs_device_free", "hs_memcpy_h2d", "hs_memcpy_d2h",
+    "hs_device_synchronize", "hs_host_alloc", "hs_host_free",
+)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
+    """Load the engine library (no GPU needed to load it)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = pathlib.Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise EngineUnavailable(f"{p} is missing: run `python -m paper_2504_15303_b200.build`")
+        lib = C.CDLL(str(p))
+        vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        sig = {
+            "hs_abi_version": ([], C.c_int),
+            "hs_ctx_create": ([C.c_int, C.POINTER(vp)], C.c_int),
+            "hs_ctx_destroy": ([vp], C.c_int),
+            "hs_last_error": ([], C.c_char_p),
+            "hs_ctx_launch_count": ([vp], i64),
+            "hs_ctx_last_kernel_ms": ([vp], dbl),
+            "hs_search_tables": ([vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, vp], C.c_int),
+            "hs_search_best": ([vp, vp, vp, i32, i64, i64, vp, vp], C.c_int),
+            "hs_search_rank": ([vp, vp, vp, i32, vp, vp, vp], C.c_int),
+            "hs_replay": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+            "hs_replay_device": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+            "hs_device_alloc": ([vp, i64, C.POINTER(vp)], C.c_int),
+            "hs_device_free": ([vp, vp], C.c_int),
+            "hs_memcpy_h2d": ([vp, vp, vp, i64], C.c_int),
+            "hs_memcpy_d2h": ([vp, vp, vp, i64], C.c_int),
+            "hs_device_synchronize": ([vp], C.c_int),
+            "hs_host_alloc": ([vp, i64, C.POINTER(vp)], C.c_int),
+            "hs_host_free": ([vp, vp], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Engine:
+    """One engine context (device, stream, device buffers).  Not thread-safe:
+    use one Engine per thread (engine_for() keeps one per (thread, device))."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        rc = self.lib.hs_ctx_create(int(device), C.byref(h))
+        if rc != HS_OK:
+            raise EngineUnavailable(f"hs_ctx_create(device={device}) failed: {self._err()}")
+        self.handle = h
+        self.device = device
+
+    def _err(self) -> str:
+        msg = self.lib.hs_last_error()
+        return msg.decode() if msg else ""
+
+    def check(self, rc: int, what: str) -> None:
+        if rc != HS_OK:
+            raise EngineError(rc, f"{what}: {self._err()}")
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.hs_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.hs_ctx_launch_count(self.handle))
+
+    @property
+    def last_kernel_ms(self) -> float:
+        return float(self.lib.hs_ctx_last_kernel_ms(self.handle))
+
+    # ---------------------------------------------------------------- search
+    def search_tables(self, model: hs_model, engine: hs_engine, limits: hs_limits, machines: np.ndarray,
+                      params: np.ndarray, present: np.ndarray, I: np.ndarray, O: np.ndarray):
+        M = len(machines)
+        table = np.zeros(M * HS_MAX_DEGREES, dtype=ENTRY_DTYPE)
+        nd = np.zeros(M, dtype=np.int32)
+        I = np.ascontiguousarray(I, dtype=np.int32)
+        O = np.ascontiguousarray(O, dtype=np.int32)
+        rc = self.lib.hs_search_tables(self.handle, C.byref(model), C.byref(engine), C.byref(limits),
+                                       machines.ctypes.data_as(C.c_void_p), M, _ptr(params), _ptr(present), _ptr(I),
+                                       _ptr(O), len(I), _ptr(table), _ptr(nd))
+        self.check(rc, "hs_search_tables")
+        return table.reshape(M, HS_MAX_DEGREES), nd
+
+    def search_best(self, table: np.ndarray, nd: np.ndarray, begin: int, end: int):
+        best = hs_cand()
+        nfeas = C.c_int64()
+        t = np.ascontiguousarray(table.reshape(-1))
+        rc = self.lib.hs_search_best(self.handle, _ptr(t), _ptr(np.ascontiguousarray(nd, np.int32)), len(nd),
+                                     int(begin), int(end), C.byref(best), C.byref(nfeas))
+        self.check(rc, "hs_search_best")
+        return float(best.total), int(best.index), int(nfeas.value)
+
+    def search_rank(self, table: np.ndarray, nd: np.ndarray):
+        P = int(np.prod(nd.astype(np.int64)))
+        ranked = np.zeros(max(P, 1), dtype=CAND_DTYPE)
+        first_bad = np.zeros(max(P, 1), dtype=np.int8)
+        n = C.c_int64()
+        t = np.ascontiguousarray(table.reshape(-1))
+        rc = self.lib.hs_search_rank(self.handle, _ptr(t), _ptr(np.ascontiguousarray(nd, np.int32)), len(nd),
+                                     _ptr(ranked), C.byref(n), _ptr(first_bad))
+        self.check(rc, "hs_search_rank")
+        return ranked[: n.value], first_bad[:P]
+
+    # ---------------------------------------------------------------- replay
+    def replay(self, instances, policy: hs_policy, offsets: np.ndarray, I: np.ndarray, O: np.ndarray,
+               P: np.ndarray, arrival: np.ndarray | None, want_assign: bool = True, want_depart: bool = True):
+        T = len(offsets) - 1
+        N = policy.n_instances
+        total = int(offsets[-1])
+        batch = hs_trace_batch(T, offsets.ctypes.data, I.ctypes.data, O.ctypes.data, P.ctypes.data,
+                               None if arrival is None else arrival.ctypes.data)
+        assign = np.zeros(max(total, 1), np.uint8) if want_assign else None
+        depart = np.zeros(max(total, 1), np.float64) if want_depart else None
+        metrics = np.zeros(max(T * N, 1), METRICS_DTYPE)
+        result = np.zeros(max(T, 1), RESULT_DTYPE)
+        rc = self.lib.hs_replay(self.handle, C.cast(instances, C.c_void_p), C.byref(policy), C.byref(batch),
+                                _ptr(assign), _ptr(depart), _ptr(metrics), _ptr(result))
+        self.check(rc, "hs_replay")
+        return (None if assign is None else assign[:total], None if depart is None else depart[:total],
+                metrics[: T * N].reshape(T, N), result[:T])
+
+
+_engines: dict = {}
+_engines_lock = threading.Lock()
+
+
+def default_device() -> int:
+    env = os.environ.get("HS_DEVICE", os.environ.get("LOCAL_RANK"))
+    return int(env) if env else 0
+
+
+def engine_for(device: int | None = None) -> Engine:
+    """The calling thread's engine on `device` (created on first use)."""
+    dev = default_device() if device is None else device
+    key = (threading.get_ident(), dev)
+    with _engines_lock:
+        eng = _engines.get(key)
+        if eng is None:
+            eng = Engine(dev)
+            _engines[key] = eng
+        return eng

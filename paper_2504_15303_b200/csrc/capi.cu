@@ -1,0 +1,590 @@
+// capi.cu -- the C ABI (include/hetserve_b200.h): context, device memory,
+// argument validation, and the host side of each entry point.  No torch
+// types cross this boundary; the Python shim binds it with ctypes.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "hs_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define HS_CUDA(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(HS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+enum Slot {
+  S_I, S_O, S_P, S_T, S_OFF, S_DESC, S_TABLE, S_BLK_BEST, S_BLK_IDX, S_BLK_CNT, S_CAND, S_CNT,
+  S_TOTAL, S_FIRSTBAD, S_FLAG, S_SELIDX, S_NSEL, S_KEYS, S_KEYS2, S_IDX2, S_CUBTMP, S_RANKED,
+  S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_QNEXT, S_HEAP, S_MINNEED, N_SLOTS
+};
+
+}  // namespace
+
+struct hs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches = 0;
+  double last_ms = 0.0;
+  void* buf[N_SLOTS] = {};
+  size_t cap[N_SLOTS] = {};
+};
+
+namespace hs {
+int sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+}  // namespace hs
+
+namespace {
+
+int ensure(hs_ctx* c, int slot, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (c->cap[slot] < bytes) {
+    if (c->buf[slot]) cudaFree(c->buf[slot]);
+    c->buf[slot] = nullptr;
+    c->cap[slot] = 0;
+    size_t want = bytes + bytes / 8;
+    cudaError_t e = cudaMalloc(&c->buf[slot], want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HS_ERR_NOMEM, std::string("cudaMalloc(") + std::to_string(want) + "): " + cudaGetErrorString(e));
+    }
+    c->cap[slot] = want;
+  }
+  *out = c->buf[slot];
+  return HS_OK;
+}
+
+template <typename T>
+int ensure_t(hs_ctx* c, int slot, size_t count, T** out) {
+  void* p = nullptr;
+  int rc = ensure(c, slot, count * sizeof(T), &p);
+  *out = static_cast<T*>(p);
+  return rc;
+}
+
+int use_device(hs_ctx* c) {
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(HS_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return HS_OK;
+}
+
+int begin_timing(hs_ctx* c) {
+  HS_CUDA(cudaEventRecord(c->ev0, c->stream));
+  return HS_OK;
+}
+int end_timing(hs_ctx* c) {
+  HS_CUDA(cudaEventRecord(c->ev1, c->stream));
+  HS_CUDA(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  HS_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->last_ms = ms;
+  return HS_OK;
+}
+
+// core.py:363-371 enumerate_tp_degrees
+int degrees_of(int64_t count, int32_t* out) {
+  int n = 0;
+  for (int64_t t = 1; t <= count && n < HS_MAX_DEGREES; t *= 2)
+    if (count % t == 0) out[n++] = (int32_t)t;
+  return n;
+}
+
+// Build the K2 product-space description from a table.
+int build_space(const hs_entry* table, const int32_t* nd, int32_t M, hs::SpaceDesc* sd, int32_t* m_off,
+                int64_t* P) {
+  if (M < 1 || M > HS_MAX_MACHINES) return fail(HS_ERR_ARG, "n_machines out of range");
+  std::memset(sd, 0, sizeof(*sd));
+  int off = M == 1 ? 1 : 0;
+  sd->M = M + off;
+  if (off) {
+    sd->D[0] = 1;
+    sd->okcnt[0] = 1;
+    sd->C[0] = 0.0;
+  }
+  long double size = 1;
+  double abs_sum = 0.0;
+  int64_t p = 1;
+  for (int32_t i = 0; i < M; ++i) {
+    if (nd[i] < 1 || nd[i] > HS_MAX_DEGREES) return fail(HS_ERR_ARG, "n_degrees out of range");
+    sd->D[i + off] = nd[i];
+    size *= nd[i];
+    if (size > 4.6e18L) return fail(HS_ERR_ARG, "candidate space exceeds 2^62");
+    p *= nd[i];
+    double mx = 0.0;
+    int64_t ok = 0;
+    for (int32_t d = 0; d < nd[i]; ++d) {
+      const hs_entry& e = table[i * HS_MAX_DEGREES + d];
+      double v = -INFINITY;
+      if (e.status == HS_ENTRY_OK) {
+        v = e.contribution;
+        if (std::isnan(v) || v == -INFINITY)
+          return fail(HS_ERR_UNSUPPORTED, "a feasible contribution is NaN or -inf");
+        if (std::isfinite(v) && std::fabs(v) > mx) mx = std::fabs(v);
+        ++ok;
+      }
+      sd->C[(i + off) * HS_MAX_DEGREES + d] = v;
+    }
+    sd->okcnt[i + off] = ok;
+    abs_sum += mx;
+  }
+  if (!(abs_sum < 1e300)) return fail(HS_ERR_UNSUPPORTED, "contributions large enough to overflow a total");
+  *m_off = off;
+  *P = p;
+  return HS_OK;
+}
+
+// Python sum() semantics for the WRR total (scheduling.py:326)
+double pysum(const double* x, int n) {
+  double f = 0.0, c = 0.0;
+  for (int i = 0; i < n; ++i) {
+    if (i == 0) {
+      f = 0.0 + x[0];
+      continue;
+    }
+    double t = f + x[i];
+    if (std::fabs(f) >= std::fabs(x[i])) c += (f - t) + x[i];
+    else c += (x[i] - t) + f;
+    f = t;
+  }
+  if (c != 0.0 && std::isfinite(c)) f += c;
+  return f;
+}
+
+__global__ void k_orderable_keys(const double* total, const int64_t* sel, const int64_t* nsel, uint64_t* keys) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= *nsel) return;
+  double x = -total[sel[k]];
+  if (x == 0.0) x = 0.0;  // -0.0 and 0.0 tie in Python's sort
+  uint64_t u = (uint64_t)__double_as_longlong(x);
+  keys[k] = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__global__ void k_gather_ranked(const double* total, const int64_t* idx, const int64_t* nsel, hs_cand* out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= *nsel) return;
+  out[k].total = total[idx[k]];
+  out[k].index = idx[k];
+}
+
+int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_t T, const int64_t* d_off,
+                const int64_t* h_off, const int32_t* d_I, const int32_t* d_O, const int32_t* d_P, const double* d_arr,
+                uint8_t* d_assign, double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result) {
+  const int N = pol->n_instances;
+  if (N < 1) return fail(HS_ERR_ARG, "n_instances must be >= 1");
+  if (N > HS_MAX_INSTANCES)
+    return fail(HS_ERR_UNSUPPORTED, "more than 32 instances per deployment is not supported yet");
+  if (pol->policy < HS_POLICY_OS || pol->policy > HS_POLICY_MB) return fail(HS_ERR_ARG, "unknown policy");
+  if (pol->per_token <= 0) return fail(HS_ERR_ARG, "per_token must be positive");
+  hs::ReplayConst rc;
+  std::memset(&rc, 0, sizeof(rc));
+  rc.N = N;
+  rc.policy = pol->policy;
+  rc.theta = pol->theta;
+  rc.per_token = pol->per_token;
+  rc.has_arrival = d_arr != nullptr;
+  int nt = 0;
+  std::vector<double> wts(N);
+  for (int j = 0; j < N; ++j) {
+    const int ty = inst[j].type;
+    if (ty < 0 || ty >= N) return fail(HS_ERR_ARG, "instance type out of range");
+    if (!(inst[j].budget > 0)) return fail(HS_ERR_ARG, "instance budget must be positive");
+    rc.inst_type[j] = ty;
+    if (ty >= nt) {
+      for (int k = nt; k <= ty; ++k) rc.type_budget[k] = 0.0;
+      nt = ty + 1;
+    }
+    std::memcpy(rc.type_p[ty], inst[j].p, sizeof(double) * 8);
+    rc.type_budget[ty] = inst[j].budget;
+    rc.wrr_weight[j] = inst[j].wrr_weight;
+    wts[j] = inst[j].wrr_weight;
+  }
+  rc.n_types = nt;
+  rc.wrr_total = pysum(wts.data(), N);
+  const int64_t total_q = h_off[T] - h_off[0];
+  int64_t max_q = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    const int64_t qt = h_off[t + 1] - h_off[t];
+    if (qt < 0) return fail(HS_ERR_ARG, "offsets must be non-decreasing");
+    if (qt > INT32_MAX) return fail(HS_ERR_UNSUPPORTED, "trace longer than 2^31 requests");
+    if (qt > max_q) max_q = qt;
+  }
+  // active-set bound per instance: per_token * sum(I+O) <= budget
+  int32_t* d_min = nullptr;
+  int rcode;
+  if ((rcode = ensure_t(c, S_MINNEED, 1, &d_min))) return rcode;
+  HS_CUDA(cudaMemsetAsync(d_min, 0x7f, sizeof(int32_t), c->stream));
+  if (total_q > 0) {
+    HS_CUDA(hs::launch_min_need(d_I + h_off[0], d_O + h_off[0], total_q, d_min, c->stream));
+    c->launches += 1;
+  }
+  int32_t min_need = 0;
+  HS_CUDA(cudaMemcpyAsync(&min_need, d_min, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  if (min_need < 1) min_need = 1;
+  int64_t acc = 0;
+  for (int j = 0; j < N; ++j) {
+    const double tokens = std::floor(inst[j].budget / (double)pol->per_token);
+    double capd = std::floor(tokens / (double)min_need) + 1.0;
+    int64_t capj = capd > (double)max_q ? max_q : (int64_t)capd;
+    if (capj < 1) capj = 1;
+    rc.heap_off[j] = acc;
+    acc += capj;
+  }
+  rc.heap_off[N] = acc;
+  rc.heap_stride = (acc + 15) / 16 * 16;
+
+  double* d_wrec;
+  int32_t* d_qnext;
+  if ((rcode = ensure_t(c, S_WREC, (size_t)(h_off[T] > 0 ? h_off[T] : 1), &d_wrec))) return rcode;
+  if ((rcode = ensure_t(c, S_QNEXT, (size_t)(h_off[T] > 0 ? h_off[T] : 1), &d_qnext))) return rcode;
+  // heap region, chunked over traces to bound memory
+  size_t free_b = 0, tot_b = 0;
+  HS_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+  const size_t per_trace = (size_t)rc.heap_stride * sizeof(uint64_t);
+  size_t budget_b = (size_t)((double)(free_b + c->cap[S_HEAP]) * 0.6);
+  int64_t chunk = per_trace ? (int64_t)(budget_b / per_trace) : T;
+  if (chunk < 1) chunk = 1;
+  if (chunk > T) chunk = T;
+  if (chunk > 16384) chunk = 16384;
+  uint64_t* d_heap = nullptr;
+  if ((rcode = ensure_t(c, S_HEAP, (size_t)(chunk > 0 ? chunk : 1) * rc.heap_stride, &d_heap))) return rcode;
+  for (int64_t t0 = 0; t0 < T; t0 += chunk) {
+    const int64_t nt_ = (T - t0) < chunk ? (T - t0) : chunk;
+    HS_CUDA(hs::launch_replay(rc, nt_, d_off + t0, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics + t0 * N,
+                              d_result + t0, d_wrec, d_qnext, d_heap, c->stream));
+    c->launches += 1;
+  }
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hs_abi_version(void) { return HS_ABI_VERSION; }
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+
+int hs_ctx_create(int device, hs_ctx** out) {
+  if (!out) return fail(HS_ERR_ARG, "out is null");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(HS_ERR_CUDA, "no CUDA device available");
+  if (device < 0 || device >= n) return fail(HS_ERR_ARG, "device index out of range");
+  hs_ctx* c = new hs_ctx();
+  c->device = device;
+  if (use_device(c)) {
+    delete c;
+    return HS_ERR_CUDA;
+  }
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    delete c;
+    return fail(HS_ERR_CUDA, "stream/event creation failed");
+  }
+  *out = c;
+  return HS_OK;
+}
+
+int hs_ctx_destroy(hs_ctx* c) {
+  if (!c) return HS_OK;
+  cudaSetDevice(c->device);
+  for (int s = 0; s < N_SLOTS; ++s)
+    if (c->buf[s]) cudaFree(c->buf[s]);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return HS_OK;
+}
+
+int64_t hs_ctx_launch_count(const hs_ctx* c) { return c ? c->launches : 0; }
+double hs_ctx_last_kernel_ms(const hs_ctx* c) { return c ? c->last_ms : 0.0; }
+
+int hs_search_tables(hs_ctx* c, const hs_model* model, const hs_engine* engine, const hs_limits* limits,
+                     const hs_machine* machines, int32_t M, const double* params, const uint8_t* present,
+                     const int32_t* I, const int32_t* O, int64_t q, hs_entry* table, int32_t* n_degrees) {
+  if (!c || !model || !engine || !limits || !machines || !params || !present || !table || !n_degrees)
+    return fail(HS_ERR_ARG, "null argument");
+  if (M < 1 || M > HS_MAX_MACHINES) return fail(HS_ERR_ARG, "n_machines out of range");
+  if (q < 0 || (q > 0 && (!I || !O))) return fail(HS_ERR_ARG, "bad trace arguments");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  std::vector<hs::EntryDesc> desc;
+  std::vector<int> slot;
+  for (int32_t i = 0; i < M; ++i) {
+    const hs_machine& own = machines[i];
+    if (own.spec_index < 0 || own.spec_index >= M) return fail(HS_ERR_ARG, "spec_index out of range");
+    const hs_machine& spec = machines[own.spec_index];
+    int32_t deg[HS_MAX_DEGREES];
+    int nd;
+    if (own.fixed_degree > 0) {
+      deg[0] = own.fixed_degree;
+      nd = 1;
+    } else {
+      nd = degrees_of(own.accelerator_count, deg);
+    }
+    n_degrees[i] = nd;
+    for (int d = 0; d < nd; ++d) {
+      hs::EntryDesc e;
+      std::memcpy(e.p, params + ((size_t)i * HS_MAX_DEGREES + d) * 8, sizeof(double) * 8);
+      e.own_count = own.accelerator_count;
+      e.spec_count = spec.accelerator_count;
+      e.spec_mem = spec.accelerator_mem_bytes;
+      e.tp = deg[d];
+      e.present = present[i * HS_MAX_DEGREES + d] ? 1 : 0;
+      desc.push_back(e);
+      slot.push_back(i * HS_MAX_DEGREES + d);
+    }
+  }
+  hs::SearchConst sc;
+  sc.per_token = 2 * model->layers * model->hidden_dim * model->bytes_per_param;
+  sc.required = sc.per_token * (limits->max_input_len + limits->max_output_len);
+  sc.weights = model->param_count * model->bytes_per_param;
+  sc.static_overhead = engine->static_overhead_bytes;
+  sc.phi = engine->mem_utilization_fraction;
+  sc.q = q;
+  const int n = (int)desc.size();
+  int32_t *dI, *dO;
+  hs::EntryDesc* dD;
+  hs_entry* dT;
+  if ((rc = ensure_t(c, S_I, (size_t)(q > 0 ? q : 1), &dI)) || (rc = ensure_t(c, S_O, (size_t)(q > 0 ? q : 1), &dO)) ||
+      (rc = ensure_t(c, S_DESC, (size_t)n, &dD)) || (rc = ensure_t(c, S_TABLE, (size_t)n, &dT)))
+    return rc;
+  if (q > 0) {
+    HS_CUDA(cudaMemcpyAsync(dI, I, sizeof(int32_t) * q, cudaMemcpyHostToDevice, c->stream));
+    HS_CUDA(cudaMemcpyAsync(dO, O, sizeof(int32_t) * q, cudaMemcpyHostToDevice, c->stream));
+  }
+  HS_CUDA(cudaMemcpyAsync(dD, desc.data(), sizeof(hs::EntryDesc) * n, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = begin_timing(c))) return rc;
+  HS_CUDA(hs::launch_table_build(dD, n, sc, dI, dO, dT, c->stream));
+  c->launches += 1;
+  if ((rc = end_timing(c))) return rc;
+  std::vector<hs_entry> out(n);
+  HS_CUDA(cudaMemcpyAsync(out.data(), dT, sizeof(hs_entry) * n, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < n; ++k) table[slot[k]] = out[k];
+  return HS_OK;
+}
+
+int hs_search_best(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, int32_t M, int64_t begin, int64_t end,
+                   hs_cand* best, int64_t* n_feasible) {
+  if (!c || !table || !n_degrees || !best || !n_feasible) return fail(HS_ERR_ARG, "null argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  hs::SpaceDesc sd;
+  int32_t m_off;
+  int64_t P;
+  if ((rc = build_space(table, n_degrees, M, &sd, &m_off, &P))) return rc;
+  if (begin < 0 || end > P || begin > end) return fail(HS_ERR_ARG, "index range outside the candidate space");
+  const int64_t Din = (int64_t)sd.D[sd.M - 2] * sd.D[sd.M - 1];
+  const int64_t items = (end - begin) / Din + 2;
+  int blocks = hs::sm_count() * 8;
+  const int64_t need_blocks = (items + 255) / 256;
+  if (need_blocks < blocks) blocks = (int)(need_blocks > 0 ? need_blocks : 1);
+  double* bb;
+  int64_t *bi, *bc, *cnt;
+  hs_cand* cand;
+  if ((rc = ensure_t(c, S_BLK_BEST, (size_t)blocks, &bb)) || (rc = ensure_t(c, S_BLK_IDX, (size_t)blocks, &bi)) ||
+      (rc = ensure_t(c, S_BLK_CNT, (size_t)blocks, &bc)) || (rc = ensure_t(c, S_CAND, 1, &cand)) ||
+      (rc = ensure_t(c, S_CNT, 1, &cnt)))
+    return rc;
+  if ((rc = begin_timing(c))) return rc;
+  HS_CUDA(hs::launch_search_best(sd, begin, end, blocks, bb, bi, bc, cand, cnt, c->stream));
+  c->launches += 2;
+  if ((rc = end_timing(c))) return rc;
+  HS_CUDA(cudaMemcpyAsync(best, cand, sizeof(hs_cand), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaMemcpyAsync(n_feasible, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+
+int hs_search_rank(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, int32_t M, hs_cand* ranked,
+                   int64_t* n_ranked, int8_t* first_bad) {
+  if (!c || !table || !n_degrees || !ranked || !n_ranked || !first_bad) return fail(HS_ERR_ARG, "null argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  hs::SpaceDesc sd;
+  int32_t m_off;
+  int64_t P;
+  if ((rc = build_space(table, n_degrees, M, &sd, &m_off, &P))) return rc;
+  if (P > (int64_t(1) << 26)) return fail(HS_ERR_UNSUPPORTED, "space too large to rank in full (use hs_search_best)");
+  double* tot;
+  int8_t* fb;
+  uint8_t* flag;
+  int64_t *sel, *nsel, *idx2;
+  uint64_t *keys, *keys2;
+  hs_cand* out;
+  if ((rc = ensure_t(c, S_TOTAL, (size_t)P, &tot)) || (rc = ensure_t(c, S_FIRSTBAD, (size_t)P, &fb)) ||
+      (rc = ensure_t(c, S_FLAG, (size_t)P, &flag)) || (rc = ensure_t(c, S_SELIDX, (size_t)P, &sel)) ||
+      (rc = ensure_t(c, S_NSEL, 1, &nsel)) || (rc = ensure_t(c, S_KEYS, (size_t)P, &keys)) ||
+      (rc = ensure_t(c, S_KEYS2, (size_t)P, &keys2)) || (rc = ensure_t(c, S_IDX2, (size_t)P, &idx2)) ||
+      (rc = ensure_t(c, S_RANKED, (size_t)P, &out)))
+    return rc;
+  size_t tmp1 = 0, tmp2 = 0;
+  cub::CountingInputIterator<int64_t> counting(0);
+  HS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp1, counting, flag, sel, nsel, P, c->stream));
+  HS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, keys, keys2, sel, idx2, (int)P, 0, 64, c->stream));
+  void* tmp;
+  if ((rc = ensure(c, S_CUBTMP, tmp1 > tmp2 ? tmp1 : tmp2, &tmp))) return rc;
+  size_t tmpn = c->cap[S_CUBTMP];
+  if ((rc = begin_timing(c))) return rc;
+  HS_CUDA(hs::launch_search_score(sd, m_off, P, tot, fb, flag, c->stream));
+  HS_CUDA(cub::DeviceSelect::Flagged(tmp, tmpn, counting, flag, sel, nsel, P, c->stream));
+  const unsigned g = (unsigned)((P + 255) / 256);
+  k_orderable_keys<<<g, 256, 0, c->stream>>>(tot, sel, nsel, keys);
+  HS_CUDA(cudaGetLastError());
+  int64_t h_nsel = 0;
+  HS_CUDA(cudaMemcpyAsync(&h_nsel, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  if (h_nsel > 0) {
+    tmpn = c->cap[S_CUBTMP];
+    HS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmpn, keys, keys2, sel, idx2, (int)h_nsel, 0, 64, c->stream));
+    k_gather_ranked<<<g, 256, 0, c->stream>>>(tot, idx2, nsel, out);
+    HS_CUDA(cudaGetLastError());
+  }
+  c->launches += 5;
+  if ((rc = end_timing(c))) return rc;
+  if (h_nsel > 0)
+    HS_CUDA(cudaMemcpyAsync(ranked, out, sizeof(hs_cand) * h_nsel, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaMemcpyAsync(first_bad, fb, (size_t)P, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  *n_ranked = h_nsel;
+  return HS_OK;
+}
+
+int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b, uint8_t* assign,
+              double* depart, hs_inst_metrics* metrics, hs_trace_result* result) {
+  if (!c || !inst || !pol || !b || !metrics || !result || !b->offsets) return fail(HS_ERR_ARG, "null argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  const int64_t T = b->n_traces;
+  if (T < 0) return fail(HS_ERR_ARG, "n_traces < 0");
+  const int64_t* off = b->offsets;
+  if (off[0] != 0) return fail(HS_ERR_ARG, "offsets[0] must be 0");
+  const int64_t total = off[T];
+  if (total > 0 && (!b->input_len || !b->output_len || !b->pred_output_len)) return fail(HS_ERR_ARG, "null trace");
+  const int N = pol->n_instances;
+  int64_t* dOff;
+  int32_t *dI, *dO, *dP;
+  double* dT = nullptr;
+  uint8_t* dA = nullptr;
+  double* dDep = nullptr;
+  hs_inst_metrics* dM;
+  hs_trace_result* dR;
+  const size_t tq = (size_t)(total > 0 ? total : 1);
+  if ((rc = ensure_t(c, S_OFF, (size_t)T + 1, &dOff)) || (rc = ensure_t(c, S_I, tq, &dI)) ||
+      (rc = ensure_t(c, S_O, tq, &dO)) || (rc = ensure_t(c, S_P, tq, &dP)) ||
+      (rc = ensure_t(c, S_METRICS, (size_t)(T > 0 ? T : 1) * (N > 0 ? N : 1), &dM)) ||
+      (rc = ensure_t(c, S_RESULT, (size_t)(T > 0 ? T : 1), &dR)))
+    return rc;
+  if (b->arrival && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
+  if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
+  if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
+  HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
+  if (total > 0) {
+    HS_CUDA(cudaMemcpyAsync(dI, b->input_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
+    HS_CUDA(cudaMemcpyAsync(dO, b->output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
+    HS_CUDA(cudaMemcpyAsync(dP, b->pred_output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
+    if (dT) HS_CUDA(cudaMemcpyAsync(dT, b->arrival, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
+  }
+  if ((rc = begin_timing(c))) return rc;
+  if ((rc = replay_impl(c, inst, pol, T, dOff, off, dI, dO, dP, dT, dA, dDep, dM, dR))) return rc;
+  if ((rc = end_timing(c))) return rc;
+  if (T > 0) {
+    HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * N, cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
+  if (depart && total > 0)
+    HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+
+int hs_replay_device(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b,
+                     uint8_t* assign, double* depart, hs_inst_metrics* metrics, hs_trace_result* result) {
+  if (!c || !inst || !pol || !b || !metrics || !result || !b->offsets) return fail(HS_ERR_ARG, "null argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  const int64_t T = b->n_traces;
+  if (T < 0) return fail(HS_ERR_ARG, "n_traces < 0");
+  std::vector<int64_t> off((size_t)T + 1);
+  HS_CUDA(cudaMemcpyAsync(off.data(), b->offsets, sizeof(int64_t) * (T + 1), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  if ((rc = begin_timing(c))) return rc;
+  if ((rc = replay_impl(c, inst, pol, T, b->offsets, off.data(), b->input_len, b->output_len, b->pred_output_len,
+                        b->arrival, assign, depart, metrics, result)))
+    return rc;
+  if ((rc = end_timing(c))) return rc;
+  return HS_OK;
+}
+
+int hs_device_alloc(hs_ctx* c, int64_t bytes, void** out) {
+  if (!c || !out || bytes < 0) return fail(HS_ERR_ARG, "bad argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  HS_CUDA(cudaMalloc(out, (size_t)(bytes > 0 ? bytes : 16)));
+  return HS_OK;
+}
+int hs_device_free(hs_ctx* c, void* p) {
+  if (!c) return fail(HS_ERR_ARG, "null ctx");
+  use_device(c);
+  if (p) HS_CUDA(cudaFree(p));
+  return HS_OK;
+}
+int hs_memcpy_h2d(hs_ctx* c, void* dst, const void* src, int64_t bytes) {
+  if (!c) return fail(HS_ERR_ARG, "null ctx");
+  use_device(c);
+  HS_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+int hs_memcpy_d2h(hs_ctx* c, void* dst, const void* src, int64_t bytes) {
+  if (!c) return fail(HS_ERR_ARG, "null ctx");
+  use_device(c);
+  HS_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+int hs_device_synchronize(hs_ctx* c) {
+  if (!c) return fail(HS_ERR_ARG, "null ctx");
+  use_device(c);
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+int hs_host_alloc(hs_ctx* c, int64_t bytes, void** out) {
+  if (!c || !out || bytes < 0) return fail(HS_ERR_ARG, "bad argument");
+  use_device(c);
+  HS_CUDA(cudaHostAlloc(out, (size_t)(bytes > 0 ? bytes : 16), cudaHostAllocPortable));
+  return HS_OK;
+}
+int hs_host_free(hs_ctx* c, void* p) {
+  if (!c) return fail(HS_ERR_ARG, "null ctx");
+  if (p) HS_CUDA(cudaFreeHost(p));
+  return HS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+// hs_device.cuh -- device-side fp64 semantics of the reference (CPython 3.12
+// on glibc 2.39), shared by the search and replay kernels.
+//
+// Everything is evaluated exactly as CPython evaluates the reference
+// expressions: left to right, one rounding per operation (the library is
+// compiled with -fmad=false so nvcc never contracts a*b+c; the only fused
+// operations are the explicit __fma_rn calls of the exp port, which mirror
+// the vfmadd instructions of glibc's FMA exp body).
+#pragma once
+#include <stdint.h>
+
+#include "exp_table.cuh"
+
+namespace hs {
+
+__device__ __forceinline__ double u2d(uint64_t u) { return __longlong_as_double((long long)u); }
+__device__ __forceinline__ uint64_t d2u(double d) { return (uint64_t)__double_as_longlong(d); }
+
+// Python float(int) for |v| < 2^63: correctly rounded (PyLong_AsDouble).
+__device__ __forceinline__ double i2d(int64_t v) { return __ll2double_rn(v); }
+
+// Python `int > float`, exact (Objects/floatobject.c float_richcompare).
+__device__ __forceinline__ bool int_gt_double(int64_t v, double b) {
+  if (b != b) return false;
+  if (b >= 9223372036854775808.0) return false;
+  if (b < -9223372036854775808.0) return true;
+  return v > (int64_t)floor(b);
+}
+
+// Saturating int64 helpers (values are non-negative byte/token counts; a
+// saturated value compares greater than any budget below 2^63).
+__device__ __forceinline__ int64_t sat_mul(int64_t a, int64_t b) {
+  if (a == 0 || b == 0) return 0;
+  if (a > INT64_MAX / b) return INT64_MAX;
+  return a * b;
+}
+__device__ __forceinline__ int64_t sat_add(int64_t a, int64_t b) {
+  return (a > INT64_MAX - b) ? INT64_MAX : a + b;
+}
+
+// latency.py:90-92  p1*b*I + p2*b + p3*I + p4
+__device__ __forceinline__ double prefill_time(const double* p, int64_t b, int64_t I) {
+  double db = i2d(b), dI = i2d(I);
+  double x = __dmul_rn(__dmul_rn(p[0], db), dI);
+  x = __dadd_rn(x, __dmul_rn(p[1], db));
+  x = __dadd_rn(x, __dmul_rn(p[2], dI));
+  return __dadd_rn(x, p[3]);
+}
+
+// latency.py:95-97  p5*b*c + p6*b + p7*c + p8
+__device__ __forceinline__ double decode_iteration_time(const double* p, int64_t cached, int64_t b) {
+  double db = i2d(b), dc = i2d(cached);
+  double x = __dmul_rn(__dmul_rn(p[4], db), dc);
+  x = __dadd_rn(x, __dmul_rn(p[5], db));
+  x = __dadd_rn(x, __dmul_rn(p[6], dc));
+  return __dadd_rn(x, p[7]);
+}
+
+// latency.py:100-109 closed form: S = O*I + O*(O+1)/2.0;
+// (p5*b + p7)*S + (p6*b + p8)*O
+__device__ __forceinline__ double decode_time(const double* p, int64_t b, int64_t I, int64_t O) {
+  double S = __dadd_rn(i2d(O * I), __ddiv_rn(i2d(O * (O + 1)), 2.0));
+  double db = i2d(b);
+  double a = __dmul_rn(__dadd_rn(__dmul_rn(p[4], db), p[6]), S);
+  double c = __dmul_rn(__dadd_rn(__dmul_rn(p[5], db), p[7]), i2d(O));
+  return __dadd_rn(a, c);
+}
+
+// CPython float floor division (Objects/floatobject.c _float_div_mod); here
+// both operands are positive (scheduling.py:128: budget > 0, bytes > 0).
+__device__ __forceinline__ double py_floordiv(double vx, double wx) {
+  double mod = fmod(vx, wx);
+  double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
+  if (mod != 0.0) {
+    if ((wx < 0) != (mod < 0)) {
+      mod = __dadd_rn(mod, wx);
+      div = __dsub_rn(div, 1.0);
+    }
+  }
+  double fl;
+  if (div != 0.0) {
+    fl = floor(div);
+    if (__dsub_rn(div, fl) > 0.5) fl = __dadd_rn(fl, 1.0);
+  } else {
+    fl = copysign(0.0, __ddiv_rn(vx, wx));
+  }
+  return fl;
+}
+
+// CPython 3.12 builtin sum() over floats with int start 0 (Neumaier).
+struct PySum {
+  double f, c;
+  int64_t n;
+  __device__ __forceinline__ void init() { f = 0.0; c = 0.0; n = 0; }
+  __device__ __forceinline__ void add(double x) {
+    if (n++ == 0) { f = __dadd_rn(0.0, x); return; }
+    double t = __dadd_rn(f, x);
+    if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+    else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+    f = t;
+  }
+  __device__ __forceinline__ double result() const {
+    double r = f;
+    if (c != 0.0 && isfinite(c)) r = __dadd_rn(r, c);
+    return r;
+  }
+};
+
+// glibc 2.39 exp, FMA variant (sysdeps/ieee754/dbl-64/e_exp.c compiled with
+// FMA contraction; CPython's math.exp on an FMA x86-64 host).  `tab` is the
+// 256-entry table (shared or global memory).  *overflow set when CPython
+// raises OverflowError.
+__device__ __forceinline__ double py_exp(double x, const uint64_t* tab, bool* overflow) {
+  const double kInvLn2N = 0x1.71547652b82fep+7;
+  const double kShift = 0x1.8p52;
+  const double kNegLn2HiN = -0x1.62e42fefa0000p-8;
+  const double kNegLn2LoN = -0x1.cf79abc9e3b3ap-47;
+  const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
+  const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+  *overflow = false;
+  uint64_t ix = d2u(x);
+  uint32_t abstop = (uint32_t)(ix >> 52) & 0x7ff;
+  if (abstop - 969u >= 63u) {
+    if ((int32_t)(abstop - 969u) < 0) return __dadd_rn(1.0, x);
+    if (abstop >= 1033u) {
+      if (ix == 0xfff0000000000000ull) return 0.0;
+      if (abstop >= 0x7ffu) return __dadd_rn(1.0, x);
+      if (ix >> 63) return 0.0;
+      *overflow = true;
+      return __longlong_as_double(0x7ff0000000000000ll);
+    }
+    abstop = 0;
+  }
+  double kd = __fma_rn(x, kInvLn2N, kShift);
+  uint64_t ki = d2u(kd);
+  kd = __dsub_rn(kd, kShift);
+  double r = __fma_rn(kd, kNegLn2HiN, x);
+  r = __fma_rn(kd, kNegLn2LoN, r);
+  uint32_t idx = 2u * (uint32_t)(ki & 127u);
+  uint64_t top = ki << 45;
+  double tail = u2d(tab[idx]);
+  uint64_t sbits = tab[idx + 1] + top;
+  double a = __fma_rn(r, C3, C2);
+  double t1 = __dadd_rn(r, tail);
+  double r2 = __dmul_rn(r, r);
+  double b = __fma_rn(r, C5, C4);
+  double tmp = __fma_rn(a, r2, t1);
+  double r4 = __dmul_rn(r2, r2);
+  tmp = __fma_rn(r4, b, tmp);
+  if (abstop == 0) {
+    if ((ki & 0x80000000u) == 0) {
+      double scale = u2d(sbits - (1009ull << 52));
+      double y = __dmul_rn(0x1p1009, __fma_rn(scale, tmp, scale));
+      if (isinf(y)) *overflow = true;
+      return y;
+    }
+    double scale = u2d(sbits + (1022ull << 52));
+    double st = __dmul_rn(scale, tmp);
+    double y = __dadd_rn(scale, st);
+    if (y < 1.0) {
+      double lo = __dadd_rn(__dsub_rn(scale, y), st);
+      double hi = __dadd_rn(1.0, y);
+      lo = __dadd_rn(__dadd_rn(__dsub_rn(1.0, hi), y), lo);
+      y = __dsub_rn(__dadd_rn(lo, hi), 1.0);
+      if (y == 0.0) y = 0.0;
+    }
+    return __dmul_rn(0x1p-1022, y);
+  }
+  double scale = u2d(sbits);
+  return __fma_rn(scale, tmp, scale);
+}
+
+// warp helpers --------------------------------------------------------------
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+}  // namespace hs

@@ -1,0 +1,74 @@
+// hs_internal.h -- host-side glue shared by the C-ABI and the kernel files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hetserve_b200.h"
+
+namespace hs {
+
+// One (machine, degree) work item of the table build.
+struct EntryDesc {
+  double p[8];
+  int64_t own_count;   // accelerator_count of the machine itself (instance count)
+  int64_t spec_count;  // accelerator_count of cluster.machine(name)
+  int64_t spec_mem;    // accelerator_mem_bytes of cluster.machine(name)
+  int32_t tp;
+  int32_t present;
+};
+
+struct SearchConst {
+  int64_t per_token;        // capacity.py:67-69
+  int64_t required;         // capacity.py:93 per_token * (Imax + Omax)
+  int64_t weights;          // capacity.py:85 param_count * bytes_per_param
+  int64_t static_overhead;  // EngineOverheads.static_overhead_bytes
+  double phi;               // EngineOverheads.mem_utilization_fraction
+  int64_t q;
+};
+
+// Product space for K2: machines padded to M >= 2 (a leading virtual
+// machine with one degree and contribution +0.0 leaves every total
+// unchanged: 0.0 + 0.0 + C0 == 0.0 + C0).
+constexpr int kMaxM = HS_MAX_MACHINES + 1;
+struct SpaceDesc {
+  int32_t M;
+  int32_t D[kMaxM];
+  int64_t okcnt[kMaxM];
+  // contributions, -inf where the entry is not OK; [M][HS_MAX_DEGREES]
+  double C[kMaxM * HS_MAX_DEGREES];
+};
+
+struct ReplayConst {
+  int32_t N;
+  int32_t policy;
+  int32_t n_types;
+  int32_t has_arrival;
+  double theta;
+  int64_t per_token;
+  double wrr_total;
+  int64_t heap_stride;            // heap entries per trace
+  int64_t heap_off[HS_MAX_INSTANCES + 1];
+  int32_t inst_type[HS_MAX_INSTANCES];
+  double type_p[HS_MAX_INSTANCES][8];
+  double type_budget[HS_MAX_INSTANCES];
+  double wrr_weight[HS_MAX_INSTANCES];
+};
+
+// launchers (return cudaError_t as int)
+cudaError_t launch_table_build(const EntryDesc* d_desc, int n, const SearchConst& sc, const int32_t* d_I,
+                               const int32_t* d_O, hs_entry* d_out, cudaStream_t st);
+// workspace: 3 * blocks doubles/int64s
+cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, int blocks,
+                               double* d_blk_best, int64_t* d_blk_idx, int64_t* d_blk_cnt,
+                               hs_cand* d_out, int64_t* d_cnt_out, cudaStream_t st);
+cudaError_t launch_search_score(const SpaceDesc& sd, int32_t m_real_offset, int64_t P, double* d_total,
+                                int8_t* d_first_bad, uint8_t* d_flag, cudaStream_t st);
+cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st);
+cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
+                          const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
+                          double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result,
+                          double* d_wrec, int32_t* d_qnext, uint64_t* d_heap, cudaStream_t st);
+
+int sm_count();
+
+}  // namespace hs

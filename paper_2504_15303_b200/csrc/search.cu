@@ -1,0 +1,429 @@
+// search.cu -- deployment-configuration search on the GPU.
+//
+// K1 k_table_build: one warp per (machine, tp degree).  Replaces the
+//   per-machine body of planner.py:152-179 (estimate_system_throughput),
+//   i.e. capacity.py:72-95 budget + feasibility and planner.py:51-118: the
+//   greedy static-batch scan over the trace, batch pricing, CPython's
+//   compensated sum of batch times and tokens / total_time.  The greedy scan
+//   is sequential in batch boundaries; within a batch the warp tests 32
+//   candidate extensions at once (warp prefix sum of inputs, prefix max of
+//   outputs, one ballot), so a batch of width w costs ceil((w+1)/32) steps.
+//
+// K2 k_search_best: exhaustive argmax over the mixed-radix candidate space
+//   of planner.py:213-228 (itertools.product, machine 0 most significant;
+//   best = max total, ties -> lowest index, as ranked.sort's key).  Every
+//   candidate's total is evaluated in the reference's left-to-right order
+//   (planner.py:151,180): the shared prefix over the outer machines is kept
+//   incrementally (odometer), and each candidate costs one DADD (prefix +
+//   last contribution) and one DSETP.GT.OR against the thread's best.
+//   Non-OK table entries hold -inf, so infeasible candidates evaluate to
+//   -inf (or NaN) and can never satisfy `> best`.
+//
+// k_search_score: per-candidate total + first failing machine, for the full
+//   ranking of small spaces (sorted afterwards with CUB).
+#include <cub/cub.cuh>
+
+#include "hs_device.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+// ----------------------------------------------------------------- K1
+__global__ void __launch_bounds__(128) k_table_build(const EntryDesc* __restrict__ desc, int n, SearchConst sc,
+                                                     const int32_t* __restrict__ I, const int32_t* __restrict__ O,
+                                                     hs_entry* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (e >= n) return;
+  const EntryDesc d = desc[e];
+  hs_entry r;
+  r.contribution = 0.0;
+  r.rate = 0.0;
+  r.budget = 0.0;
+  r.slack = 0.0;
+  r.tp_degree = d.tp;
+  r.instance_count = d.tp > 0 ? d.own_count / d.tp : 0;
+  r.bad_request = -1;
+  r.token_count = 0;
+  r.zero_div_int = 0;
+  r._pad = 0;
+  r.status = HS_ENTRY_OK;
+  const int64_t q = sc.q;
+  // token_count = sum(I + O) (planner.py:117)
+  int64_t tok = 0;
+  for (int64_t k = lane; k < q; k += 32) tok += (int64_t)I[k] + O[k];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tok += __shfl_xor_sync(0xffffffffu, tok, off);
+  r.token_count = tok;
+
+  if (d.tp < 1 || d.spec_count % d.tp != 0) {
+    r.status = HS_ENTRY_BAD_DEGREE;
+  } else {
+    // capacity.py:84-86: ((t*mem) * phi - delta) - weights
+    double usable = __dmul_rn(i2d(d.tp * d.spec_mem), sc.phi);
+    double budget = __dsub_rn(__dsub_rn(usable, i2d(sc.static_overhead)), i2d(sc.weights));
+    double slack = __dsub_rn(budget, i2d(sc.required));
+    r.budget = budget;
+    r.slack = slack;
+    if (!(slack >= 0.0)) {
+      r.status = HS_ENTRY_INFEASIBLE_CONFIG;
+    } else if (!d.present) {
+      r.status = HS_ENTRY_MISSING_PARAMS;
+    } else {
+      PySum tot;
+      tot.init();
+      int64_t start = 0;
+      const int64_t pt = sc.per_token;
+      while (start < q) {
+        int64_t sumI = 0, maxO = 0, maxI = 0;  // carries of the batch so far
+        int64_t pos = start, stop = start, bMO = 0, bMI = 0;
+        for (;;) {
+          const int64_t idx = pos + lane;
+          const bool valid = idx < q;
+          int64_t s = valid ? (int64_t)I[idx] : 0;
+          int64_t mo = valid ? (int64_t)O[idx] : 0;
+          int64_t mi = s;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            int64_t ts = __shfl_up_sync(0xffffffffu, s, off);
+            int64_t to = __shfl_up_sync(0xffffffffu, mo, off);
+            int64_t ti = __shfl_up_sync(0xffffffffu, mi, off);
+            if (lane >= off) {
+              s += ts;
+              mo = mo > to ? mo : to;
+              mi = mi > ti ? mi : ti;
+            }
+          }
+          const int64_t candI = sumI + s;
+          const int64_t candMO = maxO > mo ? maxO : mo;
+          const int64_t candMI = maxI > mi ? maxI : mi;
+          const int64_t width = idx - start + 1;
+          // planner.py:69-74: per_token*sum(I) + width*per_token*max(O) > budget
+          const int64_t reserved = sat_add(sat_mul(pt, candI), sat_mul(sat_mul(width, pt), candMO));
+          const bool fail = !valid || int_gt_double(reserved, budget);
+          const unsigned bal = __ballot_sync(0xffffffffu, fail);
+          if (bal) {
+            const int f = __ffs(bal) - 1;
+            stop = pos + f;
+            const int src = f > 0 ? f - 1 : 0;
+            const int64_t sMO = __shfl_sync(0xffffffffu, candMO, src);
+            const int64_t sMI = __shfl_sync(0xffffffffu, candMI, src);
+            bMO = f > 0 ? sMO : maxO;
+            bMI = f > 0 ? sMI : maxI;
+            break;
+          }
+          sumI = __shfl_sync(0xffffffffu, candI, 31);
+          maxO = __shfl_sync(0xffffffffu, candMO, 31);
+          maxI = __shfl_sync(0xffffffffu, candMI, 31);
+          pos += 32;
+        }
+        if (stop == start) {  // planner.py:78-84
+          r.status = HS_ENTRY_INFEASIBLE_REQUEST;
+          r.bad_request = start;
+          break;
+        }
+        const int64_t b = stop - start;
+        // planner.py:90-101 estimate_batch_time
+        tot.add(__dadd_rn(prefill_time(d.p, b, bMI), decode_time(d.p, b, bMI, bMO)));
+        start = stop;
+      }
+      if (r.status == HS_ENTRY_OK) {
+        const double total = tot.result();  // planner.py:46-48 sum(per_batch_time)
+        if (tot.n == 0 || total == 0.0) {
+          r.status = HS_ENTRY_ZERO_DIVISION;
+          r.zero_div_int = tot.n == 0;
+        } else {
+          r.rate = __ddiv_rn(i2d(tok), total);                        // planner.py:118
+          r.contribution = __dmul_rn(r.rate, i2d(r.instance_count));  // planner.py:168
+        }
+      }
+    }
+  }
+  if (lane == 0) out[e] = r;
+}
+
+cudaError_t launch_table_build(const EntryDesc* d_desc, int n, const SearchConst& sc, const int32_t* d_I,
+                               const int32_t* d_O, hs_entry* d_out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int warps_per_block = 4;
+  int blocks = (n + warps_per_block - 1) / warps_per_block;
+  k_table_build<<<blocks, warps_per_block * 32, 0, st>>>(d_desc, n, sc, d_I, d_O, d_out);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- K2
+__constant__ SpaceDesc c_space;
+
+// Fully unrolled innermost level for a compile-time innermost radix DL.
+template <int DL>
+struct Inner {
+  // Evaluates the D1*DL candidates of one item (prefix s); returns true if
+  // any total is > best.
+  static __device__ __forceinline__ bool any_gt(double s, const double* C1, int D1, const double* CL,
+                                                double best) {
+    bool hit = false;
+    for (int d1 = 0; d1 < D1; ++d1) {
+      const double v1 = __dadd_rn(s, C1[d1]);
+#pragma unroll
+      for (int d2 = 0; d2 < DL; ++d2) hit |= __dadd_rn(v1, CL[d2]) > best;
+    }
+    return hit;
+  }
+};
+
+// Slow path: scan one item in index order, tracking (best, lowest index).
+// Candidates outside [lo, hi) (item-relative) are skipped.
+__device__ __forceinline__ void item_scan(double s, bool prefix_ok, const double* C1, int D1, const double* CL,
+                                          int DL, int64_t base, int64_t lo, int64_t hi, double& best,
+                                          int64_t& bidx, int64_t& cnt, bool count) {
+  const int M = c_space.M;
+  for (int d1 = 0; d1 < D1; ++d1) {
+    const double v1 = __dadd_rn(s, C1[d1]);
+    for (int d2 = 0; d2 < DL; ++d2) {
+      const int64_t c = (int64_t)d1 * DL + d2;
+      if (c < lo || c >= hi) continue;
+      const double v = __dadd_rn(v1, CL[d2]);
+      const bool ok = prefix_ok && c_space.C[(M - 2) * HS_MAX_DEGREES + d1] != -INFINITY &&
+                      c_space.C[(M - 1) * HS_MAX_DEGREES + d2] != -INFINITY;
+      if (count && ok) ++cnt;
+      if (ok && v > best) {
+        best = v;
+        bidx = base + c;
+      }
+    }
+  }
+}
+
+template <int DL>
+__global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t item_end, int64_t begin,
+                                                     int64_t end, int64_t chunk, double* blk_best,
+                                                     int64_t* blk_idx, int64_t* blk_cnt) {
+  __shared__ double sC[kMaxM * HS_MAX_DEGREES];
+  __shared__ double rb[256 / 32];
+  __shared__ int64_t ri[256 / 32], rc[256 / 32];
+  const int M = c_space.M;
+  for (int k = threadIdx.x; k < M * HS_MAX_DEGREES; k += blockDim.x) sC[k] = c_space.C[k];
+  __syncthreads();
+  const int D1 = c_space.D[M - 2];
+  const int DLr = DL > 0 ? DL : c_space.D[M - 1];
+  const int64_t Din = (int64_t)D1 * DLr;
+  const double* C1 = &sC[(M - 2) * HS_MAX_DEGREES];
+  double CL[DL > 0 ? DL : 1];
+  if (DL > 0) {
+#pragma unroll
+    for (int d = 0; d < (DL > 0 ? DL : 1); ++d) CL[d] = sC[(M - 1) * HS_MAX_DEGREES + d];
+  }
+  const double* CLp = DL > 0 ? CL : &sC[(M - 1) * HS_MAX_DEGREES];
+  const int64_t inner_ok = c_space.okcnt[M - 2] * c_space.okcnt[M - 1];
+
+  double best = -INFINITY;
+  int64_t bidx = -1, cnt = 0;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t it = item_begin + tid * chunk;
+  int64_t it_end = it + chunk;
+  if (it_end > item_end) it_end = item_end;
+  if (it < it_end) {
+    // decode the outer digits of the first item (machines 0..M-3)
+    int32_t dig[kMaxM];
+    double ps[kMaxM];  // ps[i] = left-to-right sum of machines 0..i
+    int64_t x = it;
+    for (int i = M - 3; i >= 0; --i) {
+      dig[i] = (int32_t)(x % c_space.D[i]);
+      x /= c_space.D[i];
+    }
+    double acc = 0.0;
+    for (int i = 0; i <= M - 3; ++i) {
+      acc = __dadd_rn(acc, sC[i * HS_MAX_DEGREES + dig[i]]);
+      ps[i] = acc;
+    }
+    for (; it < it_end; ++it) {
+      const double s = M >= 3 ? ps[M - 3] : 0.0;
+      const bool prefix_ok = s != -INFINITY && s == s;
+      const int64_t base = it * Din;
+      const bool partial = base < begin || base + Din > end;
+      if (partial) {
+        item_scan(s, prefix_ok, C1, D1, CLp, DLr, base, begin - base, end - base, best, bidx, cnt, true);
+      } else {
+        bool hit;
+        if (DL > 0) {
+          hit = Inner<(DL > 0 ? DL : 1)>::any_gt(s, C1, D1, CLp, best);
+        } else {
+          hit = false;
+          for (int d1 = 0; d1 < D1; ++d1) {
+            const double v1 = __dadd_rn(s, C1[d1]);
+            for (int d2 = 0; d2 < DLr; ++d2) hit |= __dadd_rn(v1, CLp[d2]) > best;
+          }
+        }
+        if (hit) item_scan(s, prefix_ok, C1, D1, CLp, DLr, base, 0, Din, best, bidx, cnt, false);
+        if (prefix_ok) cnt += inner_ok;
+      }
+      // odometer over the outer digits, recomputing the changed prefix sums
+      int i = M - 3;
+      while (i >= 0) {
+        if (++dig[i] < c_space.D[i]) break;
+        dig[i] = 0;
+        --i;
+      }
+      if (i < 0) i = 0;
+      double a = i > 0 ? ps[i - 1] : 0.0;
+      for (int j = i; j <= M - 3; ++j) {
+        a = __dadd_rn(a, sC[j * HS_MAX_DEGREES + dig[j]]);
+        ps[j] = a;
+      }
+    }
+  }
+  // block reduction: max total, then lowest index
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if (oi >= 0 && (bidx < 0 || ob > best || (ob == best && oi < bidx))) {
+      best = ob;
+      bidx = oi;
+    }
+  }
+  if (lane == 0) {
+    rb[w] = best;
+    ri[w] = bidx;
+    rc[w] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      cnt += rc[k];
+      if (ri[k] >= 0 && (bidx < 0 || rb[k] > best || (rb[k] == best && ri[k] < bidx))) {
+        best = rb[k];
+        bidx = ri[k];
+      }
+    }
+    blk_best[blockIdx.x] = best;
+    blk_idx[blockIdx.x] = bidx;
+    blk_cnt[blockIdx.x] = cnt;
+  }
+}
+
+__global__ void k_search_final(const double* blk_best, const int64_t* blk_idx, const int64_t* blk_cnt, int nblk,
+                               hs_cand* out, int64_t* cnt_out) {
+  __shared__ double rb[32];
+  __shared__ int64_t ri[32], rc[32];
+  double best = -INFINITY;
+  int64_t bidx = -1, cnt = 0;
+  for (int k = threadIdx.x; k < nblk; k += blockDim.x) {
+    cnt += blk_cnt[k];
+    const double ob = blk_best[k];
+    const int64_t oi = blk_idx[k];
+    if (oi >= 0 && (bidx < 0 || ob > best || (ob == best && oi < bidx))) {
+      best = ob;
+      bidx = oi;
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if (oi >= 0 && (bidx < 0 || ob > best || (ob == best && oi < bidx))) {
+      best = ob;
+      bidx = oi;
+    }
+  }
+  if (lane == 0) {
+    rb[w] = best;
+    ri[w] = bidx;
+    rc[w] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      cnt += rc[k];
+      if (ri[k] >= 0 && (bidx < 0 || rb[k] > best || (rb[k] == best && ri[k] < bidx))) {
+        best = rb[k];
+        bidx = ri[k];
+      }
+    }
+    out->total = bidx >= 0 ? best : 0.0;
+    out->index = bidx;
+    *cnt_out = cnt;
+  }
+}
+
+cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, int blocks, double* d_blk_best,
+                               int64_t* d_blk_idx, int64_t* d_blk_cnt, hs_cand* d_out, int64_t* d_cnt_out,
+                               cudaStream_t st) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_space, &sd, sizeof(SpaceDesc), 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  const int threads = 256;
+  const int64_t Din = (int64_t)sd.D[sd.M - 2] * sd.D[sd.M - 1];
+  const int64_t item_begin = begin / Din;
+  const int64_t item_end = end > begin ? (end + Din - 1) / Din : item_begin;
+  const int64_t n_items = item_end - item_begin;
+  const int64_t nthreads = (int64_t)blocks * threads;
+  int64_t chunk = (n_items + nthreads - 1) / nthreads;
+  if (chunk < 1) chunk = 1;
+  const int DL = sd.D[sd.M - 1];
+#define HS_LAUNCH_BEST(K)                                                                                   \
+  k_search_best<K><<<blocks, threads, 0, st>>>(item_begin, item_end, begin, end, chunk, d_blk_best, d_blk_idx, \
+                                               d_blk_cnt)
+  switch (DL) {
+    case 1: HS_LAUNCH_BEST(1); break;
+    case 2: HS_LAUNCH_BEST(2); break;
+    case 3: HS_LAUNCH_BEST(3); break;
+    case 4: HS_LAUNCH_BEST(4); break;
+    case 5: HS_LAUNCH_BEST(5); break;
+    case 6: HS_LAUNCH_BEST(6); break;
+    case 7: HS_LAUNCH_BEST(7); break;
+    case 8: HS_LAUNCH_BEST(8); break;
+    default: HS_LAUNCH_BEST(0); break;
+  }
+#undef HS_LAUNCH_BEST
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_search_final<<<1, 1024, 0, st>>>(d_blk_best, d_blk_idx, d_blk_cnt, blocks, d_out, d_cnt_out);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------- full ranking
+// One thread per candidate: left-to-right total and the first machine whose
+// entry is not OK (the one whose exception search_optimal_config records).
+__global__ void k_search_score(int32_t m_off, int64_t P, double* __restrict__ total, int8_t* __restrict__ first_bad,
+                               uint8_t* __restrict__ flag) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P) return;
+  const int M = c_space.M;
+  int32_t dig[kMaxM];
+  int64_t x = c;
+  for (int i = M - 1; i >= 0; --i) {
+    dig[i] = (int32_t)(x % c_space.D[i]);
+    x /= c_space.D[i];
+  }
+  double acc = 0.0;
+  int fb = -1;
+  for (int i = 0; i < M; ++i) {
+    const double v = c_space.C[i * HS_MAX_DEGREES + dig[i]];
+    // status is carried in okcnt bit tricks: -inf marks non-OK entries
+    if (v == -INFINITY) {
+      fb = i - m_off;
+      break;
+    }
+    acc = __dadd_rn(acc, v);
+  }
+  total[c] = acc;
+  first_bad[c] = (int8_t)fb;
+  flag[c] = fb < 0;
+}
+
+cudaError_t launch_search_score(const SpaceDesc& sd, int32_t m_off, int64_t P, double* d_total, int8_t* d_first_bad,
+                                uint8_t* d_flag, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_space, &sd, sizeof(SpaceDesc), 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  if (P <= 0) return cudaSuccess;
+  const int threads = 256;
+  k_search_score<<<(unsigned)((P + threads - 1) / threads), threads, 0, st>>>(m_off, P, d_total, d_first_bad,
+                                                                              d_flag);
+  return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,298 @@
+"""Cluster replay on the GPU, behind the reference's simulator API.
+
+Drop-in entry points (reference /root/reference/pkg/src/hetserve/simulator.py):
+
+* ``run_continuous(scenario)`` (simulator.py:272-363) -> SimMetrics, with
+  assignments, departure times, per-instance metrics and residual loads
+  bit-identical to the reference;
+* ``run_scenario`` / ``run_policy_comparison`` (simulator.py:366-380);
+* ``generate_arrivals`` / ``build_instances`` (simulator.py:112-158): host
+  setup, same arithmetic as the reference.
+
+Engine-level API: ``replay_traces(...)`` replays a batch of traces (one warp
+each) on one deployment and returns arrays, for the batched-replay configs.
+
+Static mode (``run_static``, simulator.py:206-250) is the next row of the
+hot-path scope and is not in the engine yet.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native as nat
+from .domain import (
+    InfeasibleConfigError,
+    InfeasibleRequestError,
+    SchedulingError,
+    SpecError,
+    check_memory_constraint,
+    kv_budget,
+    kv_bytes_per_token,
+)
+from .scheduling import InstanceHandle, OutputLengthPredictor, PolicyConfig, PredictorConfig
+
+
+@dataclass(frozen=True)
+class Scenario:
+    cluster: object
+    config: object
+    trace: tuple
+    arrival_rate: float
+    policy: PolicyConfig
+    mode: str
+    seed: int
+    params: dict
+
+    def __post_init__(self):
+        if not self.trace:
+            raise SpecError("scenario trace must be non-empty")
+        if self.mode not in ("static", "continuous"):
+            raise SpecError(f"mode must be 'static' or 'continuous', got {self.mode!r}")
+        if not (self.arrival_rate > 0):
+            raise SpecError(f"arrival rate must be positive or inf, got {self.arrival_rate}")
+
+
+@dataclass(frozen=True)
+class InstanceMetrics:
+    id: str
+    completion_time: float
+    request_count: int
+    token_count: int
+    peak_kv_usage: float
+
+
+@dataclass(frozen=True)
+class SimMetrics:
+    policy: str
+    mode: str
+    rate: float
+    system_throughput: float
+    makespan: float
+    completion_time_spread: float
+    per_instance: tuple
+    assignments: tuple
+    request_times: tuple
+    residual_loads: tuple
+
+
+def arrival_times(n: int, rate: float, seed: int) -> np.ndarray:
+    """simulator.py:112-124 as an fp64 array: all 0.0 at rate=inf, else the
+    running sum of seeded exponential gaps (np.cumsum is sequential)."""
+    if math.isinf(rate):
+        return np.zeros(n, np.float64)
+    if rate <= 0:
+        raise SpecError(f"arrival rate must be positive, got {rate}")
+    rng = np.random.default_rng(seed)
+    return np.cumsum(rng.exponential(1.0 / rate, size=n))
+
+
+def generate_arrivals(trace, rate: float, seed: int) -> list:
+    return [(r, float(t)) for r, t in zip(trace, arrival_times(len(trace), rate, seed))]
+
+
+def build_instances(cluster, config, params) -> list:
+    """Every deployed instance in config order (simulator.py:127-158)."""
+    out = []
+    for placement in config.per_machine:
+        machine = cluster.machine(placement.machine)
+        budget = kv_budget(machine, placement.tp_degree, cluster.model, cluster.engine)
+        verdict = check_memory_constraint(budget, cluster.limits, cluster.model)
+        if not verdict.feasible:
+            raise InfeasibleConfigError(
+                f"machine {machine.name!r} at tp={placement.tp_degree} cannot hold one maximal "
+                f"request (slack {verdict.slack_bytes:.0f} bytes)",
+                machine=machine.name,
+                slack_bytes=verdict.slack_bytes,
+            )
+        key = (machine.name, placement.tp_degree)
+        if key not in params:
+            raise SpecError(f"no fitted parameters for machine {machine.name!r} at tp={placement.tp_degree}")
+        for k in range(placement.instance_count):
+            out.append(InstanceHandle(id=f"{machine.name}/{k}", machine=machine.name,
+                                      tp_degree=placement.tp_degree, params=params[key], budget=budget))
+    return out
+
+
+def _params_tuple(p) -> tuple:
+    return tuple(float(x) for x in (p.p1, p.p2, p.p3, p.p4, p.p5, p.p6, p.p7, p.p8))
+
+
+def engine_instances(handles, policy: PolicyConfig):
+    """hs_instance array: classes = bit-identical (params, budget)."""
+    n = len(handles)
+    arr = (nat.hs_instance * max(n, 1))()
+    classes = {}
+    for j, h in enumerate(handles):
+        pt = _params_tuple(h.params)
+        b = float(h.budget.total_bytes)
+        key = (tuple(x.hex() for x in pt), b.hex())
+        ty = classes.setdefault(key, len(classes))
+        for k in range(8):
+            arr[j].p[k] = pt[k]
+        arr[j].budget = b
+        arr[j].wrr_weight = float(policy.wrr_weights[j]) if policy.policy == "WRR" else 0.0
+        arr[j].type = ty
+    return arr
+
+
+def _check_scheduler(handles, policy: PolicyConfig) -> None:
+    """Scheduler.__init__ validation (scheduling.py:184-199)."""
+    if not handles:
+        raise SchedulingError("scheduler needs at least one instance")
+    if policy.policy == "WRR" and len(policy.wrr_weights) != len(handles):
+        raise SpecError(f"WRR needs one weight per instance ({len(handles)}), got {len(policy.wrr_weights)}")
+    for h in handles:
+        if h.budget.total_bytes <= 0:
+            raise SpecError(f"instance {h.id!r} has a non-positive KV budget")
+
+
+def _predictor(scenario) -> OutputLengthPredictor:
+    cfg = scenario.policy.predictor
+    if cfg.seed is None:
+        cfg = replace(cfg, seed=scenario.seed)
+    return OutputLengthPredictor(cfg, scenario.cluster.limits.max_output_len)
+
+
+def _raise_trace_error(res, handles, trace, per_token, theta=None) -> None:
+    err = int(res["error"])
+    if err == nat.TRACE_OK:
+        return
+    inst = int(res["err_instance"])
+    ridx = int(res["err_request"])
+    if err == nat.TRACE_INFEASIBLE_REQUEST:
+        r = trace[ridx]
+        need = r.input_len + r.output_len
+        budget = handles[inst].budget.total_bytes
+        raise InfeasibleRequestError(
+            f"request {r.id!r} needs {per_token * need:.0f} KV bytes alone, budget of "
+            f"instance {handles[inst].id!r} is {budget:.0f}",
+            request_id=r.id,
+        )
+    if err == nat.TRACE_NONPOSITIVE_COST:
+        total = float(res["err_value"])
+        raise SpecError(
+            f"non-positive batch time {total} for request {trace[ridx].id!r}; latency parameters are corrupt"
+        )
+    if err == nat.TRACE_EXP_OVERFLOW:
+        raise OverflowError("math range error")
+    if err == nat.TRACE_NO_INSTANCE:
+        raise SchedulingError("no instance available for scheduling")
+    if err == nat.TRACE_NEGATIVE_RUNNING:
+        raise SpecError("running token sums went negative; completion applied twice?")
+    raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"replay hit an engine limit (code {err})")
+
+
+def _policy_struct(policy: PolicyConfig, n: int, per_token: int) -> nat.hs_policy:
+    return nat.hs_policy(nat.POLICY_CODE[policy.policy], n, float(policy.theta), per_token)
+
+
+def run_continuous(scenario, engine=None) -> SimMetrics:
+    """simulator.py:272-363 on the GPU (one trace, one warp)."""
+    handles = build_instances(scenario.cluster, scenario.config, scenario.params)
+    policy = scenario.policy
+    _check_scheduler(handles, policy)
+    N = len(handles)
+    if N > nat.HS_MAX_INSTANCES:
+        raise nat.EngineError(nat.HS_ERR_UNSUPPORTED,
+                              f"{N} instances: the round-1 replay kernel handles up to {nat.HS_MAX_INSTANCES}")
+    trace = scenario.trace
+    ids = [r.id for r in trace]
+    if len(set(ids)) != len(ids):
+        raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, "duplicate request ids in one trace are not supported")
+    per_token = kv_bytes_per_token(scenario.cluster.model)
+    I = np.fromiter((r.input_len for r in trace), np.int64, len(trace))
+    O = np.fromiter((r.output_len for r in trace), np.int64, len(trace))
+    P = _predictor(scenario).predict_lengths(O)
+    for a in (I, O, P):
+        if len(a) and a.max() > 2**31 - 1:
+            raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, "request lengths above 2^31 - 1")
+    T = arrival_times(len(trace), scenario.arrival_rate, scenario.seed)
+    eng = engine or nat.engine_for()
+    offsets = np.array([0, len(trace)], np.int64)
+    assign, depart, metrics, result = eng.replay(
+        engine_instances(handles, policy), _policy_struct(policy, N, per_token), offsets,
+        I.astype(np.int32), O.astype(np.int32), P.astype(np.int32),
+        None if math.isinf(scenario.arrival_rate) else T)
+    _raise_trace_error(result[0], handles, trace, per_token)
+    m = metrics[0]
+    completion = m["completion_time"].tolist()
+    req_count = m["request_count"].tolist()
+    tok_count = m["token_count"].tolist()
+    peak = m["peak_kv_usage"].tolist()
+    # request_times keeps the reference's dict insertion order = retirement
+    # order: (departure time, instance index, admission order) -- exact when
+    # step costs are non-negative (time is then monotone per instance).
+    order = np.lexsort((np.arange(len(trace)), assign.astype(np.int64), depart))
+    dep = depart.tolist()
+    arr = T.tolist()
+    request_times = tuple((ids[k], arr[k], dep[k]) for k in order.tolist())
+    makespan = max(completion) if completion else 0.0
+    total_tokens = sum(tok_count)
+    return SimMetrics(
+        policy=policy.policy,
+        mode=scenario.mode,
+        rate=scenario.arrival_rate,
+        system_throughput=total_tokens / makespan if makespan > 0 else math.inf,
+        makespan=makespan,
+        completion_time_spread=max(completion) - min(completion) if completion else 0.0,
+        per_instance=tuple(
+            InstanceMetrics(id=h.id, completion_time=completion[i], request_count=req_count[i],
+                            token_count=tok_count[i], peak_kv_usage=peak[i])
+            for i, h in enumerate(handles)
+        ),
+        assignments=tuple(assign.tolist()),
+        request_times=request_times,
+        residual_loads=tuple(m["residual_load"].tolist()),
+    )
+
+
+def run_static(scenario, engine=None) -> SimMetrics:
+    if not math.isinf(scenario.arrival_rate):
+        raise SpecError("static mode needs arrival_rate=inf (a fully known queue)")
+    raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, "static-mode replay is not in the engine yet (SURVEY 8f row 1)")
+
+
+def run_scenario(scenario, engine=None) -> SimMetrics:
+    if scenario.mode == "static":
+        return run_static(scenario, engine=engine)
+    return run_continuous(scenario, engine=engine)
+
+
+def run_policy_comparison(scenario, policies, engine=None) -> list:
+    """Each policy on the identical arrival / prediction realisation."""
+    if not policies:
+        raise SpecError("policy comparison needs at least one policy")
+    return [run_scenario(replace(scenario, policy=replace(scenario.policy, policy=p)), engine=engine)
+            for p in policies]
+
+
+# ------------------------------------------------------------ batched API
+@dataclass
+class ReplayBatchResult:
+    assign: np.ndarray | None      # [total requests] uint8
+    depart: np.ndarray | None      # [total requests] float64
+    metrics: np.ndarray            # [T, N] METRICS_DTYPE
+    result: np.ndarray             # [T] RESULT_DTYPE
+    kernel_ms: float
+
+
+def replay_traces(cluster, config, params, policy: PolicyConfig, offsets, input_len, output_len, pred_output_len,
+                  arrival=None, want_assign=True, want_depart=False, engine=None) -> ReplayBatchResult:
+    """Replay T traces (offsets [T+1]) on one deployment in one launch."""
+    handles = build_instances(cluster, config, params)
+    _check_scheduler(handles, policy)
+    N = len(handles)
+    if N > nat.HS_MAX_INSTANCES:
+        raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"{N} instances (max {nat.HS_MAX_INSTANCES})")
+    per_token = kv_bytes_per_token(cluster.model)
+    eng = engine or nat.engine_for()
+    a, d, m, r = eng.replay(engine_instances(handles, policy), _policy_struct(policy, N, per_token),
+                            np.ascontiguousarray(offsets, np.int64), np.ascontiguousarray(input_len, np.int32),
+                            np.ascontiguousarray(output_len, np.int32), np.ascontiguousarray(pred_output_len, np.int32),
+                            None if arrival is None else np.ascontiguousarray(arrival, np.float64),
+                            want_assign=want_assign, want_depart=want_depart)
+    return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)
