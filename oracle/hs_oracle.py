@@ -139,3 +139,45 @@ def replay(instances, policy, offsets, I, O, P, arrival=None, nthreads=1, want_d
                                 _p(assign), _p(depart), _p(metrics), _p(result))
     assert rc == 0
     return assign[:total], (None if depart is None else depart[:total]), metrics[: T * N].reshape(T, N), result[:T]
+
+
+def best_monotone(table, nd):
+    """Exact argmax of the left-to-right fp64 sum over the full product space
+    in O(M^2 * D), for tables whose OK contributions are all finite.
+
+    Rounded addition is monotone in each argument, so from a prefix sum s the
+    largest reachable total is the greedy completion g(s) = (((s + m_k) +
+    m_{k+1}) ...) with m_j the largest OK contribution of machine j.  The
+    global maximum V is g from the empty prefix; the lowest index reaching V
+    is found digit by digit: at each machine take the smallest OK digit whose
+    greedy completion still equals V (planner.py:227's tie rule).  Returns
+    (V, index, n_feasible) with n_feasible = prod(#OK degrees)."""
+    from paper_2504_15303_b200 import _native as nat
+    M = len(nd)
+    C = [[float(table[i, d]["contribution"]) if int(table[i, d]["status"]) == nat.ENTRY_OK else None
+          for d in range(int(nd[i]))] for i in range(M)]
+    mx = []
+    nfeas = 1
+    for row in C:
+        ok = [v for v in row if v is not None]
+        nfeas *= len(ok)
+        mx.append(max(ok) if ok else None)
+    if nfeas == 0:
+        return 0.0, -1, 0
+
+    def greedy(s, k):
+        for j in range(k, M):
+            s = s + mx[j]
+        return s
+
+    V = greedy(0.0, 0)
+    s, index = 0.0, 0
+    for i in range(M):
+        for d, v in enumerate(C[i]):
+            if v is not None and greedy(s + v, i + 1) == V:
+                s = s + v
+                index = index * int(nd[i]) + d
+                break
+        else:
+            raise AssertionError("monotone search lost the maximum")
+    return V, index, nfeas

@@ -207,7 +207,7 @@ class Engine:
         I = np.ascontiguousarray(I, dtype=np.int32)
         O = np.ascontiguousarray(O, dtype=np.int32)
         rc = self.lib.hs_search_tables(self.handle, C.byref(model), C.byref(engine), C.byref(limits),
-                                       machines.ctypes.data_as(C.c_void_p), M, _ptr(params), _ptr(present), _ptr(I),
+                                       C.cast(machines, C.c_void_p), M, _ptr(params), _ptr(present), _ptr(I),
                                        _ptr(O), len(I), _ptr(table), _ptr(nd))
         self.check(rc, "hs_search_tables")
         return table.reshape(M, HS_MAX_DEGREES), nd

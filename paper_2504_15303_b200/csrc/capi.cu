@@ -10,6 +10,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "hs_internal.h"
 
@@ -444,7 +445,7 @@ int hs_search_rank(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
       (rc = ensure_t(c, S_RANKED, (size_t)P, &out)))
     return rc;
   size_t tmp1 = 0, tmp2 = 0;
-  cub::CountingInputIterator<int64_t> counting(0);
+  thrust::counting_iterator<int64_t> counting(0);
   HS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp1, counting, flag, sel, nsel, P, c->stream));
   HS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, keys, keys2, sel, idx2, (int)P, 0, 64, c->stream));
   void* tmp;

@@ -1,0 +1,190 @@
+"""CUDA engine vs the reference (golden fixtures) and vs the C oracle.
+
+Every assertion is bit-exact (float.hex / integer equality): the path is
+integer and fp64 work evaluated in the reference's operation order.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import helpers as H
+import paper_2504_15303_b200 as hs
+from oracle import hs_oracle as orc
+from paper_2504_15303_b200 import _native as nat
+from paper_2504_15303_b200 import planner
+from paper_2504_15303_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+SEARCH = H.load("search_cases.json")
+REPLAY = H.load("replay_cases.json")
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = nat.engine_for(0)
+    yield e
+
+
+@pytest.mark.parametrize("case", [c for c in SEARCH if c["kind"] == "search"], ids=lambda c: c["name"])
+def test_search_tables_match_reference(eng, case):
+    cluster = H.cluster_from(case["profile"])
+    params_by = H.params_from(case["profile"])
+    requests = H.search_trace(case)
+    t = planner.build_tables(cluster, requests, params_by, engine=eng)
+    H.check_table(case, t.entries, t.n_degrees, requests)
+
+
+@pytest.mark.parametrize("case", [c for c in SEARCH if c["kind"] == "search" and ("ranked" in c or "error" in c)],
+                         ids=lambda c: c["name"])
+def test_search_optimal_config_matches_reference(eng, case):
+    cluster = H.cluster_from(case["profile"])
+    params_by = H.params_from(case["profile"])
+    requests = H.search_trace(case)
+    if "error" in case:
+        with pytest.raises(ZeroDivisionError, match=case["error"]["msg"]):
+            hs.search_optimal_config(cluster, requests, params_by, engine=eng)
+        return
+    out = hs.search_optimal_config(cluster, requests, params_by, engine=eng)
+    assert out.candidates_visited == case["visited"]
+    assert len(out.ranked) == len(case["ranked"])
+    for got, want in zip(out.ranked, case["ranked"]):
+        assert [p.tp_degree for p in got.config.per_machine] == want["degrees"]
+        assert got.system_tokens_per_sec.hex() == want["total"]
+        pm = [[m.instance_tokens_per_sec.hex(), m.machine_tokens_per_sec.hex(), m.budget_bytes.hex(),
+               m.slack_bytes.hex(), m.instance_count] for m in got.per_machine]
+        assert pm == want["per_machine"]
+    assert [[[p.tp_degree for p in c.per_machine], r] for c, r in out.infeasible] == case["infeasible"]
+    if out.ranked:
+        best = out.best
+        est = hs.estimate_system_throughput(cluster, best.config, requests, params_by, engine=eng)
+        assert est.system_tokens_per_sec == best.system_tokens_per_sec
+        assert est.per_machine == best.per_machine
+
+
+def test_estimate_system_throughput_errors_in_config_order(eng):
+    case = next(c for c in SEARCH if c["name"] == "mixed_failures")
+    cluster = H.cluster_from(case["profile"])
+    params_by = H.params_from(case["profile"])
+    requests = H.search_trace(case)
+    for degrees, reason in case["infeasible"][:12]:
+        cfg = hs.deployment_for(cluster.machines, {m.name: t for m, t in zip(cluster.machines, degrees)})
+        with pytest.raises((hs.InfeasibleConfigError, hs.InfeasibleRequestError, hs.SpecError)) as ei:
+            hs.estimate_system_throughput(cluster, cfg, requests, params_by, engine=eng)
+        assert str(ei.value) == reason
+
+
+def _config3_tables(eng):
+    case = next(c for c in SEARCH if c["name"] == "config3_table")
+    cluster = H.cluster_from(case["profile"])
+    params_by = H.params_from(case["profile"])
+    requests = H.search_trace(case)
+    return case, requests, planner.build_tables(cluster, requests, params_by, engine=eng)
+
+
+def test_config3_full_space_argmax(eng):
+    """5^16 = 1.5e11 candidates: every one evaluated on the GPU; the winner,
+    its total and the feasible count checked against the exact oracle."""
+    case, requests, t = _config3_tables(eng)
+    H.check_table(case, t.entries, t.n_degrees, requests)
+    P = t.space_size
+    assert P == 5**16
+    total, idx, nfeas, _ms = planner.search_best(t, engine=eng)
+    V, vidx, vfeas = orc.best_monotone(t.entries, t.n_degrees)
+    assert (total.hex(), idx, nfeas) == (V.hex(), vidx, vfeas)
+    # the winner re-scored through the table equals the reported total
+    assert planner.best_config(t, idx).system_tokens_per_sec == total
+
+
+def test_config3_sharded_ranges_combine(eng):
+    _case, _req, t = _config3_tables(eng)
+    P = t.space_size
+    cuts = [0, P // 7, P // 3, P // 3 + 12345, (2 * P) // 3, P]
+    parts = [planner.search_best(t, a, b, engine=eng) for a, b in zip(cuts, cuts[1:])]
+    best = max(((p[0], -p[1]) for p in parts if p[1] >= 0))
+    total, idx, nfeas, _ = planner.search_best(t, engine=eng)
+    assert (best[0], -best[1]) == (total, idx)
+    assert sum(p[2] for p in parts) == nfeas
+
+
+def test_search_best_random_ranges_vs_bruteforce_oracle(eng):
+    _case, _req, t = _config3_tables(eng)
+    P = t.space_size
+    rng = np.random.default_rng(7)
+    for _ in range(6):
+        a = int(rng.integers(0, P - 3_000_000))
+        b = a + int(rng.integers(1, 3_000_000))
+        got = planner.search_best(t, a, b, engine=eng)
+        want = orc.best(t.entries, t.n_degrees, a, b, nthreads=4)
+        assert (got[0], got[1], got[2]) == want or (got[1] == -1 and want[1] == -1 and got[2] == want[2])
+
+
+def test_search_best_small_spaces_vs_rank(eng):
+    """Every search fixture: argmax == head of the full ranking."""
+    for case in SEARCH:
+        if case["kind"] != "search" or not case.get("ranked"):
+            continue
+        cluster = H.cluster_from(case["profile"])
+        t = planner.build_tables(cluster, H.search_trace(case), H.params_from(case["profile"]), engine=eng)
+        total, idx, nfeas, _ = planner.search_best(t, engine=eng)
+        assert total.hex() == case["ranked"][0]["total"]
+        assert nfeas == len(case["ranked"])
+
+
+REPLAY_PARAMS = [(c, k) for c in REPLAY for k in range(len(c["results"]))]
+
+
+@pytest.mark.parametrize("case,k", REPLAY_PARAMS, ids=lambda v: v["name"] if isinstance(v, dict) else str(v))
+def test_run_continuous_matches_reference(eng, case, k):
+    want = case["results"][k]
+    sc = H.scenario_from(case, want["policy"])
+    if "error" in want:
+        exc = {"InfeasibleRequestError": hs.InfeasibleRequestError, "OverflowError": OverflowError,
+               "SpecError": hs.SpecError, "SchedulingError": hs.SchedulingError}[want["error"]]
+        with pytest.raises(exc) as ei:
+            hs.run_continuous(sc, engine=eng)
+        assert str(ei.value) == want["msg"]
+        return
+    got = H.sim_digest(hs.run_continuous(sc, engine=eng))
+    for key, val in want.items():
+        assert got[key] == val, (case["name"], want["policy"], key)
+
+
+@pytest.mark.parametrize("policy", ["OS", "RR", "WRR", "SI", "MB"])
+def test_batched_replay_vs_oracle(eng, policy):
+    """64 ragged config-4-shaped traces (incl. an empty one) at mixed rates."""
+    prof = wl.config4()
+    cluster = H.cluster_from({"model": prof.model, "engine": {"mem_utilization_fraction": (0.9).hex(),
+                              "static_overhead_bytes": prof.engine["static_overhead_bytes"]},
+                              "limits": prof.limits, "machines": [list(m) for m in prof.machines], "params": []})
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {a: 1 for a in wl.CONFIG4_TYPES})
+    rng = np.random.default_rng(99)
+    lens = [int(x) for x in rng.integers(0, 1500, 64)]
+    lens[5] = 0
+    Is, Os, Ts = [], [], []
+    for t, q in enumerate(lens):
+        I, O = wl.trace_lengths(q, seed=1000 + t)
+        rate = [20.0, 140.0, 1500.0, math.inf][t % 4]
+        Is.append(I)
+        Os.append(O)
+        Ts.append(np.zeros(q) if math.isinf(rate) else wl.arrivals(q, rate, seed=t))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    I, O, T = np.concatenate(Is), np.concatenate(Os), np.concatenate(Ts)
+    wrr = tuple(float(x) for x in rng.integers(1, 5, 32)) if policy == "WRR" else None
+    pol = hs.PolicyConfig(policy=policy, theta=2.0, wrr_weights=wrr)
+    res = hs.replay_traces(cluster, config, params, pol, off, I, O, O, arrival=T, want_assign=True,
+                           want_depart=True, engine=eng)
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    handles = build_instances(cluster, config, params)
+    a, d, m, r = orc.replay(engine_instances(handles, pol), _policy_struct(pol, 32, hs.kv_bytes_per_token(cluster.model)),
+                            off, I, O, O, T, nthreads=8)
+    assert (res.result["error"] == 0).all() and (r["error"] == 0).all()
+    assert np.array_equal(res.assign, a)
+    assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64))
+    for f in ("completion_time", "peak_kv_usage", "residual_load"):
+        assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
+    for f in ("request_count", "token_count"):
+        assert np.array_equal(res.metrics[f], m[f]), f
