@@ -1,0 +1,456 @@
+#!/usr/bin/env python
+"""Benchmark: deployment configs evaluated/sec + simulated requests/sec.
+
+One step = one pass of the hot path over one batch of synthetic input:
+  * search   -- BASELINE config 3 (8 accelerator types x 2 machines x 16
+                GPUs, 70B-class, 10k-request trace): K1 table build and K2
+                exhaustive argmax over all 5^16 = 1.53e11 candidates;
+  * replay   -- BASELINE config 4 (4096 Poisson traces x 100k requests at
+                140 req/s on 32 heterogeneous instances, OS policy): K3;
+  * combine  -- per-GPU search winners reduced with one NCCL all-reduce.
+Units per step = candidates evaluated + requests simulated (dispatched and
+run to completion); value = units / step time (max over ranks).  N GPUs
+split the candidate range and the trace batch (strong scaling: the total
+work is fixed).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "deployment configs evaluated/sec + simulated requests/sec at 1/2/4/8 B200"
+UNIT = "(configs + requests)/s"
+BYTES_PER_DISPATCH = 21  # I, O, Opred int32 + arrival fp64 + assignment u8
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
+    ap.add_argument("--traces", type=int, default=4096)
+    ap.add_argument("--q", type=int, default=100_000)
+    ap.add_argument("--rate", type=float, default=140.0)
+    ap.add_argument("--search-q", type=int, default=10_000)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- inputs
+def search_inputs(q: int):
+    import paper_2504_15303_b200 as hs
+    from paper_2504_15303_b200 import workloads as wl
+    prof = wl.config3()
+    cluster = hs.ClusterSpec(
+        model=hs.ModelSpec(**prof.model), engine=hs.EngineOverheads(**prof.engine),
+        machines=tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+        limits=hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    I, O = wl.trace_lengths(q, seed=3)
+    reqs = [hs.Request(f"r{k}", int(I[k]), int(O[k]), int(O[k])) for k in range(q)]
+    return cluster, reqs, params, I, O
+
+
+def replay_deployment():
+    import paper_2504_15303_b200 as hs
+    from paper_2504_15303_b200 import workloads as wl
+    prof = wl.config4()
+    cluster = hs.ClusterSpec(
+        model=hs.ModelSpec(**prof.model), engine=hs.EngineOverheads(**prof.engine),
+        machines=tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+        limits=hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {a: 1 for a in wl.CONFIG4_TYPES})
+    return cluster, config, params
+
+
+def replay_inputs(t_lo: int, t_hi: int, q: int, rate: float, out=None):
+    """Traces t_lo..t_hi-1: lengths seeded by trace index, arrivals by 42+t."""
+    from paper_2504_15303_b200 import workloads as wl
+    n = t_hi - t_lo
+    if out is None:
+        out = (np.empty(n * q, np.int32), np.empty(n * q, np.int32), np.empty(n * q, np.float64))
+    I, O, T = out
+
+    def one(k):
+        t = t_lo + k
+        i, o = wl.trace_lengths(q, seed=t)
+        I[k * q:(k + 1) * q] = i
+        O[k * q:(k + 1) * q] = o
+        T[k * q:(k + 1) * q] = wl.arrivals(q, rate, seed=42 + t)
+
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
+        list(ex.map(one, range(n)))
+    offsets = np.arange(n + 1, dtype=np.int64) * q
+    return offsets, I, O, T
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(target_s: float, P: int, R_total: int, q: int, rate: float):
+    """The reference's algorithm, restated in C (oracle/, kind "port"), on the
+    host cores: the literal per-candidate estimate_system_throughput on
+    random candidates of config 3 and literal run_continuous on config-4
+    traces; extrapolated to the full step workload."""
+    from oracle import hs_oracle as orc
+    import paper_2504_15303_b200 as hs
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    sys.path.insert(0, str(ROOT / "tests"))
+    cores = len(os.sched_getaffinity(0))
+    cluster, reqs, params, I, O = search_inputs(10_000)
+    from helpers import search_structs
+    model, engine, limits, machines, pr, present = search_structs(cluster, params)
+    rng = np.random.default_rng(1)
+    # calibrate the candidate sample to ~half of the budget
+    n_c = cores * 64
+    t0 = time.perf_counter()
+    orc.candidates_literal(model, engine, limits, machines, pr, present, I, O, rng.integers(0, P, n_c), cores)
+    dt = time.perf_counter() - t0
+    n_c = max(cores, int(n_c * (0.45 * target_s) / max(dt, 1e-6)))
+    idx = rng.integers(0, P, n_c)
+    t0 = time.perf_counter()
+    orc.candidates_literal(model, engine, limits, machines, pr, present, I, O, idx, cores)
+    t_search = time.perf_counter() - t0
+    cand_rate = n_c / t_search
+    # replay sample: `cores` traces in parallel, shortened if one would take too long
+    rc, config, rparams = replay_deployment()
+    handles = build_instances(rc, config, rparams)
+    pol = hs.PolicyConfig()
+    inst = engine_instances(handles, pol)
+    ps = _policy_struct(pol, len(handles), hs.kv_bytes_per_token(rc.model))
+    q_s = min(q, 20_000)
+    off, Ir, Or, Tr = replay_inputs(0, cores, q_s, rate)
+    t0 = time.perf_counter()
+    orc.replay(inst, ps, off, Ir, Or, Or, Tr, nthreads=cores, want_depart=False)
+    t_rep = time.perf_counter() - t0
+    req_rate = (cores * q_s) / t_rep
+    value = (P + R_total) / (P / cand_rate + R_total / req_rate)
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": (f"oracle/hs_oracle.c on {cores} threads: literal estimate_system_throughput on {n_c} random "
+                       f"config-3 candidates ({t_search:.1f}s, {cand_rate:.3g} cand/s) + literal run_continuous on "
+                       f"{cores} config-4 traces x {q_s} requests ({t_rep:.1f}s, {req_rate:.3g} req/s); "
+                       f"extrapolated to the step's {P:.3g} candidates + {R_total:.3g} requests"),
+            "configs_per_s": cand_rate, "requests_per_s": req_rate}
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    P = 5**16
+    R = args.traces * args.q
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(args.cpu_seconds / 3, P, R, args.q, args.rate)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(args.cpu_seconds, P, R, args.q, args.rate))
+    v = statistics.median(x["value"] for x in vals)
+    last = vals[-1]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": (P + R) / v * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
+        "config": {"workload": "config3 search (5^16 candidates, 70B, 10k trace) + config4 replay "
+                               f"({args.traces} traces x {args.q} requests, 32 instances, {args.rate} req/s, OS)",
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port", "sample": last["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "breakdown": {"configs_per_s": last["configs_per_s"], "requests_per_s": last["requests_per_s"]},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ engine
+def engine_arm(args, rank, world, local_rank):
+    import torch
+
+    import paper_2504_15303_b200 as hs
+    from paper_2504_15303_b200 import _native as nat
+    from paper_2504_15303_b200 import planner
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    eng = nat.engine_for(local_rank)
+    ext = torch.cuda.ExternalStream(eng.stream, device=dev)
+
+    def barrier():
+        if dist:
+            tdist.barrier(device_ids=[local_rank])
+
+    # ---- search inputs (every rank builds the same table; shards the index range)
+    cluster, reqs, params, sI, sO = search_inputs(args.search_q)
+    tables = planner.build_tables(cluster, reqs, params, engine=eng)
+    P = tables.space_size
+    lo, hi = P * rank // world, P * (rank + 1) // world
+    # ---- replay inputs (trace shard)
+    T_lo, T_hi = args.traces * rank // world, args.traces * (rank + 1) // world
+    nT = T_hi - T_lo
+    t0 = time.time()
+    off, I, O, T = replay_inputs(T_lo, T_hi, args.q, args.rate)
+    gen_s = time.time() - t0
+    rc, config, rparams = replay_deployment()
+    handles = build_instances(rc, config, rparams)
+    N = len(handles)
+    pol = hs.PolicyConfig()
+    inst = engine_instances(handles, pol)
+    ps = _policy_struct(pol, N, hs.kv_bytes_per_token(rc.model))
+    nreq = int(off[-1])
+    d = {}
+    for name, arr in (("off", off), ("I", I), ("O", O), ("T", T)):
+        d[name] = eng.device_alloc(arr.nbytes)
+        eng.h2d(d[name], arr)
+    d["assign"] = eng.device_alloc(max(nreq, 1))
+    d["metrics"] = eng.device_alloc(max(nT * N, 1) * nat.METRICS_DTYPE.itemsize)
+    d["result"] = eng.device_alloc(max(nT, 1) * nat.RESULT_DTYPE.itemsize)
+
+    win = torch.zeros(world, 3, dtype=torch.int64, device=dev)
+
+    def combine(total, idx, nfeas):
+        """One NCCL all-reduce of a per-rank slot buffer, then a local
+        lexicographic reduce (max total, then lowest index)."""
+        if not dist:
+            return total, idx, nfeas
+        with torch.cuda.stream(ext):
+            win.zero_()
+            win[rank, 0] = int(np.float64(total).view(np.int64))
+            win[rank, 1] = idx
+            win[rank, 2] = nfeas
+            tdist.all_reduce(win)
+            h = win.cpu().numpy()
+        best = (0.0, -1)
+        for r in range(world):
+            t = float(np.int64(h[r, 0]).view(np.float64))
+            i = int(h[r, 1])
+            if i >= 0 and (best[1] < 0 or t > best[0] or (t == best[0] and i < best[1])):
+                best = (t, i)
+        return best[0], best[1], int(h[:, 2].sum())
+
+    kms = {"k1": [], "k2": [], "k3": []}
+
+    def step():
+        t = planner.build_tables(cluster, reqs, params, engine=eng)
+        kms["k1"].append(eng.last_kernel_ms)
+        total, idx, nfeas, k2 = planner.search_best(t, lo, hi, engine=eng)
+        kms["k2"].append(k2)
+        eng.replay_device(inst, ps, nT, d["off"], d["I"], d["O"], d["O"], d["T"], d["assign"], d["metrics"],
+                          d["result"])
+        kms["k3"].append(eng.last_kernel_ms)
+        return combine(total, idx, nfeas)
+
+    def timed(fn, k):
+        barrier()
+        torch.cuda.synchronize(dev)
+        eng.lib.hs_device_synchronize(eng.handle)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        out = None
+        for _ in range(k):
+            out = fn()
+        e1.record(ext)
+        e1.synchronize()
+        eng.lib.hs_device_synchronize(eng.handle)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = e0.elapsed_time(e1) / k
+        if dist:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, out
+
+    for _ in range(args.warmup):
+        best = step()
+    for k in kms:
+        kms[k].clear()
+    launches0 = eng.launch_count
+    with ClockSampler(local_rank) as clk:
+        ms, best = timed(step, args.steps)
+    launches = (eng.launch_count - launches0) // args.steps
+    res = np.zeros(nT, nat.RESULT_DTYPE)
+    eng.d2h(res, d["result"])
+    assert (res["error"] == 0).all(), "replay reported an error"
+    n_steps_ev = int(res["n_steps"].sum())
+    R_total = args.traces * args.q
+    units = P + R_total
+    value = units / (ms / 1e3)
+
+    # ---- e2e: the public API with host (pinned) buffers, copies inside
+    e2e = None
+    if not args.no_e2e:
+        hI = eng.host_array(I.shape, np.int32); hI[:] = I
+        hO = eng.host_array(O.shape, np.int32); hO[:] = O
+        hT = eng.host_array(T.shape, np.float64); hT[:] = T
+        rc_, config_, rparams_ = rc, config, rparams
+
+        def e2e_step():
+            t = planner.build_tables(cluster, reqs, params, engine=eng)
+            total, idx, nfeas, _ = planner.search_best(t, lo, hi, engine=eng)
+            r = hs.replay_traces(rc_, config_, rparams_, pol, off, hI, hO, hO, arrival=hT, want_assign=True,
+                                 want_depart=False, engine=eng)
+            assert (r.result["error"] == 0).all()
+            return combine(total, idx, nfeas)
+
+        for _ in range(max(1, args.warmup - 1)):
+            e2e_step()
+        e2e_ms, _ = timed(e2e_step, args.steps)
+        M = len(tables.names)
+        h2d = sI.nbytes + sO.nbytes + off.nbytes + hI.nbytes + hO.nbytes * 2 + hT.nbytes
+        d2h = nreq + nT * N * nat.METRICS_DTYPE.itemsize + nT * nat.RESULT_DTYPE.itemsize + \
+            M * nat.HS_MAX_DEGREES * nat.ENTRY_DTYPE.itemsize + 16
+        if dist:
+            h2d += 0
+            d2h += world * 24
+        e2e = {"value": units / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
+               "d2h_bytes_per_step": int(d2h * world), "ms_per_step": e2e_ms}
+
+    # ---- roofline of the dominant kernel (K3 replay)
+    peaks = {}
+    pf = ROOT / "MEASURED_PEAKS.json"
+    if pf.exists():
+        peaks = json.loads(pf.read_text())
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    k3 = statistics.median(kms["k3"])
+    k2 = statistics.median(kms["k2"])
+    k1 = statistics.median(kms["k1"])
+    achieved = BYTES_PER_DISPATCH * nreq / (k3 / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "k3_replay_ncu.json"
+    if prof.exists():
+        pj = json.loads(prof.read_text())
+        if pj.get("dram_bytes_per_dispatch"):
+            traffic = pj["dram_bytes_per_dispatch"] * nreq
+    fp64_peak = eng.probe_fp64()
+    cand_local = hi - lo
+    k2_fp64 = 2.0 * cand_local / (k2 / 1e3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_seconds, P, R_total, args.q, args.rate)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (seeded numpy traces, gen-trace shapes)",
+            "config": {"workload": "config3 search (5^16 candidates, 70B, 10k trace) + config4 replay "
+                                   f"({args.traces} traces x {args.q} requests, 32 instances, {args.rate} req/s, OS)",
+                       "candidates": P, "requests": R_total, "parallelism": f"shard{world}",
+                       "l2": "inputs larger than L2 (replay inputs %.1f GB)" % ((I.nbytes * 3 + T.nbytes) * world / 1e9)},
+            "breakdown": {"k1_table_ms": k1, "k2_search_ms": k2, "k3_replay_ms": k3,
+                          "configs_per_s": P / (k2 / 1e3) if world == 1 else cand_local / (k2 / 1e3) * world,
+                          "requests_per_s_kernel": nreq / (k3 / 1e3) * world,
+                          "step_events_per_request": n_steps_ev / max(nreq, 1),
+                          "best_total": best[0], "best_index": best[1], "n_feasible": best[2],
+                          "trace_gen_s": gen_s},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "k_replay",
+                         "note": "replay is latency-bound (dependent event chains); see DESIGN.md"},
+            "roofline_k2": {"bound": "fp64", "achieved": k2_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
+                            "frac": k2_fp64 / fp64_peak, "kernel": "k_search_best",
+                            "peak_source": "hs_probe_fp64 DADD throughput measured in this run"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.barrier(device_ids=[local_rank])
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    engine_arm(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -186,9 +186,13 @@ int hs_ctx_destroy(hs_ctx* ctx);
 const char* hs_last_error(void);
 /* Kernel launches issued by this context since creation (evidence counter). */
 int64_t hs_ctx_launch_count(const hs_ctx* ctx);
-/* Device milliseconds of the last call's kernels (CUDA events on the
- * context's stream, excluding host<->device copies). */
+/* Device milliseconds of the last call's main kernel(s) (CUDA events on the
+ * context's stream around the launches only: no copies, no host work). */
 double hs_ctx_last_kernel_ms(const hs_ctx* ctx);
+/* The context's cudaStream_t (so callers can bracket work with events). */
+void* hs_ctx_stream(const hs_ctx* ctx);
+/* Diagnostic: measured FP64 add throughput of this device (DADD/s). */
+int hs_probe_fp64(hs_ctx* ctx, double* dadd_per_s);
 
 /* ---- deployment search ------------------------------------------------ */
 /* Fill table[i * HS_MAX_DEGREES + d] for d < n_degrees[i] (degree list =

@@ -294,6 +294,45 @@ double hs_oracle_candidate_literal(const hs_model* model, const hs_engine* engin
   return total;
 }
 
+typedef struct {
+  const hs_model* model; const hs_engine* engine; const hs_limits* limits; const hs_machine* machines;
+  int32_t M; const double* params; const uint8_t* present; const int32_t* I; const int32_t* O; int64_t q;
+  const int64_t* idx; int64_t n; double* totals; int32_t* first_bad; int64_t* next; pthread_mutex_t* mu;
+} lit_job_t;
+
+static void* literal_worker(void* arg) {
+  lit_job_t* j = (lit_job_t*)arg;
+  for (;;) {
+    pthread_mutex_lock(j->mu);
+    int64_t k = (*j->next)++;
+    pthread_mutex_unlock(j->mu);
+    if (k >= j->n) break;
+    int32_t fb, st;
+    double t = hs_oracle_candidate_literal(j->model, j->engine, j->limits, j->machines, j->M, j->params,
+                                           j->present, j->I, j->O, j->q, j->idx[k], &fb, &st);
+    j->totals[k] = t;
+    j->first_bad[k] = fb;
+  }
+  return NULL;
+}
+
+/* The literal per-candidate reference loop over a list of candidate indices,
+ * spread over nthreads (used as the CPU baseline of the search). */
+int hs_oracle_candidates_literal(const hs_model* model, const hs_engine* engine, const hs_limits* limits,
+                                 const hs_machine* machines, int32_t M, const double* params,
+                                 const uint8_t* present, const int32_t* I, const int32_t* O, int64_t q,
+                                 const int64_t* idx, int64_t n, int nthreads, double* totals, int32_t* first_bad) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
+  int64_t next = 0;
+  lit_job_t job = {model, engine, limits, machines, M, params, present, I, O, q, idx, n, totals, first_bad, &next, &mu};
+  for (int k = 0; k < nthreads; ++k) pthread_create(&th[k], NULL, literal_worker, &job);
+  for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
+  return HS_OK;
+}
+
 /* candidate total from the table, reference order (planner.py:151,180) */
 static double table_total(const hs_entry* table, int32_t M, const int32_t* digit, int32_t* first_bad) {
   double acc = 0.0;

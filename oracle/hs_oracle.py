@@ -43,6 +43,8 @@ def lib() -> C.CDLL:
         L.hs_oracle_candidate_literal.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, i64,
                                                   C.POINTER(i32), C.POINTER(i32)]
         L.hs_oracle_candidate_literal.restype = dbl
+        L.hs_oracle_candidates_literal.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, i64, C.c_int, vp, vp]
+        L.hs_oracle_candidates_literal.restype = C.c_int
         L.hs_oracle_best.argtypes = [vp, vp, i32, i64, i64, C.c_int, vp, vp]
         L.hs_oracle_best.restype = C.c_int
         L.hs_oracle_rank.argtypes = [vp, vp, i32, vp, vp, vp]
@@ -94,6 +96,20 @@ def candidate_literal(model, engine, limits, machines, params, present, I, O, in
                                           C.cast(machines, C.c_void_p), len(machines), _p(params), _p(present),
                                           _p(I), _p(O), len(I), int(index), C.byref(fb), C.byref(st))
     return t, fb.value, st.value
+
+
+def candidates_literal(model, engine, limits, machines, params, present, I, O, indices, nthreads=1):
+    idx = np.ascontiguousarray(indices, np.int64)
+    totals = np.zeros(max(len(idx), 1), np.float64)
+    fb = np.zeros(max(len(idx), 1), np.int32)
+    I = np.ascontiguousarray(I, np.int32)
+    O = np.ascontiguousarray(O, np.int32)
+    rc = lib().hs_oracle_candidates_literal(C.byref(model), C.byref(engine), C.byref(limits),
+                                            C.cast(machines, C.c_void_p), len(machines), _p(params), _p(present),
+                                            _p(I), _p(O), len(I), _p(idx), len(idx), int(nthreads), _p(totals),
+                                            _p(fb))
+    assert rc == 0
+    return totals[: len(idx)], fb[: len(idx)]
 
 
 def best(table, nd, begin, end, nthreads=1):

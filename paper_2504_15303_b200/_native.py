@@ -107,7 +107,7 @@ EXPORTS = (
     "hs_abi_version", "hs_ctx_create", "hs_ctx_destroy", "hs_last_error", "hs_ctx_launch_count",
     "hs_ctx_last_kernel_ms", "hs_search_tables", "hs_search_best", "hs_search_rank", "hs_replay",
     "hs_replay_device", "hs_device_alloc", "hs_device_free", "hs_memcpy_h2d", "hs_memcpy_d2h",
-    "hs_device_synchronize", "hs_host_alloc", "hs_host_free",
+    "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
 )
 
 _lib = None
@@ -144,6 +144,8 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_device_synchronize": ([vp], C.c_int),
             "hs_host_alloc": ([vp, i64, C.POINTER(vp)], C.c_int),
             "hs_host_free": ([vp, vp], C.c_int),
+            "hs_ctx_stream": ([vp], vp),
+            "hs_probe_fp64": ([vp, C.POINTER(dbl)], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -180,6 +182,9 @@ class Engine:
             raise EngineError(rc, f"{what}: {self._err()}")
 
     def close(self) -> None:
+        for p in getattr(self, "_pinned", []):
+            self.lib.hs_host_free(self.handle, C.c_void_p(p))
+        self._pinned = []
         if getattr(self, "handle", None):
             self.lib.hs_ctx_destroy(self.handle)
             self.handle = None
@@ -197,6 +202,50 @@ class Engine:
     @property
     def last_kernel_ms(self) -> float:
         return float(self.lib.hs_ctx_last_kernel_ms(self.handle))
+
+    @property
+    def stream(self) -> int:
+        """cudaStream_t of this context (for torch.cuda.ExternalStream)."""
+        return int(self.lib.hs_ctx_stream(self.handle) or 0)
+
+    def probe_fp64(self) -> float:
+        v = C.c_double()
+        self.check(self.lib.hs_probe_fp64(self.handle, C.byref(v)), "hs_probe_fp64")
+        return float(v.value)
+
+    # ------------------------------------------------------- raw buffers
+    def device_alloc(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        self.check(self.lib.hs_device_alloc(self.handle, int(nbytes), C.byref(p)), "hs_device_alloc")
+        return int(p.value)
+
+    def device_free(self, ptr: int) -> None:
+        self.check(self.lib.hs_device_free(self.handle, C.c_void_p(ptr)), "hs_device_free")
+
+    def h2d(self, dst: int, src: np.ndarray) -> None:
+        self.check(self.lib.hs_memcpy_h2d(self.handle, C.c_void_p(dst), _ptr(src), src.nbytes), "hs_memcpy_h2d")
+
+    def d2h(self, dst: np.ndarray, src: int) -> None:
+        self.check(self.lib.hs_memcpy_d2h(self.handle, _ptr(dst), C.c_void_p(src), dst.nbytes), "hs_memcpy_d2h")
+
+    def host_array(self, shape, dtype) -> np.ndarray:
+        """A numpy array over page-locked host memory (freed with the engine)."""
+        dt = np.dtype(dtype)
+        n = int(np.prod(shape)) * dt.itemsize
+        p = C.c_void_p()
+        self.check(self.lib.hs_host_alloc(self.handle, n, C.byref(p)), "hs_host_alloc")
+        buf = (C.c_byte * max(n, 1)).from_address(p.value)
+        self._pinned = getattr(self, "_pinned", [])
+        self._pinned.append(p.value)
+        return np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+    def replay_device(self, instances, policy, n_traces: int, d_off: int, d_I: int, d_O: int, d_P: int,
+                      d_T: int | None, d_assign: int | None, d_metrics: int, d_result: int) -> None:
+        batch = hs_trace_batch(n_traces, d_off, d_I, d_O, d_P, d_T)
+        rc = self.lib.hs_replay_device(self.handle, C.cast(instances, C.c_void_p), C.byref(policy), C.byref(batch),
+                                       None if d_assign is None else C.c_void_p(d_assign), None,
+                                       C.c_void_p(d_metrics), C.c_void_p(d_result))
+        self.check(rc, "hs_replay_device")
 
     # ---------------------------------------------------------------- search
     def search_tables(self, model: hs_model, engine: hs_engine, limits: hs_limits, machines: np.ndarray,

@@ -271,13 +271,26 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
   if (chunk > 16384) chunk = 16384;
   uint64_t* d_heap = nullptr;
   if ((rcode = ensure_t(c, S_HEAP, (size_t)(chunk > 0 ? chunk : 1) * rc.heap_stride, &d_heap))) return rcode;
+  if ((rcode = begin_timing(c))) return rcode;
   for (int64_t t0 = 0; t0 < T; t0 += chunk) {
     const int64_t nt_ = (T - t0) < chunk ? (T - t0) : chunk;
     HS_CUDA(hs::launch_replay(rc, nt_, d_off + t0, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics + t0 * N,
                               d_result + t0, d_wrec, d_qnext, d_heap, c->stream));
     c->launches += 1;
   }
-  return HS_OK;
+  return end_timing(c);
+}
+
+__global__ void k_probe_fp64(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+  double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+  const double b = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+    a0 = __dadd_rn(a0, b); a1 = __dadd_rn(a1, b); a2 = __dadd_rn(a2, b); a3 = __dadd_rn(a3, b);
+    a4 = __dadd_rn(a4, b); a5 = __dadd_rn(a5, b); a6 = __dadd_rn(a6, b); a7 = __dadd_rn(a7, b);
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 42.0) out[0] = s;
 }
 
 }  // namespace
@@ -322,6 +335,25 @@ int hs_ctx_destroy(hs_ctx* c) {
 }
 
 int64_t hs_ctx_launch_count(const hs_ctx* c) { return c ? c->launches : 0; }
+void* hs_ctx_stream(const hs_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int hs_probe_fp64(hs_ctx* c, double* out) {
+  if (!c || !out) return fail(HS_ERR_ARG, "null argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  double* d;
+  if ((rc = ensure_t(c, S_CAND, 2, &d))) return rc;
+  const int blocks = hs::sm_count() * 8, threads = 256, iters = 1 << 14;
+  k_probe_fp64<<<blocks, threads, 0, c->stream>>>(d, 256);  // warm-up
+  HS_CUDA(cudaGetLastError());
+  if ((rc = begin_timing(c))) return rc;
+  k_probe_fp64<<<blocks, threads, 0, c->stream>>>(d, iters);
+  HS_CUDA(cudaGetLastError());
+  if ((rc = end_timing(c))) return rc;
+  c->launches += 2;
+  *out = (double)blocks * threads * iters * 8.0 / (c->last_ms * 1e-3);
+  return HS_OK;
+}
 double hs_ctx_last_kernel_ms(const hs_ctx* c) { return c ? c->last_ms : 0.0; }
 
 int hs_search_tables(hs_ctx* c, const hs_model* model, const hs_engine* engine, const hs_limits* limits,
@@ -511,9 +543,7 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
     HS_CUDA(cudaMemcpyAsync(dP, b->pred_output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
     if (dT) HS_CUDA(cudaMemcpyAsync(dT, b->arrival, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
   }
-  if ((rc = begin_timing(c))) return rc;
   if ((rc = replay_impl(c, inst, pol, T, dOff, off, dI, dO, dP, dT, dA, dDep, dM, dR))) return rc;
-  if ((rc = end_timing(c))) return rc;
   if (T > 0) {
     HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * N, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
@@ -535,12 +565,8 @@ int hs_replay_device(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, c
   std::vector<int64_t> off((size_t)T + 1);
   HS_CUDA(cudaMemcpyAsync(off.data(), b->offsets, sizeof(int64_t) * (T + 1), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  if ((rc = begin_timing(c))) return rc;
-  if ((rc = replay_impl(c, inst, pol, T, b->offsets, off.data(), b->input_len, b->output_len, b->pred_output_len,
-                        b->arrival, assign, depart, metrics, result)))
-    return rc;
-  if ((rc = end_timing(c))) return rc;
-  return HS_OK;
+  return replay_impl(c, inst, pol, T, b->offsets, off.data(), b->input_len, b->output_len, b->pred_output_len,
+                     b->arrival, assign, depart, metrics, result);
 }
 
 int hs_device_alloc(hs_ctx* c, int64_t bytes, void** out) {

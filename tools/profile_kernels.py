@@ -1,0 +1,46 @@
+"""Small fixed workloads for ncu captures of the engine's kernels.
+
+    python tools/profile_kernels.py replay [traces] [q]
+    python tools/profile_kernels.py search
+
+Runs one warm-up call and one measured call; prints the kernel time.
+"""
+
+from __future__ import annotations
+
+import pathlib
+import sys
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402
+import paper_2504_15303_b200 as hs  # noqa: E402
+from paper_2504_15303_b200 import _native as nat  # noqa: E402
+from paper_2504_15303_b200 import planner  # noqa: E402
+
+
+def main():
+    what = sys.argv[1] if len(sys.argv) > 1 else "replay"
+    eng = nat.engine_for(0)
+    if what == "replay":
+        T = int(sys.argv[2]) if len(sys.argv) > 2 else 1184
+        q = int(sys.argv[3]) if len(sys.argv) > 3 else 20_000
+        off, I, O, Tarr = bench.replay_inputs(0, T, q, 140.0)
+        rc, config, params = bench.replay_deployment()
+        for _ in range(2):
+            r = hs.replay_traces(rc, config, params, hs.PolicyConfig(), off, I, O, O, arrival=Tarr,
+                                 want_assign=True, engine=eng)
+        assert (r.result["error"] == 0).all()
+        print(f"replay {T} traces x {q}: {r.kernel_ms:.2f} ms, {T * q / r.kernel_ms * 1e3:.3g} req/s, "
+              f"{r.result['n_steps'].sum() / (T * q):.1f} steps/request")
+    else:
+        cluster, reqs, params, _I, _O = bench.search_inputs(10_000)
+        t = planner.build_tables(cluster, reqs, params, engine=eng)
+        for _ in range(2):
+            total, idx, nf, ms = planner.search_best(t, engine=eng)
+        print(f"search {t.space_size} candidates: {ms:.2f} ms, {t.space_size / ms * 1e3:.3g} cand/s; best {idx}")
+
+
+if __name__ == "__main__":
+    main()
