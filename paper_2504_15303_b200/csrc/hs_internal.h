@@ -26,10 +26,10 @@ struct SearchConst {
   int64_t q;
 };
 
-// Product space for K2: machines padded to M >= 2 (a leading virtual
-// machine with one degree and contribution +0.0 leaves every total
-// unchanged: 0.0 + 0.0 + C0 == 0.0 + C0).
-constexpr int kMaxM = HS_MAX_MACHINES + 1;
+// Product space for K2: machines padded to M >= 3 (leading virtual
+// machines with one degree and contribution +0.0 leave every total
+// unchanged: (0.0 + 0.0) + C0 == 0.0 + C0).
+constexpr int kMaxM = HS_MAX_MACHINES + 2;
 struct SpaceDesc {
   int32_t M;
   int32_t D[kMaxM];

@@ -154,47 +154,56 @@ cudaError_t launch_table_build(const EntryDesc* d_desc, int n, const SearchConst
 // ----------------------------------------------------------------- K2
 __constant__ SpaceDesc c_space;
 
-// Fully unrolled innermost level for a compile-time innermost radix DL.
-template <int DL>
-struct Inner {
-  // Evaluates the D1*DL candidates of one item (prefix s); returns true if
-  // any total is > best.
-  static __device__ __forceinline__ bool any_gt(double s, const double* C1, int D1, const double* CL,
-                                                double best) {
-    bool hit = false;
-    for (int d1 = 0; d1 < D1; ++d1) {
-      const double v1 = __dadd_rn(s, C1[d1]);
-#pragma unroll
-      for (int d2 = 0; d2 < DL; ++d2) hit |= __dadd_rn(v1, CL[d2]) > best;
-    }
-    return hit;
-  }
+// Levels of the product space (SpaceDesc is padded to M >= 3):
+//   outer  machines 0 .. M-4   odometer, once per item (prefix sums kept)
+//   mid    machine  M-3        runtime loop, contributions in shared memory
+//   inner1 machine  M-2        compile-time radix D1 (registers)
+//   inner2 machine  M-1        compile-time radix DL (registers)
+// An item = one outer prefix = D2*D1*DL candidates.  Per candidate the fast
+// path issues one DADD (prefix + last contribution, the reference's own
+// left-to-right order) and one DSETP.GT.OR into the `hit` predicate.
+// h |= (v > b) as one DSETP.GT.OR per candidate (left to nvcc, a run of
+// `hit |= v > best` is rewritten into a max-reduction costing ~8 ALU ops
+// per candidate; ptxas folds the selp/setp pairs of consecutive calls).
+__device__ __forceinline__ void gt_or(double v, double b, unsigned& h) {
+  asm("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %0, 0;\n\tsetp.gt.or.f64 p, %1, %2, q;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "+r"(h)
+      : "d"(v), "d"(b));
+}
+
+template <int D1, int DL>
+struct Radix {
+  static constexpr bool kStatic = D1 > 0 && DL > 0;
 };
 
-// Slow path: scan one item in index order, tracking (best, lowest index).
-// Candidates outside [lo, hi) (item-relative) are skipped.
-__device__ __forceinline__ void item_scan(double s, bool prefix_ok, const double* C1, int D1, const double* CL,
-                                          int DL, int64_t base, int64_t lo, int64_t hi, double& best,
-                                          int64_t& bidx, int64_t& cnt, bool count) {
-  const int M = c_space.M;
-  for (int d1 = 0; d1 < D1; ++d1) {
-    const double v1 = __dadd_rn(s, C1[d1]);
-    for (int d2 = 0; d2 < DL; ++d2) {
-      const int64_t c = (int64_t)d1 * DL + d2;
-      if (c < lo || c >= hi) continue;
-      const double v = __dadd_rn(v1, CL[d2]);
-      const bool ok = prefix_ok && c_space.C[(M - 2) * HS_MAX_DEGREES + d1] != -INFINITY &&
-                      c_space.C[(M - 1) * HS_MAX_DEGREES + d2] != -INFINITY;
-      if (count && ok) ++cnt;
-      if (ok && v > best) {
-        best = v;
-        bidx = base + c;
+// Slow path: scan one item in index order, tracking (best, lowest index);
+// candidates outside [lo, hi) (item-relative) are skipped.
+__device__ __noinline__ void item_scan(const double* sC, int M, double s, bool prefix_ok, int64_t base, int64_t lo,
+                                       int64_t hi, double& best, int64_t& bidx, int64_t& cnt, bool count) {
+  const int D2 = c_space.D[M - 3], D1 = c_space.D[M - 2], DL = c_space.D[M - 1];
+  const double* C2 = &sC[(M - 3) * HS_MAX_DEGREES];
+  const double* C1 = &sC[(M - 2) * HS_MAX_DEGREES];
+  const double* CL = &sC[(M - 1) * HS_MAX_DEGREES];
+  int64_t c = 0;
+  for (int d2 = 0; d2 < D2; ++d2) {
+    const double s2 = __dadd_rn(s, C2[d2]);
+    for (int d1 = 0; d1 < D1; ++d1) {
+      const double v1 = __dadd_rn(s2, C1[d1]);
+      for (int dl = 0; dl < DL; ++dl, ++c) {
+        if (c < lo || c >= hi) continue;
+        const double v = __dadd_rn(v1, CL[dl]);
+        const bool ok = prefix_ok && C2[d2] != -INFINITY && C1[d1] != -INFINITY && CL[dl] != -INFINITY;
+        if (count && ok) ++cnt;
+        if (ok && v > best) {
+          best = v;
+          bidx = base + c;
+        }
       }
     }
   }
 }
 
-template <int DL>
+template <int D1, int DL>
 __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t item_end, int64_t begin,
                                                      int64_t end, int64_t chunk, double* blk_best,
                                                      int64_t* blk_idx, int64_t* blk_cnt) {
@@ -204,17 +213,16 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
   const int M = c_space.M;
   for (int k = threadIdx.x; k < M * HS_MAX_DEGREES; k += blockDim.x) sC[k] = c_space.C[k];
   __syncthreads();
-  const int D1 = c_space.D[M - 2];
-  const int DLr = DL > 0 ? DL : c_space.D[M - 1];
-  const int64_t Din = (int64_t)D1 * DLr;
-  const double* C1 = &sC[(M - 2) * HS_MAX_DEGREES];
-  double CL[DL > 0 ? DL : 1];
-  if (DL > 0) {
+  const int D2 = c_space.D[M - 3];
+  const int64_t Din = (int64_t)D2 * c_space.D[M - 2] * c_space.D[M - 1];
+  const int64_t inner_ok = c_space.okcnt[M - 3] * c_space.okcnt[M - 2] * c_space.okcnt[M - 1];
+  const double* C2 = &sC[(M - 3) * HS_MAX_DEGREES];
+  constexpr int R1 = D1 > 0 ? D1 : 1, RL = DL > 0 ? DL : 1;
+  double C1[R1], CL[RL];
 #pragma unroll
-    for (int d = 0; d < (DL > 0 ? DL : 1); ++d) CL[d] = sC[(M - 1) * HS_MAX_DEGREES + d];
-  }
-  const double* CLp = DL > 0 ? CL : &sC[(M - 1) * HS_MAX_DEGREES];
-  const int64_t inner_ok = c_space.okcnt[M - 2] * c_space.okcnt[M - 1];
+  for (int d = 0; d < R1; ++d) C1[d] = sC[(M - 2) * HS_MAX_DEGREES + d];
+#pragma unroll
+  for (int d = 0; d < RL; ++d) CL[d] = sC[(M - 1) * HS_MAX_DEGREES + d];
 
   double best = -INFINITY;
   int64_t bidx = -1, cnt = 0;
@@ -223,52 +231,67 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
   int64_t it_end = it + chunk;
   if (it_end > item_end) it_end = item_end;
   if (it < it_end) {
-    // decode the outer digits of the first item (machines 0..M-3)
+    const int nouter = M - 3;  // machines 0 .. nouter-1
     int32_t dig[kMaxM];
     double ps[kMaxM];  // ps[i] = left-to-right sum of machines 0..i
     int64_t x = it;
-    for (int i = M - 3; i >= 0; --i) {
+    for (int i = nouter - 1; i >= 0; --i) {
       dig[i] = (int32_t)(x % c_space.D[i]);
       x /= c_space.D[i];
     }
     double acc = 0.0;
-    for (int i = 0; i <= M - 3; ++i) {
+    for (int i = 0; i < nouter; ++i) {
       acc = __dadd_rn(acc, sC[i * HS_MAX_DEGREES + dig[i]]);
       ps[i] = acc;
     }
+    double s = nouter > 0 ? ps[nouter - 1] : 0.0;
     for (; it < it_end; ++it) {
-      const double s = M >= 3 ? ps[M - 3] : 0.0;
       const bool prefix_ok = s != -INFINITY && s == s;
       const int64_t base = it * Din;
-      const bool partial = base < begin || base + Din > end;
-      if (partial) {
-        item_scan(s, prefix_ok, C1, D1, CLp, DLr, base, begin - base, end - base, best, bidx, cnt, true);
+      if (base < begin || base + Din > end) {
+        item_scan(sC, M, s, prefix_ok, base, begin - base, end - base, best, bidx, cnt, true);
       } else {
-        bool hit;
-        if (DL > 0) {
-          hit = Inner<(DL > 0 ? DL : 1)>::any_gt(s, C1, D1, CLp, best);
+        unsigned hit = 0;
+        if (Radix<D1, DL>::kStatic) {
+          for (int d2 = 0; d2 < D2; ++d2) {
+            const double s2 = __dadd_rn(s, C2[d2]);
+#pragma unroll
+            for (int d1 = 0; d1 < R1; ++d1) {
+              const double v1 = __dadd_rn(s2, C1[d1]);
+#pragma unroll
+              for (int dl = 0; dl < RL; ++dl) gt_or(__dadd_rn(v1, CL[dl]), best, hit);
+            }
+          }
         } else {
-          hit = false;
-          for (int d1 = 0; d1 < D1; ++d1) {
-            const double v1 = __dadd_rn(s, C1[d1]);
-            for (int d2 = 0; d2 < DLr; ++d2) hit |= __dadd_rn(v1, CLp[d2]) > best;
+          const int rD1 = c_space.D[M - 2], rDL = c_space.D[M - 1];
+          const double* g1 = &sC[(M - 2) * HS_MAX_DEGREES];
+          const double* gl = &sC[(M - 1) * HS_MAX_DEGREES];
+          for (int d2 = 0; d2 < D2; ++d2) {
+            const double s2 = __dadd_rn(s, C2[d2]);
+            for (int d1 = 0; d1 < rD1; ++d1) {
+              const double v1 = __dadd_rn(s2, g1[d1]);
+              for (int dl = 0; dl < rDL; ++dl) gt_or(__dadd_rn(v1, gl[dl]), best, hit);
+            }
           }
         }
-        if (hit) item_scan(s, prefix_ok, C1, D1, CLp, DLr, base, 0, Din, best, bidx, cnt, false);
+        if (hit) item_scan(sC, M, s, prefix_ok, base, 0, Din, best, bidx, cnt, false);
         if (prefix_ok) cnt += inner_ok;
       }
       // odometer over the outer digits, recomputing the changed prefix sums
-      int i = M - 3;
-      while (i >= 0) {
-        if (++dig[i] < c_space.D[i]) break;
-        dig[i] = 0;
-        --i;
-      }
-      if (i < 0) i = 0;
-      double a = i > 0 ? ps[i - 1] : 0.0;
-      for (int j = i; j <= M - 3; ++j) {
-        a = __dadd_rn(a, sC[j * HS_MAX_DEGREES + dig[j]]);
-        ps[j] = a;
+      if (nouter > 0) {
+        int i = nouter - 1;
+        while (i >= 0) {
+          if (++dig[i] < c_space.D[i]) break;
+          dig[i] = 0;
+          --i;
+        }
+        if (i < 0) i = 0;
+        double a = i > 0 ? ps[i - 1] : 0.0;
+        for (int j = i; j < nouter; ++j) {
+          a = __dadd_rn(a, sC[j * HS_MAX_DEGREES + dig[j]]);
+          ps[j] = a;
+        }
+        s = a;
       }
     }
   }
@@ -350,35 +373,45 @@ __global__ void k_search_final(const double* blk_best, const int64_t* blk_idx, c
   }
 }
 
+using BestKernel = void (*)(int64_t, int64_t, int64_t, int64_t, int64_t, double*, int64_t*, int64_t*);
+constexpr int kMaxStaticRadix = 6;
+
+template <int D1, int DL>
+struct BestTable {
+  static void fill(BestKernel (&t)[kMaxStaticRadix + 1][kMaxStaticRadix + 1]) {
+    t[D1][DL] = k_search_best<D1, DL>;
+    if constexpr (DL < kMaxStaticRadix) {
+      BestTable<D1, DL + 1>::fill(t);
+    } else if constexpr (D1 < kMaxStaticRadix) {
+      BestTable<D1 + 1, 1>::fill(t);
+    }
+  }
+};
+
 cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, int blocks, double* d_blk_best,
                                int64_t* d_blk_idx, int64_t* d_blk_cnt, hs_cand* d_out, int64_t* d_cnt_out,
                                cudaStream_t st) {
+  static BestKernel table[kMaxStaticRadix + 1][kMaxStaticRadix + 1] = {};
+  static bool filled = false;
+  if (!filled) {
+    BestTable<1, 1>::fill(table);
+    filled = true;
+  }
   cudaError_t e = cudaMemcpyToSymbolAsync(c_space, &sd, sizeof(SpaceDesc), 0, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   const int threads = 256;
-  const int64_t Din = (int64_t)sd.D[sd.M - 2] * sd.D[sd.M - 1];
+  const int M = sd.M;
+  const int64_t Din = (int64_t)sd.D[M - 3] * sd.D[M - 2] * sd.D[M - 1];
   const int64_t item_begin = begin / Din;
   const int64_t item_end = end > begin ? (end + Din - 1) / Din : item_begin;
   const int64_t n_items = item_end - item_begin;
   const int64_t nthreads = (int64_t)blocks * threads;
   int64_t chunk = (n_items + nthreads - 1) / nthreads;
   if (chunk < 1) chunk = 1;
-  const int DL = sd.D[sd.M - 1];
-#define HS_LAUNCH_BEST(K)                                                                                   \
-  k_search_best<K><<<blocks, threads, 0, st>>>(item_begin, item_end, begin, end, chunk, d_blk_best, d_blk_idx, \
-                                               d_blk_cnt)
-  switch (DL) {
-    case 1: HS_LAUNCH_BEST(1); break;
-    case 2: HS_LAUNCH_BEST(2); break;
-    case 3: HS_LAUNCH_BEST(3); break;
-    case 4: HS_LAUNCH_BEST(4); break;
-    case 5: HS_LAUNCH_BEST(5); break;
-    case 6: HS_LAUNCH_BEST(6); break;
-    case 7: HS_LAUNCH_BEST(7); break;
-    case 8: HS_LAUNCH_BEST(8); break;
-    default: HS_LAUNCH_BEST(0); break;
-  }
-#undef HS_LAUNCH_BEST
+  const int D1 = sd.D[M - 2], DL = sd.D[M - 1];
+  BestKernel k = k_search_best<0, 0>;
+  if (D1 <= kMaxStaticRadix && DL <= kMaxStaticRadix) k = table[D1][DL];
+  k<<<blocks, threads, 0, st>>>(item_begin, item_end, begin, end, chunk, d_blk_best, d_blk_idx, d_blk_cnt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_search_final<<<1, 1024, 0, st>>>(d_blk_best, d_blk_idx, d_blk_cnt, blocks, d_out, d_cnt_out);
