@@ -108,7 +108,7 @@ struct Cold {
   int32_t req_count, qtail, cnt_max, err, err_req, _pad;
 };
 
-__global__ void __launch_bounds__(kWarps * 32, 6)
+__global__ void __launch_bounds__(kWarps * 32, 7)
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6)
   cold.cnt_max = 0;
   cold.err = HS_TRACE_OK;
   cold.err_req = -1;
-  int64_t n_steps = 0;
+  uint32_t n_steps = 0;
   int64_t rr_next = 0;
   int32_t t_err = HS_TRACE_OK, t_err_inst = -1;
   int64_t t_err_req = -1;
@@ -297,14 +297,29 @@ __global__ void __launch_bounds__(kWarps * 32, 6)
       if (!__any_sync(FULL, want)) break;
       if (want) {
         if (blocked && k < kr) {
-          // pure steps: decode price + clock, no heap / queue traffic
-          do {
-            const double dec = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd), B), __dmul_rn(p7, cd)), p8);
-            t_next = __dadd_rn(t_next, dec);
-            cd = __dadd_rn(cd, 1.0);
-            ++k;
-            ++n_steps;
-          } while (k < kr && (drain || t_next < t_limit));
+          // pure steps: decode price + clock, no heap / queue traffic.  Two
+          // steps per iteration: their prices depend only on the cached
+          // length, so both are computed side by side and only the clock
+          // additions stay serial (the reference's rounding order).
+          const double lim = drain ? INFINITY : t_limit;
+          const uint32_t k0 = k;
+          for (;;) {
+            const double cd1 = __dadd_rn(cd, 1.0);
+            const double c0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd), B), __dmul_rn(p7, cd)), p8);
+            const double c1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd1), B), __dmul_rn(p7, cd1)), p8);
+            const double t1 = __dadd_rn(t_next, c0);
+            if (!(k + 1 < kr && (t1 < lim || drain))) {
+              t_next = t1;
+              cd = cd1;
+              k += 1;
+              break;
+            }
+            t_next = __dadd_rn(t1, c1);
+            cd = __dadd_rn(cd1, 1.0);
+            k += 2;
+            if (!(k < kr && (t_next < lim || drain))) break;
+          }
+          n_steps += k - k0;
         } else {
           event_step();
         }
@@ -486,15 +501,16 @@ __global__ void __launch_bounds__(kWarps * 32, 6)
     m.token_count = cold.tok_count;
     metrics[tr * N + lane] = m;
   }
+  int64_t steps_all = n_steps;
 #pragma unroll
-  for (int offs = 16; offs > 0; offs >>= 1) n_steps += __shfl_xor_sync(FULL, n_steps, offs);
+  for (int offs = 16; offs > 0; offs >>= 1) steps_all += __shfl_xor_sync(FULL, steps_all, offs);
   if (lane == 0) {
     hs_trace_result r;
     r.error = failed ? t_err : HS_TRACE_OK;
     r.err_instance = failed ? t_err_inst : -1;
     r.err_request = failed ? t_err_req : -1;
     r.err_value = failed ? t_err_val : 0.0;
-    r.n_steps = n_steps;
+    r.n_steps = steps_all;
     result[tr] = r;
   }
 }
