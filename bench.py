@@ -255,9 +255,10 @@ def engine_arm(args, rank, world, local_rank):
     cluster, reqs, params, sI, sO = search_inputs(args.search_q)
     tables = planner.build_tables(cluster, reqs, params, engine=eng)
     P = tables.space_size
-    lo, hi = P * rank // world, P * (rank + 1) // world
+    from paper_2504_15303_b200.distributed import shard_range
+    lo, hi = shard_range(P, rank, world)
     # ---- replay inputs (trace shard)
-    T_lo, T_hi = args.traces * rank // world, args.traces * (rank + 1) // world
+    T_lo, T_hi = shard_range(args.traces, rank, world)
     nT = T_hi - T_lo
     t0 = time.time()
     off, I, O, T = replay_inputs(T_lo, T_hi, args.q, args.rate)
@@ -277,27 +278,14 @@ def engine_arm(args, rank, world, local_rank):
     d["metrics"] = eng.device_alloc(max(nT * N, 1) * nat.METRICS_DTYPE.itemsize)
     d["result"] = eng.device_alloc(max(nT, 1) * nat.RESULT_DTYPE.itemsize)
 
-    win = torch.zeros(world, 3, dtype=torch.int64, device=dev)
+    from paper_2504_15303_b200 import distributed as hsd
 
     def combine(total, idx, nfeas):
         """One NCCL all-reduce of a per-rank slot buffer, then a local
         lexicographic reduce (max total, then lowest index)."""
         if not dist:
             return total, idx, nfeas
-        with torch.cuda.stream(ext):
-            win.zero_()
-            win[rank, 0] = int(np.float64(total).view(np.int64))
-            win[rank, 1] = idx
-            win[rank, 2] = nfeas
-            tdist.all_reduce(win)
-            h = win.cpu().numpy()
-        best = (0.0, -1)
-        for r in range(world):
-            t = float(np.int64(h[r, 0]).view(np.float64))
-            i = int(h[r, 1])
-            if i >= 0 and (best[1] < 0 or t > best[0] or (t == best[0] and i < best[1])):
-                best = (t, i)
-        return best[0], best[1], int(h[:, 2].sum())
+        return hsd.combine_best(total, idx, nfeas, device=dev, stream=ext)
 
     kms = {"k1": [], "k2": [], "k3": []}
 

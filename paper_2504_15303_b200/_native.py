@@ -25,7 +25,7 @@ POLICY_CODE = {"OS": 0, "RR": 1, "WRR": 2, "SI": 3, "MB": 4}
 TRACE_OK, TRACE_INFEASIBLE_REQUEST, TRACE_NONPOSITIVE_COST, TRACE_EXP_OVERFLOW, TRACE_NO_INSTANCE, \
     TRACE_NEGATIVE_RUNNING, TRACE_CAPACITY = range(7)
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "libhetserve_b200.so"
+LIB_PATH = pathlib.Path(os.environ.get("HS_LIB", pathlib.Path(__file__).resolve().parent / "libhetserve_b200.so"))
 
 
 class EngineUnavailable(RuntimeError):

@@ -30,21 +30,21 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, force: bool = False) -> pathlib.Path:
+def build(verbose: bool = False, force: bool = False, timers: bool = False) -> pathlib.Path:
+    lib = PKG / "libhetserve_b200_timers.so" if timers else LIB
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
     deps.append(PKG.parent / "include" / "hetserve_b200.h")
-    if not force and LIB.exists() and all(LIB.stat().st_mtime >= d.stat().st_mtime for d in deps):
-        return LIB
+    if not force and lib.exists() and all(lib.stat().st_mtime >= d.stat().st_mtime for d in deps):
+        return lib
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-cudart", "static", "-o", str(LIB) + ".tmp",
+           "-Xptxas", "-v" if verbose else "-O3", "-cudart", "static", *(["-DHS_TIMERS"] if timers else []), "-o", str(lib) + ".tmp",
            *[str(CSRC / s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force=True)
-    print(LIB)
+    print(build(verbose="-v" in sys.argv, force=True, timers="--timers" in sys.argv))

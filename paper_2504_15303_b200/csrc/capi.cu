@@ -156,6 +156,16 @@ int build_space(const hs_entry* table, const int32_t* nd, int32_t M, hs::SpaceDe
   return HS_OK;
 }
 
+// Largest integer X with per_token * X <= budget (budget > 0): an integer
+// product exceeds a float B exactly when it exceeds floor(B)
+// (simulator.py:303, planner.py:73).
+int64_t cap_tokens(double budget, int64_t per_token) {
+  if (!(budget >= 0)) return -1;
+  if (budget >= 9.2e18) return INT64_MAX;
+  const int64_t fb = (int64_t)std::floor(budget);
+  return fb / per_token;
+}
+
 // Python sum() semantics for the WRR total (scheduling.py:326)
 double pysum(const double* x, int n) {
   double f = 0.0, c = 0.0;
@@ -218,6 +228,7 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
     }
     std::memcpy(rc.type_p[ty], inst[j].p, sizeof(double) * 8);
     rc.type_budget[ty] = inst[j].budget;
+    rc.type_cap_tokens[ty] = cap_tokens(inst[j].budget, pol->per_token);
     rc.wrr_weight[j] = inst[j].wrr_weight;
     wts[j] = inst[j].wrr_weight;
   }
@@ -249,6 +260,7 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
     const double tokens = std::floor(inst[j].budget / (double)pol->per_token);
     double capd = std::floor(tokens / (double)min_need) + 1.0;
     int64_t capj = capd > (double)max_q ? max_q : (int64_t)capd;
+    capj -= hs::kHeapShared;  // the first entries live in shared memory
     if (capj < 1) capj = 1;
     rc.heap_off[j] = acc;
     acc += capj;
@@ -256,26 +268,24 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
   rc.heap_off[N] = acc;
   rc.heap_stride = (acc + 15) / 16 * 16;
 
-  double* d_wrec;
-  int32_t* d_qnext;
-  if ((rcode = ensure_t(c, S_WREC, (size_t)(h_off[T] > 0 ? h_off[T] : 1), &d_wrec))) return rcode;
-  if ((rcode = ensure_t(c, S_QNEXT, (size_t)(h_off[T] > 0 ? h_off[T] : 1), &d_qnext))) return rcode;
+  void* d_qrec;
+  if ((rcode = ensure(c, S_WREC, (size_t)(h_off[T] > 0 ? h_off[T] : 1) * hs::kQRecBytes, &d_qrec))) return rcode;
   // heap region, chunked over traces to bound memory
   size_t free_b = 0, tot_b = 0;
   HS_CUDA(cudaMemGetInfo(&free_b, &tot_b));
-  const size_t per_trace = (size_t)rc.heap_stride * sizeof(uint64_t);
+  const size_t per_trace = (size_t)rc.heap_stride * hs::kHEntBytes;
   size_t budget_b = (size_t)((double)(free_b + c->cap[S_HEAP]) * 0.6);
   int64_t chunk = per_trace ? (int64_t)(budget_b / per_trace) : T;
   if (chunk < 1) chunk = 1;
   if (chunk > T) chunk = T;
   if (chunk > 16384) chunk = 16384;
   uint64_t* d_heap = nullptr;
-  if ((rcode = ensure_t(c, S_HEAP, (size_t)(chunk > 0 ? chunk : 1) * rc.heap_stride, &d_heap))) return rcode;
+  if ((rcode = ensure_t(c, S_HEAP, (size_t)(chunk > 0 ? chunk : 1) * rc.heap_stride * 2, &d_heap))) return rcode;
   if ((rcode = begin_timing(c))) return rcode;
   for (int64_t t0 = 0; t0 < T; t0 += chunk) {
     const int64_t nt_ = (T - t0) < chunk ? (T - t0) : chunk;
     HS_CUDA(hs::launch_replay(rc, nt_, d_off + t0, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics + t0 * N,
-                              d_result + t0, d_wrec, d_qnext, d_heap, c->stream));
+                              d_result + t0, d_qrec, d_heap, c->stream));
     c->launches += 1;
   }
   return end_timing(c);

@@ -51,6 +51,7 @@ struct ReplayConst {
   int32_t inst_type[HS_MAX_INSTANCES];
   double type_p[HS_MAX_INSTANCES][8];
   double type_budget[HS_MAX_INSTANCES];
+  int64_t type_cap_tokens[HS_MAX_INSTANCES];  // floor(floor(budget) / per_token)
   double wrr_weight[HS_MAX_INSTANCES];
 };
 
@@ -67,7 +68,10 @@ cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, i
 cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                           const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
                           double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result,
-                          double* d_wrec, int32_t* d_qnext, uint64_t* d_heap, cudaStream_t st);
+                          void* d_qrec, uint64_t* d_heap, cudaStream_t st);
+constexpr int kQRecBytes = 24;  // replay.cu QRec
+constexpr int kHEntBytes = 16;  // replay.cu HEnt
+constexpr int kHeapShared = 8;  // replay.cu kHS
 
 int sm_count();
 

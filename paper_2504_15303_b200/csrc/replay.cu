@@ -43,41 +43,82 @@ namespace hs {
 
 __constant__ ReplayConst c_rep;
 
+#ifdef HS_TIMERS
+// Diagnostic build only (-DHS_TIMERS): per-warp cycle counts of the replay
+// phases, summed over the launch: [advance, price, evaluate, mapping, commit].
+__device__ unsigned long long g_timers[8];
+#define HS_T0(v) long long v = clock64()
+#define HS_T1(slot, v) \
+  do { if (lane == 0) atomicAdd(&g_timers[slot], (unsigned long long)(clock64() - v)); } while (0)
+#else
+#define HS_T0(v)
+#define HS_T1(slot, v)
+#endif
+
 constexpr int kWarps = 4;
+#ifndef HS_REPLAY_MIN_BLOCKS
+#define HS_REPLAY_MIN_BLOCKS 4
+#endif
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ __forceinline__ void heap_push(uint64_t* h, int32_t& n, uint64_t key) {
-  int32_t i = n++;
-  while (i > 0) {
-    const int32_t p = (i - 1) >> 1;
-    const uint64_t hp = h[p];
-    if (hp <= key) break;
-    h[i] = hp;
-    i = p;
+// Per-lane min-heap of retirement entries: key = departure step << 32 |
+// request (orders retirements as the reference's active list does) and
+// mk = I - k_admit (the quantity whose max gives the cached length).
+// Entries [0, kHS) live in shared memory, the rest in global memory.
+constexpr int kHS = 8;
+struct HEnt {
+  uint64_t key;
+  int64_t mk;
+};
+struct Heap {
+  HEnt* s;  // shared part, kHS entries
+  HEnt* g;  // global part (entry i >= kHS at g[i - kHS])
+  __device__ __forceinline__ HEnt get(int32_t i) const { return i < kHS ? s[i] : g[i - kHS]; }
+  __device__ __forceinline__ void set(int32_t i, HEnt v) const {
+    if (i < kHS) s[i] = v;
+    else g[i - kHS] = v;
   }
-  h[i] = key;
-}
-
-__device__ __forceinline__ void heap_pop(uint64_t* h, int32_t& n) {
-  const uint64_t last = h[--n];
-  int32_t i = 0;
-  for (;;) {
-    int32_t l = 2 * i + 1;
-    if (l >= n) break;
-    uint64_t hl = h[l];
-    if (l + 1 < n) {
-      const uint64_t hr = h[l + 1];
-      if (hr < hl) {
-        hl = hr;
-        ++l;
-      }
+  __device__ __forceinline__ void push(int32_t& n, HEnt e) const {
+    int32_t i = n++;
+    while (i > 0) {
+      const int32_t p = (i - 1) >> 1;
+      const HEnt hp = get(p);
+      if (hp.key <= e.key) break;
+      set(i, hp);
+      i = p;
     }
-    if (last <= hl) break;
-    h[i] = hl;
-    i = l;
+    set(i, e);
   }
-  if (n > 0) h[i] = last;
-}
+  __device__ __forceinline__ void pop(int32_t& n) const {
+    const HEnt last = get(--n);
+    int32_t i = 0;
+    for (;;) {
+      int32_t l = 2 * i + 1;
+      if (l >= n) break;
+      HEnt hl = get(l);
+      if (l + 1 < n) {
+        const HEnt hr = get(l + 1);
+        if (hr.key < hl.key) {
+          hl = hr;
+          ++l;
+        }
+      }
+      if (last.key <= hl.key) break;
+      set(i, hl);
+      i = l;
+    }
+    if (n > 0) set(i, last);
+  }
+};
+
+// Queue record of request a (written by the lane that owns the request):
+// P and the recorded workload W at dispatch; next / nI / nO when the next
+// request is enqueued behind it, so popping a head yields the new head's
+// lengths in the same load.
+struct QRec {
+  int32_t next, nI, nO, P;
+  double W;
+};
 
 // order-preserving key of a double (ascending); +0.0 and -0.0 share one key
 // because Python's comparisons treat them as equal.
@@ -108,14 +149,14 @@ struct Cold {
   int32_t req_count, qtail, cnt_max, err, err_req, _pad;
 };
 
-__global__ void __launch_bounds__(kWarps * 32, 7)
+__global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
-             hs_trace_result* __restrict__ result, double* __restrict__ wrec, int32_t* __restrict__ qnext,
-             uint64_t* __restrict__ heap_all) {
+             hs_trace_result* __restrict__ result, QRec* __restrict__ qrec_all, uint64_t* __restrict__ heap_all) {
   __shared__ uint64_t s_tab[256];
   __shared__ Cold s_cold[kWarps * 32];
+  __shared__ HEnt s_heap[kWarps * 32][kHS];
   extern __shared__ double s_cost[];  // [kWarps][32 * n_types]
   for (int k = threadIdx.x; k < 256; k += blockDim.x) s_tab[k] = kExpTab[k];
   __syncthreads();
@@ -138,8 +179,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
   const int32_t* O = gO + o;
   const int32_t* P = gP + o;
   const double* T = gT ? gT + o : nullptr;
-  double* W = wrec + o;
-  int32_t* QN = qnext + o;
+  QRec* R = qrec_all + o;
   double* DEP = depart ? depart + o : nullptr;
 
   const bool valid = lane < N;
@@ -148,16 +188,24 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
   const double* tp = c_rep.type_p[ty];
   const double budget = c_rep.type_budget[ty];
   const double p7 = tp[6], p8 = tp[7];
-  uint64_t* heap = heap_all + tr * c_rep.heap_stride + c_rep.heap_off[j];
-  const int32_t cap = (int32_t)(c_rep.heap_off[j + 1] - c_rep.heap_off[j]);
+  const Heap heap{s_heap[threadIdx.x],
+                  reinterpret_cast<HEnt*>(heap_all) + tr * c_rep.heap_stride + c_rep.heap_off[j]};
+  const int64_t cap_tok = c_rep.type_cap_tokens[ty];  // floor(floor(budget) / per_token)
+  const int32_t cap = (int32_t)(c_rep.heap_off[j + 1] - c_rep.heap_off[j]) + kHS;
 
   // hot per-lane state (registers)
   double load = 0.0, ex = 1.0;
-  int64_t run_i = 0, run_p = 0, reserved = 0, cur_max = INT64_MIN;
+  int64_t run_i = 0, run_p = 0, reserved = 0, cur_max = INT64_MIN, max_res = 0;
   uint32_t k = 0, kr = 0xffffffffu;  // steps executed; step of the next retirement
   double t_next = 0.0, cd = 0.0, A = 0.0, B = 0.0;  // clock, cached len (double), p5*b, p6*b
-  int32_t qhead = -1, hI = 0, hO = 0, nact = 0;
-  bool sched = false, dirty = true, ex_over = false, max_dirty = false, blocked = false;
+  // queue head: index, lengths, and its prefetched record
+  int32_t qhead = -1, qtail = -1, hI = 0, hO = 0, hP = 0, hnext = -1, hnI = 0, hnO = 0;
+  double hW = 0.0;
+  // heap: size, minimum key and the prefetched payload of the minimum
+  int32_t nact = 0, topI = 0, topO = 0, topP = 0;
+  uint64_t topkey = 0;
+  double topW = 0.0;
+  bool sched = false, dirty = true, ex_over = false, max_dirty = false, blocked = false, lerr = false;
   cold.completion = 0.0;
   cold.peak = 0.0;
   cold.wcur = 0.0;
@@ -174,69 +222,100 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
   int64_t t_err_req = -1;
   double t_err_val = 0.0;
 
+  auto set_err = [&](int32_t code, int32_t r, double t) {
+    cold.err = code;
+    cold.err_req = r;
+    cold.err_t = t;
+    lerr = true;
+  };
+
   // A full STEP event (simulator.py:330-355): retirements due at this step,
   // FCFS admission, prefill for newcomers, one decode iteration.
   auto event_step = [&]() {
     const double t = t_next;
     sched = false;
     ++n_steps;
-    if (nact > 0 && (uint32_t)(heap[0] >> 32) == k) {
-      do {  // retire in (departure step, admission order)
-        const uint64_t top = heap[0];
-        const int32_t r = (int32_t)(top & 0xffffffffu);
-        heap_pop(heap, nact);
-        const int64_t Ir = I[r], Or = O[r], Pr = P[r];
-        const double wr = W[r];
-        reserved -= Ir + Or;
-        cold.completion = t;
-        cold.req_count += 1;
-        cold.tok_count += Ir + Or;
-        if (DEP) DEP[r] = t;
-        load = __dsub_rn(load, wr);  // Scheduler.complete: recorded values
-        run_i -= Ir;
-        run_p -= Pr;
-        dirty = true;
-        if (run_i < 0 || run_p < 0) {
-          cold.err = HS_TRACE_NEGATIVE_RUNNING;
-          cold.err_req = r;
-          cold.err_t = t;
-          return;
-        }
-        const int64_t ka = (int64_t)k - (Or > 1 ? Or : 1);
-        if (Ir - ka == cur_max && --cold.cnt_max == 0) max_dirty = true;
-      } while (nact > 0 && (uint32_t)(heap[0] >> 32) == k);
+    while (nact > 0 && (uint32_t)(topkey >> 32) == k) {
+      // retire in (departure step, admission order); payload was prefetched
+      const int32_t r = (int32_t)(topkey & 0xffffffffu);
+      const int64_t Ir = topI, Or = topO, Pr = topP;
+      const double wr = topW;
+      heap.pop(nact);
+      if (nact > 0) {
+        topkey = heap.get(0).key;
+        const int32_t r2 = (int32_t)(topkey & 0xffffffffu);
+        topI = I[r2];
+        topO = O[r2];
+        topP = R[r2].P;
+        topW = R[r2].W;
+      }
+      reserved -= Ir + Or;
+      cold.completion = t;
+      cold.req_count += 1;
+      cold.tok_count += Ir + Or;
+      if (DEP) DEP[r] = t;
+      load = __dsub_rn(load, wr);  // Scheduler.complete: the recorded values
+      run_i -= Ir;
+      run_p -= Pr;
+      dirty = true;
+      if (run_i < 0 || run_p < 0) {
+        set_err(HS_TRACE_NEGATIVE_RUNNING, r, t);
+        return;
+      }
+      const int64_t ka = (int64_t)k - (Or > 1 ? Or : 1);
+      if (Ir - ka == cur_max && --cold.cnt_max == 0) max_dirty = true;
+    }
+    if (nact == 0) {
+      cur_max = INT64_MIN;
+      cold.cnt_max = 0;
+      max_dirty = false;
     }
     // admit FCFS (simulator.py:297-316)
     int64_t newly = 0, max_i_new = 0;
     while (qhead >= 0) {
       const int64_t need = (int64_t)hI + hO;
-      if (int_gt_double(sat_mul(pt, reserved + need), budget)) {
+      // simulator.py:303 per_token * (reserved + need) > budget, exactly:
+      // an integer X satisfies pt*X > B iff X > floor(floor(B) / pt)
+      if (reserved + need > cap_tok) {
         if (nact == 0 && newly == 0) {
-          cold.err = HS_TRACE_INFEASIBLE_REQUEST;
-          cold.err_req = qhead;
-          cold.err_t = t;
+          set_err(HS_TRACE_INFEASIBLE_REQUEST, qhead, t);
           return;
         }
         break;
       }
+      if (nact >= cap || k > 0x7fffffffu) {
+        set_err(HS_TRACE_CAPACITY, qhead, t);
+        return;
+      }
       const int32_t r = qhead;
-      const int64_t Ir = hI, Or = hO;
-      qhead = (r == cold.qtail) ? -1 : QN[r];
-      if (qhead >= 0) {
-        hI = I[qhead];
-        hO = O[qhead];
+      const int64_t Ir = hI, Or = hO, Pr = hP;
+      const double wr = hW;
+      if (r == qtail) {
+        qhead = -1;
+      } else {  // the next head's lengths came with the popped record
+        qhead = hnext;
+        hI = hnI;
+        hO = hnO;
+        const QRec nr = R[qhead];  // prefetch the new head's record
+        hnext = nr.next;
+        hnI = nr.nI;
+        hnO = nr.nO;
+        hP = nr.P;
+        hW = nr.W;
       }
       reserved += need;
       if (Ir > max_i_new) max_i_new = Ir;
       ++newly;
-      if (nact >= cap || k > 0x7fffffffu) {
-        cold.err = HS_TRACE_CAPACITY;
-        cold.err_req = r;
-        cold.err_t = t;
-        return;
+      const uint64_t key = ((uint64_t)(k + (uint32_t)(Or > 1 ? Or : 1)) << 32) | (uint32_t)r;
+      if (nact == 0 || key < topkey) {
+        topkey = key;
+        topI = (int32_t)Ir;
+        topO = (int32_t)Or;
+        topP = (int32_t)Pr;
+        topW = wr;
       }
-      heap_push(heap, nact, ((uint64_t)(k + (uint32_t)(Or > 1 ? Or : 1)) << 32) | (uint32_t)r);
       const int64_t mk = Ir - (int64_t)k;
+      heap.push(nact, HEnt{key, mk});
       if (mk > cur_max) {
         cur_max = mk;
         cold.cnt_max = 1;
@@ -246,10 +325,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
       }
     }
     blocked = true;  // queue empty or its head does not fit: nothing changes until an event
-    if (newly) {
-      const double u = __ddiv_rn(i2d(pt * reserved), budget);  // simulator.py:315
-      if (u > cold.peak) cold.peak = u;
-    }
+    // simulator.py:315 peak = max(peak, per_token*reserved / budget): the
+    // quotient is monotone in the numerator, so the max of the quotients is
+    // the quotient of the max reservation (divided once, at the end).
+    if (newly && reserved > max_res) max_res = reserved;
     if (nact == 0) {  // idle until the next dispatch (simulator.py:344-345)
       kr = 0xffffffffu;
       return;
@@ -260,10 +339,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
       int64_t m = INT64_MIN;
       int32_t cm = 0;
       for (int32_t h = 0; h < nact; ++h) {
-        const uint64_t key = heap[h];
-        const int32_t r = (int32_t)(key & 0xffffffffu);
-        const int64_t Or = O[r];
-        const int64_t mk = (int64_t)I[r] - ((int64_t)(uint32_t)(key >> 32) - (Or > 1 ? Or : 1));
+        const int64_t mk = heap.get(h).mk;
         if (mk > m) {
           m = mk;
           cm = 1;
@@ -284,7 +360,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
     c = __dadd_rn(c, dec);
     k += 1;
     cd = __dadd_rn(cd, 1.0);
-    kr = (uint32_t)(heap[0] >> 32);
+    kr = (uint32_t)(topkey >> 32);
     t_next = __dadd_rn(t, c);
     sched = true;
   };
@@ -292,43 +368,47 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
   // Advance every lane's steps with t_next < t_limit (strict: steps at an
   // arrival's own time run after it), or every step when draining.
   auto advance = [&](double t_limit, bool drain) -> bool {
+    const double lim = drain ? INFINITY : t_limit;
     for (;;) {
-      const bool want = valid && sched && (drain || t_next < t_limit) && cold.err == HS_TRACE_OK;
+      const bool want = valid && sched && (drain || t_next < t_limit) && !lerr;
       if (!__any_sync(FULL, want)) break;
-      if (want) {
-        if (blocked && k < kr) {
-          // pure steps: decode price + clock, no heap / queue traffic.  Two
-          // steps per iteration: their prices depend only on the cached
-          // length, so both are computed side by side and only the clock
-          // additions stay serial (the reference's rounding order).
-          const double lim = drain ? INFINITY : t_limit;
-          const uint32_t k0 = k;
-          for (;;) {
-            const double cd1 = __dadd_rn(cd, 1.0);
-            const double c0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd), B), __dmul_rn(p7, cd)), p8);
-            const double c1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd1), B), __dmul_rn(p7, cd1)), p8);
-            const double t1 = __dadd_rn(t_next, c0);
-            if (!(k + 1 < kr && (t1 < lim || drain))) {
-              t_next = t1;
-              cd = cd1;
-              k += 1;
-              break;
-            }
-            t_next = __dadd_rn(t1, c1);
-            cd = __dadd_rn(cd1, 1.0);
-            k += 2;
-            if (!(k < kr && (t_next < lim || drain))) break;
+      // phase 1: lanes whose next step is an event (retirement due, or an
+      // admission may succeed)
+      if (want && !(blocked && k < kr)) event_step();
+      // phase 2: every lane whose next steps are pure runs them together,
+      // up to its next event or the arrival time.  Two steps per iteration:
+      // their prices depend only on the cached length, so both are computed
+      // side by side and only the clock additions stay serial (the
+      // reference's rounding order).
+      const bool pure = valid && sched && !lerr && blocked && k < kr && (drain || t_next < t_limit);
+      if (pure) {
+        const uint32_t k0 = k;
+        for (;;) {
+          const double cd1 = __dadd_rn(cd, 1.0);
+          const double c0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd), B), __dmul_rn(p7, cd)), p8);
+          const double c1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd1), B), __dmul_rn(p7, cd1)), p8);
+          const double t1 = __dadd_rn(t_next, c0);
+          if (!(k + 1 < kr && (t1 < lim || drain))) {
+            t_next = t1;
+            cd = cd1;
+            k += 1;
+            break;
           }
-          n_steps += k - k0;
-        } else {
-          event_step();
+          t_next = __dadd_rn(t1, c1);
+          cd = __dadd_rn(cd1, 1.0);
+          k += 2;
+          if (!(k < kr && (t_next < lim || drain))) break;
         }
+        n_steps += k - k0;
       }
+#ifdef HS_TIMERS
+      if (lane == 0) atomicAdd(&g_timers[7], 1ull);
+#endif
     }
-    const unsigned eb = __ballot_sync(FULL, valid && cold.err != HS_TRACE_OK);
+    const unsigned eb = __ballot_sync(FULL, valid && lerr);
     if (!eb) return false;
     // the earliest failing step event wins (heap order: time, then instance)
-    const uint64_t tk = (valid && cold.err != HS_TRACE_OK) ? okey(cold.err_t) : ~0ull;
+    const uint64_t tk = (valid && lerr) ? okey(cold.err_t) : ~0ull;
     const uint64_t mt = warp_min_u64(tk);
     const int bl = __ffs(__ballot_sync(FULL, tk == mt)) - 1;
     t_err = __shfl_sync(FULL, cold.err, bl);
@@ -352,6 +432,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
     }
     // price (arrival, class) pairs: scheduling.py:119-147
     __syncwarp();
+    HS_T0(tp0);
     if (policy != HS_POLICY_MB) {
       for (int pair0 = 0; pair0 < n_in * NT; pair0 += 32) {
         const int pair = pair0 + lane;
@@ -370,13 +451,17 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
       }
       __syncwarp();
     }
+    HS_T1(1, tp0);
     for (int al = 0; al < n_in; ++al) {
       const int64_t a = base + al;
       const double ta = shfl_d(cT, al);
+      HS_T0(ta0);
       if (advance(ta, false)) {
         failed = true;
         break;
       }
+      HS_T1(0, ta0);
+      HS_T0(te0);
       const int64_t Ia = __shfl_sync(FULL, cI, al);
       const int64_t Oa = __shfl_sync(FULL, cO, al);
       const int64_t Pa = __shfl_sync(FULL, cP, al);
@@ -417,6 +502,8 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
         eerr = ex_over;
         w = __dmul_rn(cst, ex);
       }
+      HS_T1(2, te0);
+      HS_T0(tm0);
       const unsigned errb = __ballot_sync(FULL, need && (cerr || eerr));
       if (errb) {  // the first instance in evaluation order raises
         const int el = __ffs(errb) - 1;
@@ -464,22 +551,35 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
         }
         chosen = __ffs(win) - 1;
       }
+      HS_T1(3, tm0);
+      HS_T0(tc0);
       // ---- commit (scheduling.py:335-346) and enqueue (simulator.py:323-327)
       if (lane == chosen) {
         load = __dadd_rn(load, w);
         run_i += Ia;
         run_p += Pa;
         dirty = true;
-        W[a] = w;
+        R[a].P = (int32_t)Pa;
+        R[a].W = w;
         if (qhead < 0) {
           qhead = (int32_t)a;
           hI = (int32_t)Ia;
           hO = (int32_t)Oa;
+          hP = (int32_t)Pa;
+          hW = w;
           blocked = false;  // a new queue head may be admitted at the next step
+        } else if (qtail == qhead) {  // the head's prefetched record gains its successor
+          hnext = (int32_t)a;
+          hnI = (int32_t)Ia;
+          hnO = (int32_t)Oa;
+          R[qtail].next = (int32_t)a;
         } else {
-          QN[cold.qtail] = (int32_t)a;
+          QRec& tr_ = R[qtail];
+          tr_.next = (int32_t)a;
+          tr_.nI = (int32_t)Ia;
+          tr_.nO = (int32_t)Oa;
         }
-        cold.qtail = (int32_t)a;
+        qtail = (int32_t)a;
         if (!sched) {
           sched = true;
           t_next = ta;
@@ -487,6 +587,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
         }
       }
       if (lane == al) my_assign = (uint8_t)chosen;
+      HS_T1(4, tc0);
     }
     if (assign && lane < n_in && !failed) assign[o + base + lane] = my_assign;
   }
@@ -495,7 +596,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
   if (valid) {
     hs_inst_metrics m;
     m.completion_time = cold.completion;
-    m.peak_kv_usage = cold.peak;
+    m.peak_kv_usage = max_res > 0 ? __ddiv_rn(i2d(pt * max_res), budget) : 0.0;
     m.residual_load = load;
     m.request_count = cold.req_count;
     m.token_count = cold.tok_count;
@@ -517,19 +618,19 @@ __global__ void __launch_bounds__(kWarps * 32, 7)
 
 cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                           const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
-                          double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result, double* d_wrec,
-                          int32_t* d_qnext, uint64_t* d_heap, cudaStream_t st) {
+                          double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec,
+                          uint64_t* d_heap, cudaStream_t st) {
   cudaError_t e = cudaMemcpyToSymbolAsync(c_rep, &rc, sizeof(ReplayConst), 0, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   if (n_traces <= 0) return cudaSuccess;
   const size_t smem = (size_t)kWarps * 32 * rc.n_types * sizeof(double);
-  if (smem > 32 * 1024) {
+  if (smem > 16 * 1024) {
     e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const unsigned blocks = (unsigned)((n_traces + kWarps - 1) / kWarps);
   k_replay<<<blocks, kWarps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
-                                              d_result, d_wrec, d_qnext, d_heap);
+                                              d_result, static_cast<QRec*>(d_qrec), d_heap);
   return cudaGetLastError();
 }
 
@@ -555,3 +656,16 @@ cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, i
 }
 
 }  // namespace hs
+
+#ifdef HS_TIMERS
+// diagnostic export of the timers build (not part of the ABI header)
+extern "C" int hs_debug_timers(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaError_t e = cudaMemcpyFromSymbol(out, hs::g_timers, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(hs::g_timers, z, sizeof(z));
+  }
+  return e == cudaSuccess ? 0 : 1;
+}
+#endif

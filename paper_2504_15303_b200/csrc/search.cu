@@ -74,6 +74,9 @@ __global__ void __launch_bounds__(128) k_table_build(const EntryDesc* __restrict
       tot.init();
       int64_t start = 0;
       const int64_t pt = sc.per_token;
+      // planner.py:69-74 per_token*sum(I) + width*per_token*max(O) > budget,
+      // exactly: the integer pt*X exceeds B iff X > floor(floor(B) / pt)
+      const int64_t cap = budget >= 9.2e18 ? INT64_MAX : (int64_t)floor(budget) / pt;
       while (start < q) {
         int64_t sumI = 0, maxO = 0, maxI = 0;  // carries of the batch so far
         int64_t pos = start, stop = start, bMO = 0, bMI = 0;
@@ -98,9 +101,8 @@ __global__ void __launch_bounds__(128) k_table_build(const EntryDesc* __restrict
           const int64_t candMO = maxO > mo ? maxO : mo;
           const int64_t candMI = maxI > mi ? maxI : mi;
           const int64_t width = idx - start + 1;
-          // planner.py:69-74: per_token*sum(I) + width*per_token*max(O) > budget
-          const int64_t reserved = sat_add(sat_mul(pt, candI), sat_mul(sat_mul(width, pt), candMO));
-          const bool fail = !valid || int_gt_double(reserved, budget);
+          const int64_t tokens = sat_add(candI, sat_mul(width, candMO));
+          const bool fail = !valid || tokens > cap;
           const unsigned bal = __ballot_sync(0xffffffffu, fail);
           if (bal) {
             const int f = __ffs(bal) - 1;

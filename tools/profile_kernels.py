@@ -34,6 +34,17 @@ def main():
         assert (r.result["error"] == 0).all()
         print(f"replay {T} traces x {q}: {r.kernel_ms:.2f} ms, {T * q / r.kernel_ms * 1e3:.3g} req/s, "
               f"{r.result['n_steps'].sum() / (T * q):.1f} steps/request")
+        if hasattr(eng.lib, "hs_debug_timers"):
+            import ctypes
+            import numpy as np
+            buf = np.zeros(8, np.uint64)
+            eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 1)
+            hs.replay_traces(rc, config, params, hs.PolicyConfig(), off, I, O, O, arrival=Tarr, engine=eng)
+            eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 0)
+            names = ["advance", "price", "evaluate", "mapping", "commit", "-", "-"]
+            per = buf[:7].astype(float) / (T * q)
+            print("cycles per arrival per warp:", {n: round(v, 1) for n, v in zip(names, per)})
+            print("advance iterations per arrival:", int(buf[7]) / (T * q))
     else:
         cluster, reqs, params, _I, _O = bench.search_inputs(10_000)
         t = planner.build_tables(cluster, reqs, params, engine=eng)
