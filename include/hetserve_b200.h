@@ -17,8 +17,9 @@
  *   hs_search_rank     planner.py:213-228 again, full ranking (ranked.sort
  *                      key (-total, tp tuple)) for spaces small enough to
  *                      materialise.
- *   hs_replay          simulator.py:272-363 run_continuous with
- *                      scheduling.py:216-346 Scheduler.evaluate/choose/
+ *   hs_replay          simulator.py:272-363 run_continuous (or, with
+ *                      hs_policy.mode = 1, simulator.py:206-250 run_static)
+ *                      with scheduling.py:216-346 Scheduler.evaluate/choose/
  *                      complete, for a batch of independent traces.
  *
  * Conventions: plain pointers and sizes, caller-owned host buffers, calls are
@@ -38,7 +39,7 @@
 extern "C" {
 #endif
 
-#define HS_ABI_VERSION 1
+#define HS_ABI_VERSION 2
 #define HS_MAX_DEGREES 32   /* power-of-two divisors of an accelerator count  */
 #define HS_MAX_MACHINES 64
 #define HS_MAX_INSTANCES 32 /* one warp lane per instance (round-1 kernel)    */
@@ -146,6 +147,9 @@ typedef struct {
   int32_t n_instances;
   double theta;
   int64_t per_token;     /* capacity.py:67-69 kv_bytes_per_token */
+  int32_t mode;          /* 0 continuous batching (simulator.py:272-363),
+                            1 static batching (simulator.py:206-250; rate=inf) */
+  int32_t _pad;
 } hs_policy;
 
 /* simulator.py:82-88 InstanceMetrics + scheduler.loads() residual. */

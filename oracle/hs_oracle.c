@@ -513,6 +513,7 @@ int hs_oracle_replay_one(const hs_instance* inst, const hs_policy* pol, const in
     wrr_total = pysum_result(&s);
   }
   heap_t ev = {0, 0, 0};
+  const int is_static = pol->mode == 1;
   for (int64_t s = 0; s < q; ++s) {
     ev_t e = {arrival ? arrival[s] : 0.0, 0, s};
     heap_push(&ev, e);
@@ -594,6 +595,7 @@ int hs_oracle_replay_one(const hs_instance* inst, const hs_policy* pol, const in
       w_rec[r] = weights[chosen];
       if (assign) assign[r] = (uint8_t)chosen;
       st[chosen].queue[st[chosen].qt++] = r;
+      if (is_static) continue; /* run_static: dispatch everything first (simulator.py:216-220) */
       if (!st[chosen].step_scheduled) {
         st[chosen].step_scheduled = 1;
         ev_t se = {t, 1, chosen};
@@ -672,6 +674,57 @@ int hs_oracle_replay_one(const hs_instance* inst, const hs_policy* pol, const in
     run->step_scheduled = 1;
     ev_t se = {t + cost, 1, j};
     heap_push(&ev, se);
+  }
+  if (!err && is_static) {
+    /* simulator.py:229-247: per instance, plan_static_batches over its
+     * assigned requests (planner.py:51-87), clock += estimate_batch_time,
+     * complete() in batch order; the first failing instance raises. */
+    for (int32_t j = 0; j < N && !err; ++j) {
+      inst_t* run = &st[j];
+      double clock = 0.0;
+      int64_t a = run->qh;
+      while (a < run->qt) {
+        i128 input_sum = 0;
+        int64_t max_o = 0, b = a;
+        while (b < run->qt) {
+          int64_t r = run->queue[b];
+          i128 ci = input_sum + I[r];
+          int64_t cmo = max_o > O[r] ? max_o : O[r];
+          int64_t width = b - a + 1;
+          i128 reserved = (i128)per_token * ci + (i128)width * per_token * cmo;
+          if (i128_gt_double(reserved, inst[j].budget)) break;
+          input_sum = ci;
+          max_o = cmo;
+          ++b;
+        }
+        if (b == a) {
+          err = HS_TRACE_INFEASIBLE_REQUEST; res->err_instance = j; res->err_request = run->queue[a];
+          break;
+        }
+        int64_t si = 0, mi = 0, mo = 0;
+        for (int64_t x = a; x < b; ++x) {
+          int64_t r = run->queue[x];
+          si += I[r];
+          if (I[r] > mi) mi = I[r];
+          if (O[r] > mo) mo = O[r];
+        }
+        i128 reserved = (i128)per_token * (si + (b - a) * mo);
+        double u = i128_to_double(reserved) / inst[j].budget;
+        if (u > run->peak) run->peak = u;
+        clock += prefill(inst[j].p, b - a, mi) + decode_total(inst[j].p, b - a, mi, mo);
+        for (int64_t x = a; x < b; ++x) {
+          int64_t r = run->queue[x];
+          run->load -= w_rec[r];
+          run->run_i -= I[r];
+          run->run_p -= P[r];
+          if (depart) depart[r] = clock;
+          run->token_count += (int64_t)I[r] + O[r];
+          run->request_count += 1;
+        }
+        a = b;
+      }
+      run->completion_time = clock;
+    }
   }
   res->error = err;
   res->n_steps = steps;

@@ -74,7 +74,8 @@ class hs_instance(C.Structure):
 
 
 class hs_policy(C.Structure):
-    _fields_ = [("policy", C.c_int32), ("n_instances", C.c_int32), ("theta", C.c_double), ("per_token", C.c_int64)]
+    _fields_ = [("policy", C.c_int32), ("n_instances", C.c_int32), ("theta", C.c_double), ("per_token", C.c_int64),
+                ("mode", C.c_int32), ("_pad", C.c_int32)]
 
 
 class hs_inst_metrics(C.Structure):

@@ -215,6 +215,9 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
   rc.theta = pol->theta;
   rc.per_token = pol->per_token;
   rc.has_arrival = d_arr != nullptr;
+  if (pol->mode != 0 && pol->mode != 1) return fail(HS_ERR_ARG, "mode must be 0 (continuous) or 1 (static)");
+  if (pol->mode == 1 && d_arr) return fail(HS_ERR_ARG, "static mode needs arrival = NULL (rate = inf)");
+  rc.mode = pol->mode;
   int nt = 0;
   std::vector<double> wts(N);
   for (int j = 0; j < N; ++j) {

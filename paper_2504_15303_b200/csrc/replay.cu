@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     return true;
   };
 
+  const bool is_static = c_rep.mode == 1;
   bool failed = false;
   uint8_t my_assign = 0;
   for (int64_t base = 0; base < q && !failed; base += 32) {
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       const int64_t a = base + al;
       const double ta = shfl_d(cT, al);
       HS_T0(ta0);
-      if (advance(ta, false)) {
+      if (!is_static && advance(ta, false)) {
         failed = true;
         break;
       }
@@ -591,7 +592,61 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     }
     if (assign && lane < n_in && !failed) assign[o + base + lane] = my_assign;
   }
-  if (!failed && advance(0.0, true)) failed = true;
+  if (!failed && !is_static && advance(0.0, true)) failed = true;
+  if (!failed && is_static) {
+    // run_static (simulator.py:229-247): each instance runs its assigned
+    // requests (queue order = trace order) as greedy KV-feasible static
+    // batches (planner.py:51-87 with the true output lengths), prices each
+    // with estimate_batch_time (planner.py:90-101), advances its clock and
+    // fires the completion hooks in batch order.
+    bool bad = false;
+    int32_t bad_r = -1;
+    if (valid) {
+      double clock = 0.0;
+      int32_t r = qhead;
+      while (r >= 0) {
+        int64_t sumI = 0, maxO = 0, maxI = 0, width = 0;
+        int32_t c = r, stop = -1;
+        while (c >= 0) {
+          const int64_t Ic = I[c], Oc = O[c];
+          const int64_t cI = sumI + Ic, cMO = maxO > Oc ? maxO : Oc;
+          if (sat_add(cI, sat_mul(width + 1, cMO)) > cap_tok) break;
+          sumI = cI;
+          maxO = cMO;
+          if (Ic > maxI) maxI = Ic;
+          ++width;
+          c = (c == qtail) ? -1 : R[c].next;
+        }
+        stop = c;
+        if (width == 0) {
+          bad = true;
+          bad_r = r;
+          break;
+        }
+        const int64_t res_tok = sumI + width * maxO;
+        if (res_tok > max_res) max_res = res_tok;
+        clock = __dadd_rn(clock, __dadd_rn(prefill_time(tp, width, maxI), decode_time(tp, width, maxI, maxO)));
+        for (int32_t m = r; m != stop;) {
+          const QRec rec = R[m];
+          load = __dsub_rn(load, rec.W);
+          if (DEP) DEP[m] = clock;
+          cold.tok_count += (int64_t)I[m] + O[m];
+          cold.req_count += 1;
+          m = (m == qtail) ? -1 : rec.next;
+        }
+        r = stop;
+      }
+      cold.completion = clock;
+    }
+    const unsigned bb = __ballot_sync(FULL, bad);
+    if (bb) {  // the first instance (config order) whose plan fails raises
+      const int bl = __ffs(bb) - 1;
+      t_err = HS_TRACE_INFEASIBLE_REQUEST;
+      t_err_req = __shfl_sync(FULL, bad_r, bl);
+      t_err_inst = bl;
+      failed = true;
+    }
+  }
 
   if (valid) {
     hs_inst_metrics m;

@@ -12,8 +12,8 @@ Drop-in entry points (reference /root/reference/pkg/src/hetserve/simulator.py):
 Engine-level API: ``replay_traces(...)`` replays a batch of traces (one warp
 each) on one deployment and returns arrays, for the batched-replay configs.
 
-Static mode (``run_static``, simulator.py:206-250) is the next row of the
-hot-path scope and is not in the engine yet.
+``run_static`` (simulator.py:206-250), the first "next" row of SURVEY.md
+section 8f, runs on the same kernel in static mode.
 """
 
 from __future__ import annotations
@@ -157,7 +157,7 @@ def _predictor(scenario) -> OutputLengthPredictor:
     return OutputLengthPredictor(cfg, scenario.cluster.limits.max_output_len)
 
 
-def _raise_trace_error(res, handles, trace, per_token, theta=None) -> None:
+def _raise_trace_error(res, handles, trace, per_token, static=False) -> None:
     err = int(res["error"])
     if err == nat.TRACE_OK:
         return
@@ -167,6 +167,11 @@ def _raise_trace_error(res, handles, trace, per_token, theta=None) -> None:
         r = trace[ridx]
         need = r.input_len + r.output_len
         budget = handles[inst].budget.total_bytes
+        if static:  # raised by plan_static_batches (planner.py:80-83)
+            raise InfeasibleRequestError(
+                f"request {r.id!r} needs {per_token * need:.0f} KV bytes alone, budget is {budget:.0f}",
+                request_id=r.id,
+            )
         raise InfeasibleRequestError(
             f"request {r.id!r} needs {per_token * need:.0f} KV bytes alone, budget of "
             f"instance {handles[inst].id!r} is {budget:.0f}",
@@ -186,12 +191,11 @@ def _raise_trace_error(res, handles, trace, per_token, theta=None) -> None:
     raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"replay hit an engine limit (code {err})")
 
 
-def _policy_struct(policy: PolicyConfig, n: int, per_token: int) -> nat.hs_policy:
-    return nat.hs_policy(nat.POLICY_CODE[policy.policy], n, float(policy.theta), per_token)
+def _policy_struct(policy: PolicyConfig, n: int, per_token: int, mode: int = 0) -> nat.hs_policy:
+    return nat.hs_policy(nat.POLICY_CODE[policy.policy], n, float(policy.theta), per_token, mode, 0)
 
 
-def run_continuous(scenario, engine=None) -> SimMetrics:
-    """simulator.py:272-363 on the GPU (one trace, one warp)."""
+def _run(scenario, static: bool, engine=None) -> SimMetrics:
     handles = build_instances(scenario.cluster, scenario.config, scenario.params)
     policy = scenario.policy
     _check_scheduler(handles, policy)
@@ -214,19 +218,23 @@ def run_continuous(scenario, engine=None) -> SimMetrics:
     eng = engine or nat.engine_for()
     offsets = np.array([0, len(trace)], np.int64)
     assign, depart, metrics, result = eng.replay(
-        engine_instances(handles, policy), _policy_struct(policy, N, per_token), offsets,
+        engine_instances(handles, policy), _policy_struct(policy, N, per_token, 1 if static else 0), offsets,
         I.astype(np.int32), O.astype(np.int32), P.astype(np.int32),
         None if math.isinf(scenario.arrival_rate) else T)
-    _raise_trace_error(result[0], handles, trace, per_token)
+    _raise_trace_error(result[0], handles, trace, per_token, static=static)
     m = metrics[0]
     completion = m["completion_time"].tolist()
     req_count = m["request_count"].tolist()
     tok_count = m["token_count"].tolist()
     peak = m["peak_kv_usage"].tolist()
-    # request_times keeps the reference's dict insertion order = retirement
-    # order: (departure time, instance index, admission order) -- exact when
-    # step costs are non-negative (time is then monotone per instance).
-    order = np.lexsort((np.arange(len(trace)), assign.astype(np.int64), depart))
+    idx = np.arange(len(trace))
+    if static:
+        # simulator.py:229-245: times filled instance by instance, batch by batch
+        order = np.lexsort((idx, assign.astype(np.int64)))
+    else:
+        # retirement order: (departure time, instance index, admission order) --
+        # the reference's heap order whenever step costs are non-negative
+        order = np.lexsort((idx, assign.astype(np.int64), depart))
     dep = depart.tolist()
     arr = T.tolist()
     request_times = tuple((ids[k], arr[k], dep[k]) for k in order.tolist())
@@ -250,10 +258,17 @@ def run_continuous(scenario, engine=None) -> SimMetrics:
     )
 
 
+def run_continuous(scenario, engine=None) -> SimMetrics:
+    """simulator.py:272-363 on the GPU (one trace, one warp)."""
+    return _run(scenario, static=False, engine=engine)
+
+
 def run_static(scenario, engine=None) -> SimMetrics:
+    """simulator.py:206-250 on the GPU: the rate=inf dispatch sequence, then
+    per-instance greedy static batches (planner.py:51-101)."""
     if not math.isinf(scenario.arrival_rate):
         raise SpecError("static mode needs arrival_rate=inf (a fully known queue)")
-    raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, "static-mode replay is not in the engine yet (SURVEY 8f row 1)")
+    return _run(scenario, static=True, engine=engine)
 
 
 def run_scenario(scenario, engine=None) -> SimMetrics:
@@ -281,7 +296,7 @@ class ReplayBatchResult:
 
 
 def replay_traces(cluster, config, params, policy: PolicyConfig, offsets, input_len, output_len, pred_output_len,
-                  arrival=None, want_assign=True, want_depart=False, engine=None) -> ReplayBatchResult:
+                  arrival=None, want_assign=True, want_depart=False, engine=None, static=False) -> ReplayBatchResult:
     """Replay T traces (offsets [T+1]) on one deployment in one launch."""
     handles = build_instances(cluster, config, params)
     _check_scheduler(handles, policy)
@@ -290,7 +305,7 @@ def replay_traces(cluster, config, params, policy: PolicyConfig, offsets, input_
         raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"{N} instances (max {nat.HS_MAX_INSTANCES})")
     per_token = kv_bytes_per_token(cluster.model)
     eng = engine or nat.engine_for()
-    a, d, m, r = eng.replay(engine_instances(handles, policy), _policy_struct(policy, N, per_token),
+    a, d, m, r = eng.replay(engine_instances(handles, policy), _policy_struct(policy, N, per_token, 1 if static else 0),
                             np.ascontiguousarray(offsets, np.int64), np.ascontiguousarray(input_len, np.int32),
                             np.ascontiguousarray(output_len, np.int32), np.ascontiguousarray(pred_output_len, np.int32),
                             None if arrival is None else np.ascontiguousarray(arrival, np.float64),

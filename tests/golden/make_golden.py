@@ -179,28 +179,28 @@ def metrics_desc(m) -> dict:
     }
 
 
-def replay_scenario(profile, degrees, trace, rate, policy, seed):
+def replay_scenario(profile, degrees, trace, rate, policy, seed, mode="continuous"):
     cluster, params = ref_cluster(profile), ref_params(profile)
     cfg = hs.deployment_for(cluster.machines, degrees)
     return hs.Scenario(cluster=cluster, config=cfg, trace=tuple(trace), arrival_rate=rate, policy=policy,
-                       mode="continuous", seed=seed, params=params)
+                       mode=mode, seed=seed, params=params)
 
 
 def replay_case(name, profile, degrees, trace_desc, I, O, rate, seed, policies, predictor=None,
-                theta=2.0, wrr=None) -> dict:
+                theta=2.0, wrr=None, mode="continuous") -> dict:
     trace = ref_trace(I, O)
     pred = predictor or {"mode": "oracle"}
     pc = hs.PredictorConfig(mode=pred["mode"], mean=pred.get("mean"), stddev=pred.get("stddev"),
                             seed=pred.get("seed"))
     base = hs.PolicyConfig(policy=policies[0], theta=theta, wrr_weights=wrr, predictor=pc)
-    sc = replay_scenario(profile, degrees, trace, rate, base, seed)
-    case = {"kind": "replay", "name": name, "profile": profile_desc(profile), "degrees": degrees,
+    sc = replay_scenario(profile, degrees, trace, rate, base, seed, mode)
+    case = {"kind": "replay", "mode": mode, "name": name, "profile": profile_desc(profile), "degrees": degrees,
             "trace": trace_desc, "q": len(I), "rate": "inf" if math.isinf(rate) else H(rate), "seed": seed,
             "predictor": pred, "theta": H(theta), "wrr": wrr, "results": []}
     t0 = time.time()
     for pol in policies:
         scp = replay_scenario(profile, degrees, trace, rate,
-                              hs.PolicyConfig(policy=pol, theta=theta, wrr_weights=wrr, predictor=pc), seed)
+                              hs.PolicyConfig(policy=pol, theta=theta, wrr_weights=wrr, predictor=pc), seed, mode)
         try:
             m = hs.run_scenario(scp)
             case["results"].append(metrics_desc(m))
@@ -356,6 +356,36 @@ def build_replay_cases() -> list:
     return cases
 
 
+def build_static_cases() -> list:
+    """run_static (simulator.py:206-250), the first 'next' row of SURVEY 8f."""
+    cases = []
+    pols = ["OS", "RR", "WRR", "SI", "MB"]
+    rng = random.Random(21)
+    I = np.array([rng.randint(1, 64) for _ in range(300)], np.int32)
+    O = np.array([rng.randint(1, 64) for _ in range(300)], np.int32)
+    cases.append(replay_case("static_two_instance", two_instance_profile(), {"strong": 1, "weak": 1},
+                             {"kind": "randint64"}, I, O, math.inf, 0, pols, wrr=(4.0, 1.0), mode="static"))
+    cases.append(replay_case("static_two_instance_normal", two_instance_profile(), {"strong": 1, "weak": 1},
+                             {"kind": "randint64"}, I, O, math.inf, 5, ["OS", "MB"],
+                             predictor={"mode": "normal", "mean": 30, "stddev": 10, "seed": None}, mode="static"))
+    # criterion-3 shape: one machine x4 at tp 4, SI, 2000-token budget (test_acceptance.py:170-219)
+    p3 = tiny_profile([("m0", 4, (32 * 2000 + 200) // 4 + 1, "x")], limits=dict(max_input_len=512, max_output_len=512))
+    p3.params = {("m0", 4): POSITIVE}
+    rng3 = random.Random(1000)
+    I3 = np.array([rng3.randint(1, 64) for _ in range(200)], np.int32)
+    O3 = np.array([rng3.randint(1, 64) for _ in range(200)], np.int32)
+    cases.append(replay_case("static_criterion3", p3, {"m0": 4}, {"kind": "crit3"}, I3, O3, math.inf, 0, ["SI", "OS"],
+                             mode="static"))
+    I, O = wl.trace_lengths(3000, seed=7)
+    cases.append(replay_case("static_config4_small", wl.config4(), {a: 1 for a in wl.CONFIG4_TYPES}, {"seed": 7},
+                             I, O, math.inf, 0, ["OS", "RR", "MB"], mode="static"))
+    pb = tiny_profile([("m0", 1, 32 * 100 + 200, "x")], limits=dict(max_input_len=32, max_output_len=32))
+    pb.params = {("m0", 1): POSITIVE}
+    cases.append(replay_case("static_err_oversized", pb, {"m0": 1}, {"kind": "fixed"}, np.array([5, 400, 6], np.int32),
+                             np.array([5, 400, 6], np.int32), math.inf, 0, ["OS"], mode="static"))
+    return cases
+
+
 def build_exp_vectors() -> dict:
     rng = np.random.default_rng(5)
     xs = np.concatenate([rng.uniform(0, 1, 3000), rng.uniform(0, 20, 3000), rng.uniform(0, 709.7, 3000),
@@ -366,13 +396,15 @@ def build_exp_vectors() -> dict:
 
 
 def main() -> None:
-    which = sys.argv[1:] or ["exp", "search", "replay"]
+    which = sys.argv[1:] or ["exp", "search", "replay", "static"]
     if "exp" in which:
         (OUT / "exp_vectors.json").write_text(json.dumps(build_exp_vectors()))
     if "search" in which:
         (OUT / "search_cases.json").write_text(json.dumps(build_search_cases()))
     if "replay" in which:
         (OUT / "replay_cases.json").write_text(json.dumps(build_replay_cases()))
+    if "static" in which:
+        (OUT / "static_cases.json").write_text(json.dumps(build_static_cases()))
 
 
 if __name__ == "__main__":

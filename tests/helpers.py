@@ -72,9 +72,15 @@ def replay_trace(case):
         rng5 = np.random.default_rng(0)
         I = np.clip(np.round(rng5.lognormal(math.log(200) - 0.405, 0.9, 4000)), 1, 1024).astype(np.int64)
         O = np.clip(np.round(rng5.lognormal(math.log(150) - 0.08, 0.4, 4000)), 1, 1024).astype(np.int64)
+    elif kind == "crit3":
+        rng3 = random.Random(1000)
+        I = np.array([rng3.randint(1, 64) for _ in range(200)], np.int64)
+        O = np.array([rng3.randint(1, 64) for _ in range(200)], np.int64)
     elif kind == "fixed":
         if case["name"] == "err_oversized":
             I = np.array([400, 5, 6]); O = np.array([400, 5, 6])
+        elif case["name"] == "static_err_oversized":
+            I = np.array([5, 400, 6]); O = np.array([5, 400, 6])
         else:
             I = np.full(50, 60); O = np.full(50, 60)
             if case["name"] == "err_nonpositive_cost":
@@ -95,8 +101,8 @@ def scenario_from(case, policy_name: str) -> hs.Scenario:
     policy = hs.PolicyConfig(policy=policy_name, theta=fx(case["theta"]), wrr_weights=wrr, predictor=pc)
     rate = math.inf if case["rate"] == "inf" else fx(case["rate"])
     return hs.Scenario(cluster=cluster, config=hs.deployment_for(cluster.machines, case["degrees"]),
-                       trace=tuple(replay_trace(case)), arrival_rate=rate, policy=policy, mode="continuous",
-                       seed=case["seed"], params=params)
+                       trace=tuple(replay_trace(case)), arrival_rate=rate, policy=policy,
+                       mode=case.get("mode", "continuous"), seed=case["seed"], params=params)
 
 
 # ----------------------------------------------------------- C-struct inputs
@@ -129,6 +135,7 @@ def search_structs(cluster, params_by):
 
 def replay_structs(scenario):
     """(instances, policy, I, O, P, arrival-or-None) for hs_replay / oracle."""
+    static = scenario.mode == "static"
     from paper_2504_15303_b200.simulator import _policy_struct, _predictor, arrival_times, build_instances
     handles = build_instances(scenario.cluster, scenario.config, scenario.params)
     per_token = hs.kv_bytes_per_token(scenario.cluster.model)
@@ -137,8 +144,8 @@ def replay_structs(scenario):
     O = np.array([r.output_len for r in tr], np.int32)
     P = _predictor(scenario).predict_lengths(O.astype(np.int64)).astype(np.int32)
     T = None if math.isinf(scenario.arrival_rate) else arrival_times(len(tr), scenario.arrival_rate, scenario.seed)
-    return (engine_instances(handles, scenario.policy), _policy_struct(scenario.policy, len(handles), per_token),
-            handles, I, O, P, T)
+    return (engine_instances(handles, scenario.policy),
+            _policy_struct(scenario.policy, len(handles), per_token, 1 if static else 0), handles, I, O, P, T)
 
 
 ENTRY_STATUS = {"ok": nat.ENTRY_OK, "infeasible_config": nat.ENTRY_INFEASIBLE_CONFIG,
@@ -174,14 +181,17 @@ def check_table(case, table, nd, requests):
                 assert msg == row["msg"], (msg, row["msg"])
 
 
-def metrics_digest(assign, depart, metrics_row, handles, trace, arrival, policy):
+def metrics_digest(assign, depart, metrics_row, handles, trace, arrival, policy, static=False):
     """The same digest make_golden.metrics_desc computes from a SimMetrics."""
     import hashlib
     H = lambda x: float(x).hex()  # noqa: E731
     completion = metrics_row["completion_time"].tolist()
     tok = metrics_row["token_count"].tolist()
     makespan = max(completion)
-    order = np.lexsort((np.arange(len(trace)), assign.astype(np.int64), depart))
+    if static:
+        order = np.lexsort((np.arange(len(trace)), assign.astype(np.int64)))
+    else:
+        order = np.lexsort((np.arange(len(trace)), assign.astype(np.int64), depart))
     ids = [r.id for r in trace]
     arr = [0.0] * len(trace) if arrival is None else arrival.tolist()
     times = [(ids[k], arr[k], float(depart[k])) for k in order.tolist()]

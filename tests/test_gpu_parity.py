@@ -19,7 +19,7 @@ from paper_2504_15303_b200 import workloads as wl
 pytestmark = pytest.mark.gpu
 
 SEARCH = H.load("search_cases.json")
-REPLAY = H.load("replay_cases.json")
+REPLAY = H.load("replay_cases.json") + H.load("static_cases.json")
 
 
 @pytest.fixture(scope="module")
@@ -137,17 +137,17 @@ REPLAY_PARAMS = [(c, k) for c in REPLAY for k in range(len(c["results"]))]
 
 
 @pytest.mark.parametrize("case,k", REPLAY_PARAMS, ids=lambda v: v["name"] if isinstance(v, dict) else str(v))
-def test_run_continuous_matches_reference(eng, case, k):
+def test_run_scenario_matches_reference(eng, case, k):
     want = case["results"][k]
     sc = H.scenario_from(case, want["policy"])
     if "error" in want:
         exc = {"InfeasibleRequestError": hs.InfeasibleRequestError, "OverflowError": OverflowError,
                "SpecError": hs.SpecError, "SchedulingError": hs.SchedulingError}[want["error"]]
         with pytest.raises(exc) as ei:
-            hs.run_continuous(sc, engine=eng)
+            hs.run_scenario(sc, engine=eng)
         assert str(ei.value) == want["msg"]
         return
-    got = H.sim_digest(hs.run_continuous(sc, engine=eng))
+    got = H.sim_digest(hs.run_scenario(sc, engine=eng))
     for key, val in want.items():
         assert got[key] == val, (case["name"], want["policy"], key)
 
@@ -188,3 +188,32 @@ def test_batched_replay_vs_oracle(eng, policy):
         assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
     for f in ("request_count", "token_count"):
         assert np.array_equal(res.metrics[f], m[f]), f
+
+
+@pytest.mark.parametrize("policy", ["OS", "RR", "MB"])
+def test_batched_static_replay_vs_oracle(eng, policy):
+    """run_static on 48 ragged config-4-shaped traces vs the oracle."""
+    prof = wl.config4()
+    cluster = hs.ClusterSpec(hs.ModelSpec(**prof.model), hs.EngineOverheads(**prof.engine),
+                             tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+                             hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {a: 1 for a in wl.CONFIG4_TYPES})
+    rng = np.random.default_rng(5)
+    lens = [int(x) for x in rng.integers(1, 4000, 48)]
+    Is, Os = zip(*(wl.trace_lengths(q, seed=500 + t) for t, q in enumerate(lens)))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    I, O = np.concatenate(Is), np.concatenate(Os)
+    pol = hs.PolicyConfig(policy=policy)
+    res = hs.replay_traces(cluster, config, params, pol, off, I, O, O, want_assign=True, want_depart=True,
+                           engine=eng, static=True)
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    handles = build_instances(cluster, config, params)
+    a, d, m, r = orc.replay(engine_instances(handles, pol),
+                            _policy_struct(pol, 32, hs.kv_bytes_per_token(cluster.model), 1), off, I, O, O, None,
+                            nthreads=8)
+    assert (res.result["error"] == 0).all() and (r["error"] == 0).all()
+    assert np.array_equal(res.assign, a)
+    assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64))
+    for f in ("completion_time", "peak_kv_usage", "residual_load"):
+        assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f

@@ -114,7 +114,7 @@ def test_oracle_literal_candidates_match_reference_samples():
     assert n_ok >= 20
 
 
-REPLAY = H.load("replay_cases.json")
+REPLAY = H.load("replay_cases.json") + H.load("static_cases.json")
 REPLAY_PARAMS = [(c, k) for c in REPLAY for k in range(len(c["results"]))]
 
 
@@ -132,7 +132,8 @@ def test_oracle_replay_matches_reference(case, k):
         assert int(result[0]["error"]) == exp_err
         return
     assert int(result[0]["error"]) == nat.TRACE_OK
-    got = H.metrics_digest(assign, depart, metrics[0], handles, sc.trace, T, want["policy"])
+    got = H.metrics_digest(assign, depart, metrics[0], handles, sc.trace, T, want["policy"],
+                           static=sc.mode == "static")
     for key in ("assign_head", "assign_sha", "makespan", "per_instance", "residual_loads", "depart_sha",
                 "times_sha", "times_head", "throughput", "spread"):
         assert got[key] == want[key], (case["name"], want["policy"], key)
