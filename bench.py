@@ -357,7 +357,8 @@ def engine_arm(args, rank, world, local_rank):
             e2e_step()
         e2e_ms, _ = timed(e2e_step, args.steps)
         M = len(tables.names)
-        h2d = sI.nbytes + sO.nbytes + off.nbytes + hI.nbytes + hO.nbytes * 2 + hT.nbytes
+        # predictions are the outputs (oracle predictor): the library copies that buffer once
+        h2d = sI.nbytes + sO.nbytes + off.nbytes + hI.nbytes + hO.nbytes + hT.nbytes
         d2h = nreq + nT * N * nat.METRICS_DTYPE.itemsize + nT * nat.RESULT_DTYPE.itemsize + \
             M * nat.HS_MAX_DEGREES * nat.ENTRY_DTYPE.itemsize + 16
         if dist:

@@ -38,10 +38,16 @@ enum Slot {
 
 }  // namespace
 
+constexpr int kPipe = 8;  // replay chunks in flight on the host path
+
 struct hs_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;          // copies + search kernels
+  cudaStream_t aux = nullptr;             // per-chunk sizing reductions
+  cudaStream_t ks[kPipe] = {};            // replay kernels of the pipelined host path
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_copy[kPipe] = {}, ev_min[kPipe] = {}, ev_done[kPipe] = {};
+  int32_t* pinned_min = nullptr;          // page-locked per-chunk min(I+O)
   int64_t launches = 0;
   double last_ms = 0.0;
   void* buf[N_SLOTS] = {};
@@ -199,24 +205,23 @@ __global__ void k_gather_ranked(const double* total, const int64_t* idx, const i
   out[k].index = idx[k];
 }
 
-int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_t T, const int64_t* d_off,
-                const int64_t* h_off, const int32_t* d_I, const int32_t* d_O, const int32_t* d_P, const double* d_arr,
-                uint8_t* d_assign, double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result) {
+// Per-launch constants shared by every chunk (instance classes, policy).
+int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, hs::ReplayConst* out) {
   const int N = pol->n_instances;
   if (N < 1) return fail(HS_ERR_ARG, "n_instances must be >= 1");
   if (N > HS_MAX_INSTANCES)
     return fail(HS_ERR_UNSUPPORTED, "more than 32 instances per deployment is not supported yet");
   if (pol->policy < HS_POLICY_OS || pol->policy > HS_POLICY_MB) return fail(HS_ERR_ARG, "unknown policy");
   if (pol->per_token <= 0) return fail(HS_ERR_ARG, "per_token must be positive");
-  hs::ReplayConst rc;
+  if (pol->mode != 0 && pol->mode != 1) return fail(HS_ERR_ARG, "mode must be 0 (continuous) or 1 (static)");
+  if (pol->mode == 1 && has_arrival) return fail(HS_ERR_ARG, "static mode needs arrival = NULL (rate = inf)");
+  hs::ReplayConst& rc = *out;
   std::memset(&rc, 0, sizeof(rc));
   rc.N = N;
   rc.policy = pol->policy;
   rc.theta = pol->theta;
   rc.per_token = pol->per_token;
-  rc.has_arrival = d_arr != nullptr;
-  if (pol->mode != 0 && pol->mode != 1) return fail(HS_ERR_ARG, "mode must be 0 (continuous) or 1 (static)");
-  if (pol->mode == 1 && d_arr) return fail(HS_ERR_ARG, "static mode needs arrival = NULL (rate = inf)");
+  rc.has_arrival = has_arrival;
   rc.mode = pol->mode;
   int nt = 0;
   std::vector<double> wts(N);
@@ -225,10 +230,7 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
     if (ty < 0 || ty >= N) return fail(HS_ERR_ARG, "instance type out of range");
     if (!(inst[j].budget > 0)) return fail(HS_ERR_ARG, "instance budget must be positive");
     rc.inst_type[j] = ty;
-    if (ty >= nt) {
-      for (int k = nt; k <= ty; ++k) rc.type_budget[k] = 0.0;
-      nt = ty + 1;
-    }
+    if (ty >= nt) nt = ty + 1;
     std::memcpy(rc.type_p[ty], inst[j].p, sizeof(double) * 8);
     rc.type_budget[ty] = inst[j].budget;
     rc.type_cap_tokens[ty] = cap_tokens(inst[j].budget, pol->per_token);
@@ -237,17 +239,51 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
   }
   rc.n_types = nt;
   rc.wrr_total = pysum(wts.data(), N);
-  const int64_t total_q = h_off[T] - h_off[0];
-  int64_t max_q = 0;
+  return HS_OK;
+}
+
+// Heap overflow regions from the exact active-set bound: at most
+// floor(budget / (per_token * min(I+O))) requests fit an instance at once.
+void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q) {
+  if (min_need < 1) min_need = 1;
+  int64_t acc = 0;
+  for (int j = 0; j < rc.N; ++j) {
+    const double tokens = std::floor(inst[j].budget / (double)rc.per_token);
+    const double capd = std::floor(tokens / (double)min_need) + 1.0;
+    int64_t capj = capd > (double)max_q ? max_q : (int64_t)capd;
+    capj -= hs::kHeapShared;  // the first entries live in shared memory
+    if (capj < 1) capj = 1;
+    rc.heap_off[j] = acc;
+    acc += capj;
+  }
+  rc.heap_off[rc.N] = acc;
+  rc.heap_stride = (acc + 15) / 16 * 16;
+}
+
+int check_offsets(const int64_t* h_off, int64_t T, int64_t* max_q) {
+  *max_q = 0;
   for (int64_t t = 0; t < T; ++t) {
     const int64_t qt = h_off[t + 1] - h_off[t];
     if (qt < 0) return fail(HS_ERR_ARG, "offsets must be non-decreasing");
     if (qt > INT32_MAX) return fail(HS_ERR_UNSUPPORTED, "trace longer than 2^31 requests");
-    if (qt > max_q) max_q = qt;
+    if (qt > *max_q) *max_q = qt;
   }
-  // active-set bound per instance: per_token * sum(I+O) <= budget
-  int32_t* d_min = nullptr;
+  return HS_OK;
+}
+
+// Device-resident inputs: one sizing reduction, then the traces in as few
+// launches as the heap memory allows.
+int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_t T, const int64_t* d_off,
+                const int64_t* h_off, const int32_t* d_I, const int32_t* d_O, const int32_t* d_P, const double* d_arr,
+                uint8_t* d_assign, double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result) {
+  hs::ReplayConst rc;
   int rcode;
+  if ((rcode = make_const(inst, pol, d_arr != nullptr, &rc))) return rcode;
+  const int N = rc.N;
+  int64_t max_q;
+  if ((rcode = check_offsets(h_off, T, &max_q))) return rcode;
+  const int64_t total_q = h_off[T] - h_off[0];
+  int32_t* d_min = nullptr;
   if ((rcode = ensure_t(c, S_MINNEED, 1, &d_min))) return rcode;
   HS_CUDA(cudaMemsetAsync(d_min, 0x7f, sizeof(int32_t), c->stream));
   if (total_q > 0) {
@@ -257,23 +293,9 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
   int32_t min_need = 0;
   HS_CUDA(cudaMemcpyAsync(&min_need, d_min, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  if (min_need < 1) min_need = 1;
-  int64_t acc = 0;
-  for (int j = 0; j < N; ++j) {
-    const double tokens = std::floor(inst[j].budget / (double)pol->per_token);
-    double capd = std::floor(tokens / (double)min_need) + 1.0;
-    int64_t capj = capd > (double)max_q ? max_q : (int64_t)capd;
-    capj -= hs::kHeapShared;  // the first entries live in shared memory
-    if (capj < 1) capj = 1;
-    rc.heap_off[j] = acc;
-    acc += capj;
-  }
-  rc.heap_off[N] = acc;
-  rc.heap_stride = (acc + 15) / 16 * 16;
-
+  size_heaps(rc, inst, min_need, max_q);
   void* d_qrec;
   if ((rcode = ensure(c, S_WREC, (size_t)(h_off[T] > 0 ? h_off[T] : 1) * hs::kQRecBytes, &d_qrec))) return rcode;
-  // heap region, chunked over traces to bound memory
   size_t free_b = 0, tot_b = 0;
   HS_CUDA(cudaMemGetInfo(&free_b, &tot_b));
   const size_t per_trace = (size_t)rc.heap_stride * hs::kHEntBytes;
@@ -292,6 +314,23 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
     c->launches += 1;
   }
   return end_timing(c);
+}
+
+int ensure_pipeline(hs_ctx* c) {
+  if (c->aux) return HS_OK;
+  HS_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  for (int i = 0; i < kPipe; ++i) {
+    HS_CUDA(cudaStreamCreateWithFlags(&c->ks[i], cudaStreamNonBlocking));
+    HS_CUDA(cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming));
+    HS_CUDA(cudaEventCreateWithFlags(&c->ev_min[i], cudaEventDisableTiming));
+    HS_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+  }
+  HS_CUDA(cudaHostAlloc((void**)&c->pinned_min, sizeof(int32_t) * kPipe, cudaHostAllocDefault));
+  cudaMemPool_t pool;
+  HS_CUDA(cudaDeviceGetDefaultMemPool(&pool, c->device));
+  uint64_t keep = UINT64_MAX;  // keep freed chunk heaps in the pool between calls
+  HS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  return HS_OK;
 }
 
 __global__ void k_probe_fp64(double* out, int iters) {
@@ -342,6 +381,16 @@ int hs_ctx_destroy(hs_ctx* c) {
     if (c->buf[s]) cudaFree(c->buf[s]);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->aux) {
+    for (int i = 0; i < kPipe; ++i) {
+      cudaStreamDestroy(c->ks[i]);
+      cudaEventDestroy(c->ev_copy[i]);
+      cudaEventDestroy(c->ev_min[i]);
+      cudaEventDestroy(c->ev_done[i]);
+    }
+    cudaStreamDestroy(c->aux);
+    cudaFreeHost(c->pinned_min);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return HS_OK;
@@ -532,7 +581,14 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
   if (off[0] != 0) return fail(HS_ERR_ARG, "offsets[0] must be 0");
   const int64_t total = off[T];
   if (total > 0 && (!b->input_len || !b->output_len || !b->pred_output_len)) return fail(HS_ERR_ARG, "null trace");
+  hs::ReplayConst base;
+  if ((rc = make_const(inst, pol, b->arrival != nullptr, &base))) return rc;
+  int64_t max_q;
+  if ((rc = check_offsets(off, T, &max_q))) return rc;
+  if ((rc = ensure_pipeline(c))) return rc;
   const int N = pol->n_instances;
+  // predictions identical to the outputs (oracle predictor): copy once
+  const bool p_is_o = b->pred_output_len == b->output_len;
   int64_t* dOff;
   int32_t *dI, *dO, *dP;
   double* dT = nullptr;
@@ -540,23 +596,85 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
   double* dDep = nullptr;
   hs_inst_metrics* dM;
   hs_trace_result* dR;
+  void* dQ;
   const size_t tq = (size_t)(total > 0 ? total : 1);
   if ((rc = ensure_t(c, S_OFF, (size_t)T + 1, &dOff)) || (rc = ensure_t(c, S_I, tq, &dI)) ||
-      (rc = ensure_t(c, S_O, tq, &dO)) || (rc = ensure_t(c, S_P, tq, &dP)) ||
-      (rc = ensure_t(c, S_METRICS, (size_t)(T > 0 ? T : 1) * (N > 0 ? N : 1), &dM)) ||
-      (rc = ensure_t(c, S_RESULT, (size_t)(T > 0 ? T : 1), &dR)))
+      (rc = ensure_t(c, S_O, tq, &dO)) || (rc = ensure_t(c, S_METRICS, (size_t)(T > 0 ? T : 1) * N, &dM)) ||
+      (rc = ensure_t(c, S_RESULT, (size_t)(T > 0 ? T : 1), &dR)) ||
+      (rc = ensure(c, S_WREC, tq * hs::kQRecBytes, &dQ)))
     return rc;
+  if (p_is_o) {
+    dP = dO;
+  } else if ((rc = ensure_t(c, S_P, tq, &dP))) {
+    return rc;
+  }
   if (b->arrival && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
   if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
   if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
   HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
-  if (total > 0) {
-    HS_CUDA(cudaMemcpyAsync(dI, b->input_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
-    HS_CUDA(cudaMemcpyAsync(dO, b->output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
-    HS_CUDA(cudaMemcpyAsync(dP, b->pred_output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
-    if (dT) HS_CUDA(cudaMemcpyAsync(dT, b->arrival, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
+  // Chunks of traces: copy chunk i on the copy stream while earlier chunks
+  // replay on their own streams; each chunk sizes its heaps exactly from
+  // its own min(I + O).
+  const int64_t nch = T < kPipe ? (T > 0 ? T : 0) : kPipe;
+  std::vector<hs::ReplayConst> rcs((size_t)(nch > 0 ? nch : 1), base);
+  std::vector<void*> heaps((size_t)(nch > 0 ? nch : 1), nullptr);
+  auto bounds = [&](int64_t i, int64_t* t0, int64_t* t1) {
+    *t0 = T * i / nch;
+    *t1 = T * (i + 1) / nch;
+  };
+  auto enqueue_copy = [&](int64_t i) -> int {
+    int64_t t0, t1;
+    bounds(i, &t0, &t1);
+    const int64_t a = off[t0], n = off[t1] - off[t0];
+    if (n > 0) {
+      HS_CUDA(cudaMemcpyAsync(dI + a, b->input_len + a, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+      HS_CUDA(cudaMemcpyAsync(dO + a, b->output_len + a, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+      if (!p_is_o)
+        HS_CUDA(cudaMemcpyAsync(dP + a, b->pred_output_len + a, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                                c->stream));
+      if (dT) HS_CUDA(cudaMemcpyAsync(dT + a, b->arrival + a, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    }
+    HS_CUDA(cudaEventRecord(c->ev_copy[i], c->stream));
+    HS_CUDA(cudaStreamWaitEvent(c->aux, c->ev_copy[i], 0));
+    int32_t* d_min;
+    int r2;
+    if ((r2 = ensure_t(c, S_MINNEED, kPipe, &d_min))) return r2;
+    HS_CUDA(cudaMemsetAsync(d_min + i, 0x7f, sizeof(int32_t), c->aux));
+    if (n > 0) {
+      HS_CUDA(hs::launch_min_need(dI + a, dO + a, n, d_min + i, c->aux));
+      c->launches += 1;
+    }
+    HS_CUDA(cudaMemcpyAsync(c->pinned_min + i, d_min + i, sizeof(int32_t), cudaMemcpyDeviceToHost, c->aux));
+    HS_CUDA(cudaEventRecord(c->ev_min[i], c->aux));
+    return HS_OK;
+  };
+  auto launch_chunk = [&](int64_t i) -> int {
+    int64_t t0, t1;
+    bounds(i, &t0, &t1);
+    HS_CUDA(cudaEventSynchronize(c->ev_min[i]));
+    int64_t mq = 0;
+    for (int64_t t = t0; t < t1; ++t) mq = (off[t + 1] - off[t]) > mq ? (off[t + 1] - off[t]) : mq;
+    hs::ReplayConst& rci = rcs[i];
+    size_heaps(rci, inst, c->pinned_min[i], mq);
+    cudaStream_t ks = c->ks[i % kPipe];
+    HS_CUDA(cudaStreamWaitEvent(ks, c->ev_copy[i], 0));
+    const size_t hb = (size_t)(t1 - t0 > 0 ? t1 - t0 : 1) * rci.heap_stride * hs::kHEntBytes;
+    HS_CUDA(cudaMallocAsync(&heaps[i], hb, ks));
+    HS_CUDA(hs::launch_replay(rci, t1 - t0, dOff + t0, dI, dO, dP, dT, dA, dDep, dM + t0 * N, dR + t0, dQ,
+                              static_cast<uint64_t*>(heaps[i]), ks));
+    c->launches += 1;
+    HS_CUDA(cudaFreeAsync(heaps[i], ks));
+    HS_CUDA(cudaEventRecord(c->ev_done[i], ks));
+    return HS_OK;
+  };
+  if ((rc = begin_timing(c))) return rc;
+  if (nch > 0 && (rc = enqueue_copy(0))) return rc;
+  for (int64_t i = 0; i < nch; ++i) {
+    if (i + 1 < nch && (rc = enqueue_copy(i + 1))) return rc;
+    if ((rc = launch_chunk(i))) return rc;
   }
-  if ((rc = replay_impl(c, inst, pol, T, dOff, off, dI, dO, dP, dT, dA, dDep, dM, dR))) return rc;
+  for (int64_t i = 0; i < nch; ++i) HS_CUDA(cudaStreamWaitEvent(c->stream, c->ev_done[i], 0));
+  if ((rc = end_timing(c))) return rc;
   if (T > 0) {
     HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * N, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));

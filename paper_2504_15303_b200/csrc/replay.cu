@@ -41,7 +41,6 @@
 
 namespace hs {
 
-__constant__ ReplayConst c_rep;
 
 #ifdef HS_TIMERS
 // Diagnostic build only (-DHS_TIMERS): per-warp cycle counts of the replay
@@ -153,7 +152,8 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
-             hs_trace_result* __restrict__ result, QRec* __restrict__ qrec_all, uint64_t* __restrict__ heap_all) {
+             hs_trace_result* __restrict__ result, QRec* __restrict__ qrec_all, uint64_t* __restrict__ heap_all,
+             const __grid_constant__ ReplayConst c_rep) {
   __shared__ uint64_t s_tab[256];
   __shared__ Cold s_cold[kWarps * 32];
   __shared__ HEnt s_heap[kWarps * 32][kHS];
@@ -675,8 +675,7 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
                           double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec,
                           uint64_t* d_heap, cudaStream_t st) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_rep, &rc, sizeof(ReplayConst), 0, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   if (n_traces <= 0) return cudaSuccess;
   const size_t smem = (size_t)kWarps * 32 * rc.n_types * sizeof(double);
   if (smem > 16 * 1024) {
@@ -685,7 +684,7 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
   }
   const unsigned blocks = (unsigned)((n_traces + kWarps - 1) / kWarps);
   k_replay<<<blocks, kWarps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
-                                              d_result, static_cast<QRec*>(d_qrec), d_heap);
+                                              d_result, static_cast<QRec*>(d_qrec), d_heap, rc);
   return cudaGetLastError();
 }
 
