@@ -223,6 +223,14 @@ int hs_search_best(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees,
 int hs_search_rank(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees, int32_t n_machines,
                    hs_cand* ranked, int64_t* n_ranked, int8_t* first_bad);
 
+/* Top-k of the ranking (planner.py:227 order: total desc, index asc) over
+ * shard `shard` of `n_shards` equal blocks of the FEASIBLE sub-product
+ * (only feasible candidates are ranked).  out[0 .. *n_out) is sorted;
+ * *n_feasible = feasible candidates in the shard.  Shard results merge by
+ * the same order. */
+int hs_search_topk(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees, int32_t n_machines, int64_t k,
+                   int32_t shard, int32_t n_shards, hs_cand* out, int64_t* n_out, int64_t* n_feasible);
+
 /* ---- batched scheduler replay ------------------------------------------ */
 /* Replay every trace of the batch on the same instance set.  assign
  * ([total requests], may be NULL) receives the chosen instance per request;

@@ -404,6 +404,81 @@ int hs_oracle_best(const hs_entry* table, const int32_t* nd, int32_t M, int64_t 
   return HS_OK;
 }
 
+/* top-k of planner.py:227's order over shard `shard` of the feasible
+ * sub-product (same contract as hs_search_topk): enumerate, keep the k best
+ * in a heap whose root is the worst kept candidate. */
+static int cmp_cand(const void* a, const void* b);
+static int cand_worse(const hs_cand* a, const hs_cand* b) { /* a ranks after b */
+  double ka = -a->total, kb = -b->total;
+  if (ka != kb) return ka > kb;
+  return a->index > b->index;
+}
+static void worst_sift_down(hs_cand* h, int64_t n, int64_t i) {
+  for (;;) {
+    int64_t l = 2 * i + 1, r = l + 1, m = i;
+    if (l < n && cand_worse(&h[l], &h[m])) m = l;
+    if (r < n && cand_worse(&h[r], &h[m])) m = r;
+    if (m == i) return;
+    hs_cand t = h[i]; h[i] = h[m]; h[m] = t; i = m;
+  }
+}
+int hs_oracle_topk(const hs_entry* table, const int32_t* nd, int32_t M, int64_t k, int32_t shard, int32_t n_shards,
+                   hs_cand* out, int64_t* n_out, int64_t* n_feasible) {
+  int32_t D[HS_MAX_MACHINES], orig[HS_MAX_MACHINES][HS_MAX_DEGREES];
+  double C[HS_MAX_MACHINES][HS_MAX_DEGREES];
+  int64_t stride[HS_MAX_MACHINES];
+  int64_t st = 1;
+  i128 F = 1;
+  for (int32_t i = M - 1; i >= 0; --i) {
+    stride[i] = st;
+    st *= nd[i];
+    int32_t ok = 0;
+    for (int32_t d = 0; d < nd[i]; ++d) {
+      const hs_entry* e = &table[i * HS_MAX_DEGREES + d];
+      if (e->status != HS_ENTRY_OK) continue;
+      C[i][ok] = e->contribution;
+      orig[i][ok] = d;
+      ++ok;
+    }
+    D[i] = ok;
+    F *= ok;
+  }
+  *n_out = 0;
+  *n_feasible = 0;
+  if (F == 0) return HS_OK;
+  int64_t items = (int64_t)(F / D[M - 1]);
+  int64_t ib = items * shard / n_shards, ie = items * (shard + 1) / n_shards;
+  *n_feasible = (ie - ib) * D[M - 1];
+  int32_t dig[HS_MAX_MACHINES];
+  int64_t x = ib;
+  for (int32_t i = M - 2; i >= 0; --i) { dig[i] = (int32_t)(x % D[i]); x /= D[i]; }
+  int64_t n = 0;
+  for (int64_t it = ib; it < ie; ++it) {
+    double pre = 0.0;
+    int64_t pidx = 0;
+    for (int32_t i = 0; i < M - 1; ++i) { pre = pre + C[i][dig[i]]; pidx += (int64_t)orig[i][dig[i]] * stride[i]; }
+    for (int32_t d = 0; d < D[M - 1]; ++d) {
+      hs_cand c = {pre + C[M - 1][d], pidx + (int64_t)orig[M - 1][d] * stride[M - 1]};
+      if (n < k) {
+        out[n] = c;
+        int64_t i = n++;
+        while (i > 0) {
+          int64_t p = (i - 1) / 2;
+          if (!cand_worse(&out[i], &out[p])) break;
+          hs_cand t = out[i]; out[i] = out[p]; out[p] = t; i = p;
+        }
+      } else if (k > 0 && cand_worse(&out[0], &c)) {
+        out[0] = c;
+        worst_sift_down(out, n, 0);
+      }
+    }
+    for (int32_t i = M - 2; i >= 0; --i) { if (++dig[i] < D[i]) break; dig[i] = 0; }
+  }
+  qsort(out, (size_t)n, sizeof(hs_cand), cmp_cand);
+  *n_out = n;
+  return HS_OK;
+}
+
 /* planner.py:227 ranked.sort(key=(-total, tp tuple)): stable sort of the
  * feasible candidates (product order) by descending total. */
 static int cmp_cand(const void* a, const void* b) {

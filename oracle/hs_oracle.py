@@ -47,6 +47,8 @@ def lib() -> C.CDLL:
         L.hs_oracle_candidates_literal.restype = C.c_int
         L.hs_oracle_best.argtypes = [vp, vp, i32, i64, i64, C.c_int, vp, vp]
         L.hs_oracle_best.restype = C.c_int
+        L.hs_oracle_topk.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp]
+        L.hs_oracle_topk.restype = C.c_int
         L.hs_oracle_rank.argtypes = [vp, vp, i32, vp, vp, vp]
         L.hs_oracle_rank.restype = C.c_int
         L.hs_oracle_replay.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, vp]
@@ -121,6 +123,18 @@ def best(table, nd, begin, end, nthreads=1):
                               int(nthreads), _p(out), _p(nf))
     assert rc == 0
     return float(out["total"][0]), int(out["index"][0]), int(nf[0])
+
+
+def topk(table, nd, k, shard=0, n_shards=1):
+    from paper_2504_15303_b200 import _native as nat
+    out = np.zeros(max(k, 1), nat.CAND_DTYPE)
+    n = np.zeros(1, np.int64)
+    nf = np.zeros(1, np.int64)
+    t = np.ascontiguousarray(table.reshape(-1))
+    rc = lib().hs_oracle_topk(_p(t), _p(np.ascontiguousarray(nd, np.int32)), len(nd), int(k), int(shard),
+                              int(n_shards), _p(out), _p(n), _p(nf))
+    assert rc == 0
+    return out[: n[0]], int(nf[0])
 
 
 def rank(table, nd):

@@ -106,7 +106,7 @@ RESULT_DTYPE = np.dtype([("error", "<i4"), ("err_instance", "<i4"), ("err_reques
 # every symbol include/hetserve_b200.h declares
 EXPORTS = (
     "hs_abi_version", "hs_ctx_create", "hs_ctx_destroy", "hs_last_error", "hs_ctx_launch_count",
-    "hs_ctx_last_kernel_ms", "hs_search_tables", "hs_search_best", "hs_search_rank", "hs_replay",
+    "hs_ctx_last_kernel_ms", "hs_search_tables", "hs_search_best", "hs_search_rank", "hs_search_topk", "hs_replay",
     "hs_replay_device", "hs_device_alloc", "hs_device_free", "hs_memcpy_h2d", "hs_memcpy_d2h",
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
 )
@@ -136,6 +136,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_search_tables": ([vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, vp], C.c_int),
             "hs_search_best": ([vp, vp, vp, i32, i64, i64, vp, vp], C.c_int),
             "hs_search_rank": ([vp, vp, vp, i32, vp, vp, vp], C.c_int),
+            "hs_search_topk": ([vp, vp, vp, i32, i64, i32, i32, vp, vp, vp], C.c_int),
             "hs_replay": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
             "hs_replay_device": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
             "hs_device_alloc": ([vp, i64, C.POINTER(vp)], C.c_int),
@@ -281,6 +282,16 @@ class Engine:
                                      _ptr(ranked), C.byref(n), _ptr(first_bad))
         self.check(rc, "hs_search_rank")
         return ranked[: n.value], first_bad[:P]
+
+    def search_topk(self, table: np.ndarray, nd: np.ndarray, k: int, shard: int = 0, n_shards: int = 1):
+        out = np.zeros(max(k, 1), dtype=CAND_DTYPE)
+        n = C.c_int64()
+        nf = C.c_int64()
+        t = np.ascontiguousarray(table.reshape(-1))
+        rc = self.lib.hs_search_topk(self.handle, _ptr(t), _ptr(np.ascontiguousarray(nd, np.int32)), len(nd), int(k),
+                                     int(shard), int(n_shards), _ptr(out), C.byref(n), C.byref(nf))
+        self.check(rc, "hs_search_topk")
+        return out[: n.value], int(nf.value)
 
     # ---------------------------------------------------------------- replay
     def replay(self, instances, policy: hs_policy, offsets: np.ndarray, I: np.ndarray, O: np.ndarray,

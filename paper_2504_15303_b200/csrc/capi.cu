@@ -33,7 +33,8 @@ int fail(int code, const std::string& msg) {
 enum Slot {
   S_I, S_O, S_P, S_T, S_OFF, S_DESC, S_TABLE, S_BLK_BEST, S_BLK_IDX, S_BLK_CNT, S_CAND, S_CNT,
   S_TOTAL, S_FIRSTBAD, S_FLAG, S_SELIDX, S_NSEL, S_KEYS, S_KEYS2, S_IDX2, S_CUBTMP, S_RANKED,
-  S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_QNEXT, S_HEAP, S_MINNEED, N_SLOTS
+  S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_QNEXT, S_HEAP, S_MINNEED, S_TK_HIST, S_TK_CNT, S_TK_KEY,
+  S_TK_IDX, S_TK_KEY2, S_TK_IDX2, N_SLOTS
 };
 
 }  // namespace
@@ -567,6 +568,126 @@ int hs_search_rank(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
   HS_CUDA(cudaMemcpyAsync(first_bad, fb, (size_t)P, cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   *n_ranked = h_nsel;
+  return HS_OK;
+}
+
+int hs_search_topk(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t M, int64_t k, int32_t shard,
+                   int32_t n_shards, hs_cand* out, int64_t* n_out, int64_t* n_feasible) {
+  if (!c || !table || !nd || !out || !n_out || !n_feasible) return fail(HS_ERR_ARG, "null argument");
+  if (M < 1 || M > HS_MAX_MACHINES) return fail(HS_ERR_ARG, "n_machines out of range");
+  if (k < 0 || n_shards < 1 || shard < 0 || shard >= n_shards) return fail(HS_ERR_ARG, "bad k / shard");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  hs::FeasSpace fs;
+  std::memset(&fs, 0, sizeof(fs));
+  fs.M = M;
+  long double F = 1;
+  int64_t stride = 1;
+  for (int32_t i = M - 1; i >= 0; --i) {
+    if (nd[i] < 1 || nd[i] > HS_MAX_DEGREES) return fail(HS_ERR_ARG, "n_degrees out of range");
+    fs.stride[i] = stride;
+    stride *= nd[i];
+    int32_t ok = 0;
+    for (int32_t d = 0; d < nd[i]; ++d) {
+      const hs_entry& e = table[i * HS_MAX_DEGREES + d];
+      if (e.status != HS_ENTRY_OK) continue;
+      if (std::isnan(e.contribution)) return fail(HS_ERR_UNSUPPORTED, "a feasible contribution is NaN");
+      fs.C[i * HS_MAX_DEGREES + ok] = e.contribution;
+      fs.orig[i * HS_MAX_DEGREES + ok] = d;
+      ++ok;
+    }
+    fs.D[i] = ok;
+    F *= ok;
+  }
+  *n_out = 0;
+  *n_feasible = 0;
+  if (F == 0) return HS_OK;
+  if (F > 4.6e18L) return fail(HS_ERR_ARG, "feasible space exceeds 2^62");
+  const int64_t DL = fs.D[M - 1];
+  const int64_t items = (int64_t)(F / DL);
+  const int64_t ib = items * shard / n_shards, ie = items * (shard + 1) / n_shards;
+  const int64_t nf = (ie - ib) * DL;
+  *n_feasible = nf;
+  const int64_t K = k < nf ? k : nf;
+  if (K == 0) return HS_OK;
+  const int64_t CAP = (int64_t)1 << 20;
+  unsigned long long *d_hist, *d_cnt;
+  uint64_t *d_key, *d_key2;
+  int64_t *d_idx, *d_idx2;
+  if ((rc = ensure_t(c, S_TK_HIST, 4096, &d_hist)) || (rc = ensure_t(c, S_TK_CNT, 1, &d_cnt)) ||
+      (rc = ensure_t(c, S_TK_KEY, (size_t)CAP, &d_key)) || (rc = ensure_t(c, S_TK_IDX, (size_t)CAP, &d_idx)) ||
+      (rc = ensure_t(c, S_TK_KEY2, (size_t)CAP, &d_key2)) || (rc = ensure_t(c, S_TK_IDX2, (size_t)CAP, &d_idx2)))
+    return rc;
+  int blocks = hs::sm_count() * 8;
+  const int64_t nb = (ie - ib + 255) / 256;
+  if (nb < blocks) blocks = (int)(nb > 0 ? nb : 1);
+  std::vector<unsigned long long> h(4096);
+  uint64_t prefix = 0;
+  int64_t need = K, above = 0;
+  int shift = 52;
+  uint64_t thr = 0;
+  bool uploaded = false;
+  if ((rc = begin_timing(c))) return rc;
+  for (;; shift -= 12) {
+    HS_CUDA(cudaMemsetAsync(d_hist, 0, 4096 * sizeof(unsigned long long), c->stream));
+    HS_CUDA(hs::launch_topk_pass(fs, !uploaded, 0, ib, ie, shift, prefix, 0, d_hist, d_cnt, d_key, d_idx, CAP, blocks,
+                                 c->stream));
+    uploaded = true;
+    c->launches += 1;
+    HS_CUDA(cudaMemcpyAsync(h.data(), d_hist, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    int bsel = -1;
+    int64_t cum = 0;
+    for (int bb = 4095; bb >= 0; --bb) {
+      if (cum + (int64_t)h[bb] >= need) {
+        bsel = bb;
+        break;
+      }
+      cum += (int64_t)h[bb];
+    }
+    if (bsel < 0) return fail(HS_ERR_CUDA, "top-k radix select lost candidates");
+    need -= cum;
+    above += cum;
+    prefix = (shift == 52) ? (uint64_t)bsel : ((prefix << 12) | (uint64_t)bsel);
+    thr = prefix << shift;
+    if (above + (int64_t)h[bsel] <= CAP || shift == 4) break;
+  }
+  HS_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), c->stream));
+  HS_CUDA(hs::launch_topk_pass(fs, false, 1, ib, ie, shift, prefix, thr, d_hist, d_cnt, d_key, d_idx, CAP, blocks,
+                               c->stream));
+  c->launches += 1;
+  unsigned long long got = 0;
+  HS_CUDA(cudaMemcpyAsync(&got, d_cnt, sizeof(got), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  if ((int64_t)got > CAP) return fail(HS_ERR_UNSUPPORTED, "more than 2^20 candidates tie at the top-k boundary");
+  const int n = (int)got;
+  // stable sorts: by index ascending, then by total descending (~key ascending)
+  size_t t1 = 0, t2 = 0;
+  HS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, d_idx, d_idx2, d_key, d_key2, n, 0, 64, c->stream));
+  HS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, d_key2, d_key, d_idx2, d_idx, n, 0, 64, c->stream));
+  void* tmp;
+  if ((rc = ensure(c, S_CUBTMP, t1 > t2 ? t1 : t2, &tmp))) return rc;
+  size_t tn = c->cap[S_CUBTMP];
+  HS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tn, d_idx, d_idx2, d_key, d_key2, n, 0, 64, c->stream));
+  HS_CUDA(hs::launch_invert_keys(d_key2, n, c->stream));
+  tn = c->cap[S_CUBTMP];
+  HS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tn, d_key2, d_key, d_idx2, d_idx, n, 0, 64, c->stream));
+  c->launches += 3;
+  if ((rc = end_timing(c))) return rc;
+  std::vector<uint64_t> hk((size_t)K);
+  std::vector<int64_t> hi((size_t)K);
+  HS_CUDA(cudaMemcpyAsync(hk.data(), d_key, sizeof(uint64_t) * K, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaMemcpyAsync(hi.data(), d_idx, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int64_t j = 0; j < K; ++j) {
+    const uint64_t key = ~hk[j];
+    const uint64_t u = (key >> 63) ? (key & 0x7fffffffffffffffull) : ~key;
+    double v;
+    std::memcpy(&v, &u, 8);
+    out[j].total = v;
+    out[j].index = hi[j];
+  }
+  *n_out = K;
   return HS_OK;
 }
 

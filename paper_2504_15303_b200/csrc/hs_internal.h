@@ -38,6 +38,15 @@ struct SpaceDesc {
   double C[kMaxM * HS_MAX_DEGREES];
 };
 
+// Feasible sub-product for top-K: per machine its OK degrees only.
+struct FeasSpace {
+  int32_t M;
+  int32_t D[kMaxM];                      // OK degrees per machine
+  int64_t stride[kMaxM];                 // stride of the ORIGINAL mixed radix
+  double C[kMaxM * HS_MAX_DEGREES];      // contribution of the d-th OK degree
+  int32_t orig[kMaxM * HS_MAX_DEGREES];  // its original digit
+};
+
 struct ReplayConst {
   int32_t N;
   int32_t policy;
@@ -66,6 +75,11 @@ cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, 
                                hs_cand* d_out, int64_t* d_cnt_out, cudaStream_t st);
 cudaError_t launch_search_score(const SpaceDesc& sd, int32_t m_real_offset, int64_t P, double* d_total,
                                 int8_t* d_first_bad, uint8_t* d_flag, cudaStream_t st);
+cudaError_t launch_topk_pass(const FeasSpace& fs, bool upload, int mode, int64_t item_begin, int64_t item_end,
+                             int shift, uint64_t prefix, uint64_t thr, unsigned long long* d_hist,
+                             unsigned long long* d_cnt, uint64_t* d_key, int64_t* d_idx, int64_t cap, int blocks,
+                             cudaStream_t st);
+cudaError_t launch_invert_keys(uint64_t* d_key, int64_t n, cudaStream_t st);
 cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st);
 cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                           const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,

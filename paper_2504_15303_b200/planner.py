@@ -318,6 +318,22 @@ def search_best(tables: SearchTables, begin: int = 0, end: int | None = None, en
     return total, idx, nfeas, eng.last_kernel_ms
 
 
+def search_topk(tables: SearchTables, k: int, shard: int = 0, n_shards: int = 1, engine=None):
+    """Top-k of planner.py:227's ranking (total desc, index asc) over one
+    shard of the feasible sub-product.  Returns (cands, n_feasible,
+    kernel_ms) with cands a structured array of (total, index)."""
+    eng = engine or nat.engine_for()
+    cands, nf = eng.search_topk(tables.entries, tables.n_degrees, k, shard, n_shards)
+    return cands, nf, eng.last_kernel_ms
+
+
+def merge_topk(parts, k: int) -> np.ndarray:
+    """Merge per-shard top-k lists (same order rule)."""
+    allc = np.concatenate([p for p in parts if len(p)]) if any(len(p) for p in parts) else np.zeros(0, nat.CAND_DTYPE)
+    order = sorted(range(len(allc)), key=lambda j: (-float(allc[j]["total"]), int(allc[j]["index"])))
+    return allc[order[:k]]
+
+
 def best_config(tables: SearchTables, index: int) -> ThroughputEstimate:
     """The ThroughputEstimate of candidate `index` (as search_optimal_config
     would report it), from the table."""

@@ -217,3 +217,30 @@ def test_batched_static_replay_vs_oracle(eng, policy):
     assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64))
     for f in ("completion_time", "peak_kv_usage", "residual_load"):
         assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
+
+
+def test_config3_top1024_vs_oracle(eng):
+    """BASELINE config 5's first stage: top-1024 of the 5^16 space."""
+    _case, _req, t = _config3_tables(eng)
+    top, nf, _ms = planner.search_topk(t, 1024, engine=eng)
+    want, wnf = orc.topk(t.entries, t.n_degrees, 1024)
+    assert nf == wnf == 5184 ** 2
+    assert top["index"].tolist() == want["index"].tolist()
+    assert top["total"].view(np.uint64).tolist() == want["total"].view(np.uint64).tolist()
+    # head agrees with the exhaustive argmax
+    total, idx, _n, _ = planner.search_best(t, engine=eng)
+    assert (float(top["total"][0]), int(top["index"][0])) == (total, idx)
+    parts = [planner.search_topk(t, 1024, s, 4, engine=eng)[0] for s in range(4)]
+    merged = planner.merge_topk(parts, 1024)
+    assert merged["index"].tolist() == want["index"].tolist()
+
+
+@pytest.mark.parametrize("case", [c for c in SEARCH if c["kind"] == "search" and c.get("ranked")],
+                         ids=lambda c: c["name"])
+def test_topk_is_head_of_reference_ranking(eng, case):
+    cluster = H.cluster_from(case["profile"])
+    t = planner.build_tables(cluster, H.search_trace(case), H.params_from(case["profile"]), engine=eng)
+    k = len(case["ranked"])
+    top, nf, _ = planner.search_topk(t, k + 5, engine=eng)
+    assert nf == k
+    assert [float(x).hex() for x in top["total"]] == [r["total"] for r in case["ranked"]]

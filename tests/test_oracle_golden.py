@@ -137,3 +137,23 @@ def test_oracle_replay_matches_reference(case, k):
     for key in ("assign_head", "assign_sha", "makespan", "per_instance", "residual_loads", "depart_sha",
                 "times_sha", "times_head", "throughput", "spread"):
         assert got[key] == want[key], (case["name"], want["policy"], key)
+
+
+@pytest.mark.parametrize("case", [c for c in SEARCH if c["kind"] == "search" and c.get("ranked")],
+                         ids=lambda c: c["name"])
+def test_oracle_topk_is_head_of_reference_ranking(case):
+    cluster = H.cluster_from(case["profile"])
+    requests = H.search_trace(case)
+    model, engine, limits, machines, params, present = H.search_structs(cluster, H.params_from(case["profile"]))
+    I = np.array([r.input_len for r in requests], np.int32)
+    O = np.array([r.output_len for r in requests], np.int32)
+    table, nd = orc.tables(model, engine, limits, machines, params, present, I, O)
+    k = max(1, len(case["ranked"]) // 2)
+    top, nf = orc.topk(table, nd, k)
+    assert nf == len(case["ranked"])
+    assert [float(x).hex() for x in top["total"]] == [r["total"] for r in case["ranked"][:k]]
+    # shards merge to the same head
+    parts = [orc.topk(table, nd, k, s, 3)[0] for s in range(3)]
+    from paper_2504_15303_b200.planner import merge_topk
+    merged = merge_topk(parts, k)
+    assert merged["index"].tolist() == top["index"].tolist()
