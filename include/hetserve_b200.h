@@ -42,7 +42,8 @@ extern "C" {
 #define HS_ABI_VERSION 2
 #define HS_MAX_DEGREES 32   /* power-of-two divisors of an accelerator count  */
 #define HS_MAX_MACHINES 64
-#define HS_MAX_INSTANCES 32 /* one warp lane per instance (round-1 kernel)    */
+#define HS_MAX_INSTANCES 128 /* one lane per instance, up to 4 warps per trace */
+#define HS_MAX_CLASSES 32    /* distinct (params, budget) instance classes      */
 
 /* call status */
 enum hs_status {
@@ -239,6 +240,16 @@ int hs_search_topk(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees,
 int hs_replay(hs_ctx* ctx, const hs_instance* instances, const hs_policy* policy,
               const hs_trace_batch* batch, uint8_t* assign, double* depart,
               hs_inst_metrics* metrics, hs_trace_result* result);
+
+/* Per-trace deployments (BASELINE config 5: each of the top-k deployments
+ * replayed on its own trace).  Deployment d owns instances
+ * [inst_offsets[d], inst_offsets[d+1]) (types numbered per deployment);
+ * trace t runs deployment trace_deployment[t]; policy->n_instances is
+ * ignored.  metrics is [n_traces][max instances over deployments]. */
+int hs_replay_deployments(hs_ctx* ctx, const hs_instance* instances, const int32_t* inst_offsets,
+                          int32_t n_deployments, const hs_policy* policy, const int32_t* trace_deployment,
+                          const hs_trace_batch* batch, uint8_t* assign, double* depart, hs_inst_metrics* metrics,
+                          hs_trace_result* result);
 
 /* Device-resident variant for throughput measurement: every pointer in
  * batch / assign / depart / metrics / result is a DEVICE pointer (allocated

@@ -49,9 +49,11 @@ from .planner import (
     ThroughputEstimate,
     best_config,
     build_tables,
+    merge_topk,
     estimate_system_throughput,
     search_best,
     search_optimal_config,
+    search_topk,
 )
 from .scheduling import POLICIES, InstanceHandle, OutputLengthPredictor, PolicyConfig, PredictorConfig
 from .simulator import (
@@ -61,6 +63,7 @@ from .simulator import (
     SimMetrics,
     build_instances,
     generate_arrivals,
+    replay_deployments,
     replay_traces,
     run_continuous,
     run_policy_comparison,

@@ -15,7 +15,7 @@ import numpy as np
 
 HS_MAX_DEGREES = 32
 HS_MAX_MACHINES = 64
-HS_MAX_INSTANCES = 32
+HS_MAX_INSTANCES = 128
 
 # enums (hetserve_b200.h)
 HS_OK, HS_ERR_ARG, HS_ERR_CUDA, HS_ERR_UNSUPPORTED, HS_ERR_NOMEM = 0, 1, 2, 3, 4
@@ -107,6 +107,7 @@ RESULT_DTYPE = np.dtype([("error", "<i4"), ("err_instance", "<i4"), ("err_reques
 EXPORTS = (
     "hs_abi_version", "hs_ctx_create", "hs_ctx_destroy", "hs_last_error", "hs_ctx_launch_count",
     "hs_ctx_last_kernel_ms", "hs_search_tables", "hs_search_best", "hs_search_rank", "hs_search_topk", "hs_replay",
+    "hs_replay_deployments",
     "hs_replay_device", "hs_device_alloc", "hs_device_free", "hs_memcpy_h2d", "hs_memcpy_d2h",
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
 )
@@ -139,6 +140,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_search_topk": ([vp, vp, vp, i32, i64, i32, i32, vp, vp, vp], C.c_int),
             "hs_replay": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
             "hs_replay_device": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+            "hs_replay_deployments": ([vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp], C.c_int),
             "hs_device_alloc": ([vp, i64, C.POINTER(vp)], C.c_int),
             "hs_device_free": ([vp, vp], C.c_int),
             "hs_memcpy_h2d": ([vp, vp, vp, i64], C.c_int),
@@ -150,7 +152,10 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_probe_fp64": ([vp, C.POINTER(dbl)], C.c_int),
         }
         for name, (args, res) in sig.items():
-            fn = getattr(lib, name)
+            try:
+                fn = getattr(lib, name)
+            except AttributeError:  # an older diagnostic build (HS_LIB); the tests check the real one
+                continue
             fn.argtypes = args
             fn.restype = res
         if path is None:
@@ -240,6 +245,28 @@ class Engine:
         self._pinned = getattr(self, "_pinned", [])
         self._pinned.append(p.value)
         return np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+    def replay_deployments(self, instances, inst_offsets: np.ndarray, policy: hs_policy, trace_dep: np.ndarray,
+                           offsets: np.ndarray, I: np.ndarray, O: np.ndarray, P: np.ndarray,
+                           arrival: np.ndarray | None, want_assign: bool = True, want_depart: bool = False):
+        T = len(offsets) - 1
+        nd = len(inst_offsets) - 1
+        n_max = int(np.max(np.diff(inst_offsets))) if nd else 0
+        total = int(offsets[-1])
+        batch = hs_trace_batch(T, offsets.ctypes.data, I.ctypes.data, O.ctypes.data, P.ctypes.data,
+                               None if arrival is None else arrival.ctypes.data)
+        assign = np.zeros(max(total, 1), np.uint8) if want_assign else None
+        depart = np.zeros(max(total, 1), np.float64) if want_depart else None
+        metrics = np.zeros(max(T * n_max, 1), METRICS_DTYPE)
+        result = np.zeros(max(T, 1), RESULT_DTYPE)
+        io = np.ascontiguousarray(inst_offsets, np.int32)
+        td = np.ascontiguousarray(trace_dep, np.int32)
+        rc = self.lib.hs_replay_deployments(self.handle, C.cast(instances, C.c_void_p), _ptr(io), nd, C.byref(policy),
+                                            _ptr(td), C.byref(batch), _ptr(assign), _ptr(depart), _ptr(metrics),
+                                            _ptr(result))
+        self.check(rc, "hs_replay_deployments")
+        return (None if assign is None else assign[:total], None if depart is None else depart[:total],
+                metrics[: T * n_max].reshape(T, n_max), result[:T])
 
     def replay_device(self, instances, policy, n_traces: int, d_off: int, d_I: int, d_O: int, d_P: int,
                       d_T: int | None, d_assign: int | None, d_metrics: int, d_result: int) -> None:

@@ -34,7 +34,7 @@ enum Slot {
   S_I, S_O, S_P, S_T, S_OFF, S_DESC, S_TABLE, S_BLK_BEST, S_BLK_IDX, S_BLK_CNT, S_CAND, S_CNT,
   S_TOTAL, S_FIRSTBAD, S_FLAG, S_SELIDX, S_NSEL, S_KEYS, S_KEYS2, S_IDX2, S_CUBTMP, S_RANKED,
   S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_QNEXT, S_HEAP, S_MINNEED, S_TK_HIST, S_TK_CNT, S_TK_KEY,
-  S_TK_IDX, S_TK_KEY2, S_TK_IDX2, N_SLOTS
+  S_TK_IDX, S_TK_KEY2, S_TK_IDX2, S_DEPS, S_TDEP, S_THEAP, N_SLOTS
 };
 
 }  // namespace
@@ -210,8 +210,7 @@ __global__ void k_gather_ranked(const double* total, const int64_t* idx, const i
 int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, hs::ReplayConst* out) {
   const int N = pol->n_instances;
   if (N < 1) return fail(HS_ERR_ARG, "n_instances must be >= 1");
-  if (N > HS_MAX_INSTANCES)
-    return fail(HS_ERR_UNSUPPORTED, "more than 32 instances per deployment is not supported yet");
+  if (N > HS_MAX_INSTANCES) return fail(HS_ERR_UNSUPPORTED, "more than 128 instances per deployment");
   if (pol->policy < HS_POLICY_OS || pol->policy > HS_POLICY_MB) return fail(HS_ERR_ARG, "unknown policy");
   if (pol->per_token <= 0) return fail(HS_ERR_ARG, "per_token must be positive");
   if (pol->mode != 0 && pol->mode != 1) return fail(HS_ERR_ARG, "mode must be 0 (continuous) or 1 (static)");
@@ -229,8 +228,9 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
   for (int j = 0; j < N; ++j) {
     const int ty = inst[j].type;
     if (ty < 0 || ty >= N) return fail(HS_ERR_ARG, "instance type out of range");
+    if (ty >= hs::kMaxTypes) return fail(HS_ERR_UNSUPPORTED, "more than 32 distinct instance classes");
     if (!(inst[j].budget > 0)) return fail(HS_ERR_ARG, "instance budget must be positive");
-    rc.inst_type[j] = ty;
+    rc.inst_type[j] = (int8_t)ty;
     if (ty >= nt) nt = ty + 1;
     std::memcpy(rc.type_p[ty], inst[j].p, sizeof(double) * 8);
     rc.type_budget[ty] = inst[j].budget;
@@ -798,6 +798,95 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
   if ((rc = end_timing(c))) return rc;
   if (T > 0) {
     HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * N, cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
+  if (depart && total > 0)
+    HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+
+int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t* inst_offsets, int32_t n_dep,
+                          const hs_policy* pol, const int32_t* trace_dep, const hs_trace_batch* b, uint8_t* assign,
+                          double* depart, hs_inst_metrics* metrics, hs_trace_result* result) {
+  if (!c || !instances || !inst_offsets || !pol || !trace_dep || !b || !metrics || !result || !b->offsets)
+    return fail(HS_ERR_ARG, "null argument");
+  if (n_dep < 1) return fail(HS_ERR_ARG, "n_deployments must be >= 1");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  const int64_t T = b->n_traces;
+  const int64_t* off = b->offsets;
+  if (T < 0 || off[0] != 0) return fail(HS_ERR_ARG, "bad offsets");
+  const int64_t total = off[T];
+  int64_t max_q;
+  if ((rc = check_offsets(off, T, &max_q))) return rc;
+  std::vector<hs::ReplayConst> deps((size_t)n_dep);
+  int n_max = 0, max_types = 0;
+  for (int32_t d = 0; d < n_dep; ++d) {
+    hs_policy pd = *pol;
+    pd.n_instances = inst_offsets[d + 1] - inst_offsets[d];
+    if ((rc = make_const(instances + inst_offsets[d], &pd, b->arrival != nullptr, &deps[d]))) return rc;
+    if (pd.n_instances > n_max) n_max = pd.n_instances;
+    if (deps[d].n_types > max_types) max_types = deps[d].n_types;
+  }
+  for (int64_t t = 0; t < T; ++t)
+    if (trace_dep[t] < 0 || trace_dep[t] >= n_dep) return fail(HS_ERR_ARG, "trace_deployment out of range");
+  int64_t* dOff;
+  int32_t *dI, *dO, *dP, *dTD, *dMin;
+  double* dT = nullptr;
+  uint8_t* dA = nullptr;
+  double* dDep = nullptr;
+  hs_inst_metrics* dM;
+  hs_trace_result* dR;
+  void *dQ, *dDeps;
+  int64_t* dTH;
+  const size_t tq = (size_t)(total > 0 ? total : 1);
+  if ((rc = ensure_t(c, S_OFF, (size_t)T + 1, &dOff)) || (rc = ensure_t(c, S_I, tq, &dI)) ||
+      (rc = ensure_t(c, S_O, tq, &dO)) || (rc = ensure_t(c, S_P, tq, &dP)) ||
+      (rc = ensure_t(c, S_METRICS, (size_t)(T > 0 ? T : 1) * n_max, &dM)) ||
+      (rc = ensure_t(c, S_RESULT, (size_t)(T > 0 ? T : 1), &dR)) || (rc = ensure(c, S_WREC, tq * hs::kQRecBytes, &dQ)) ||
+      (rc = ensure(c, S_DEPS, sizeof(hs::ReplayConst) * n_dep, &dDeps)) ||
+      (rc = ensure_t(c, S_TDEP, (size_t)(T > 0 ? T : 1), &dTD)) ||
+      (rc = ensure_t(c, S_THEAP, (size_t)(T > 0 ? T : 1), &dTH)) || (rc = ensure_t(c, S_MINNEED, 1, &dMin)))
+    return rc;
+  if (b->arrival && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
+  if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
+  if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
+  HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
+  if (total > 0) {
+    HS_CUDA(cudaMemcpyAsync(dI, b->input_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
+    HS_CUDA(cudaMemcpyAsync(dO, b->output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
+    HS_CUDA(cudaMemcpyAsync(dP, b->pred_output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
+    if (dT) HS_CUDA(cudaMemcpyAsync(dT, b->arrival, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
+  }
+  HS_CUDA(cudaMemsetAsync(dMin, 0x7f, sizeof(int32_t), c->stream));
+  if (total > 0) {
+    HS_CUDA(hs::launch_min_need(dI, dO, total, dMin, c->stream));
+    c->launches += 1;
+  }
+  int32_t min_need = 0;
+  HS_CUDA(cudaMemcpyAsync(&min_need, dMin, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q);
+  std::vector<int64_t> theap((size_t)(T > 0 ? T : 1));
+  int64_t hacc = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    theap[t] = hacc;
+    hacc += deps[trace_dep[t]].heap_stride;
+  }
+  uint64_t* dHeap;
+  if ((rc = ensure_t(c, S_HEAP, (size_t)(hacc > 0 ? hacc : 1) * 2, &dHeap))) return rc;
+  HS_CUDA(cudaMemcpyAsync(dDeps, deps.data(), sizeof(hs::ReplayConst) * n_dep, cudaMemcpyHostToDevice, c->stream));
+  HS_CUDA(cudaMemcpyAsync(dTD, trace_dep, sizeof(int32_t) * T, cudaMemcpyHostToDevice, c->stream));
+  HS_CUDA(cudaMemcpyAsync(dTH, theap.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = begin_timing(c))) return rc;
+  HS_CUDA(hs::launch_replay(deps[0], T, dOff, dI, dO, dP, dT, dA, dDep, dM, dR, dQ, dHeap, c->stream,
+                            static_cast<const hs::ReplayConst*>(dDeps), dTD, dTH, n_max, max_types));
+  c->launches += 1;
+  if ((rc = end_timing(c))) return rc;
+  if (T > 0) {
+    HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * n_max, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
   }
   if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));

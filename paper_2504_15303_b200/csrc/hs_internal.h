@@ -47,6 +47,9 @@ struct FeasSpace {
   int32_t orig[kMaxM * HS_MAX_DEGREES];  // its original digit
 };
 
+constexpr int kMaxReplayInst = 128;  // up to 4 warps per trace
+constexpr int kMaxTypes = 32;         // distinct (params, budget) classes per deployment
+
 struct ReplayConst {
   int32_t N;
   int32_t policy;
@@ -57,13 +60,13 @@ struct ReplayConst {
   double theta;
   int64_t per_token;
   double wrr_total;
-  int64_t heap_stride;            // heap entries per trace
-  int64_t heap_off[HS_MAX_INSTANCES + 1];
-  int32_t inst_type[HS_MAX_INSTANCES];
-  double type_p[HS_MAX_INSTANCES][8];
-  double type_budget[HS_MAX_INSTANCES];
-  int64_t type_cap_tokens[HS_MAX_INSTANCES];  // floor(floor(budget) / per_token)
-  double wrr_weight[HS_MAX_INSTANCES];
+  int64_t heap_stride;                       // heap entries per trace
+  int64_t heap_off[kMaxReplayInst + 1];
+  int8_t inst_type[kMaxReplayInst];
+  double type_p[kMaxTypes][8];
+  double type_budget[kMaxTypes];
+  int64_t type_cap_tokens[kMaxTypes];        // floor(floor(budget) / per_token)
+  double wrr_weight[kMaxReplayInst];
 };
 
 // launchers (return cudaError_t as int)
@@ -81,10 +84,14 @@ cudaError_t launch_topk_pass(const FeasSpace& fs, bool upload, int mode, int64_t
                              cudaStream_t st);
 cudaError_t launch_invert_keys(uint64_t* d_key, int64_t n, cudaStream_t st);
 cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st);
+// deps / trace_dep / trace_heap: per-trace deployments (config 5); when
+// deps is null every trace uses rc and trace t's heap starts at t*stride.
 cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                           const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
                           double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result,
-                          void* d_qrec, uint64_t* d_heap, cudaStream_t st);
+                          void* d_qrec, uint64_t* d_heap, cudaStream_t st, const ReplayConst* d_deps = nullptr,
+                          const int32_t* d_trace_dep = nullptr, const int64_t* d_trace_heap = nullptr,
+                          int n_max = 0, int max_types = 0);
 constexpr int kQRecBytes = 24;  // replay.cu QRec
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
 constexpr int kHeapShared = 8;  // replay.cu kHS

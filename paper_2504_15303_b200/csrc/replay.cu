@@ -148,23 +148,43 @@ struct Cold {
   int32_t req_count, qtail, cnt_max, err, err_req, _pad;
 };
 
+// Cross-warp exchange for traces spanning W > 1 warps: one slot per warp of
+// the trace group, a named barrier per group (ids 1..4).
+struct Xch {
+  uint64_t a, b;
+  int32_t c, d;
+};
+__device__ __forceinline__ void group_bar(int g, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(nthreads) : "memory");
+}
+
+template <int W, bool MULTI>
 __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
              hs_trace_result* __restrict__ result, QRec* __restrict__ qrec_all, uint64_t* __restrict__ heap_all,
-             const __grid_constant__ ReplayConst c_rep) {
+             const ReplayConst* __restrict__ deps, const int32_t* __restrict__ trace_dep,
+             const int64_t* __restrict__ trace_heap, int n_max, const __grid_constant__ ReplayConst c_one) {
+  constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);  // trace groups per block
   __shared__ uint64_t s_tab[256];
   __shared__ Cold s_cold[kWarps * 32];
   __shared__ HEnt s_heap[kWarps * 32][kHS];
+  __shared__ Xch s_x[G][W];
+  __shared__ uint32_t s_steps[G];
   extern __shared__ double s_cost[];  // [kWarps][32 * n_types]
   for (int k = threadIdx.x; k < 256; k += blockDim.x) s_tab[k] = kExpTab[k];
+  if (threadIdx.x < G) s_steps[threadIdx.x] = 0;
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int64_t tr = (int64_t)blockIdx.x * kWarps + wib;
+  const int g = wib / W, wsub = wib - g * W;
+  const int64_t tr = (int64_t)blockIdx.x * G + g;
   if (tr >= n_traces) return;
+  // single deployment: the kernel parameter (constant bank); per-trace
+  // deployments: the trace's record in global memory
+  const ReplayConst& c_rep = MULTI ? deps[trace_dep[tr]] : c_one;
   const int N = c_rep.N;
   const int NT = c_rep.n_types;
   const int policy = c_rep.policy;
@@ -172,6 +192,19 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   const double theta = c_rep.theta;
   double* cost = s_cost + (size_t)wib * 32 * NT;
   Cold& cold = s_cold[threadIdx.x];
+  Xch* xg = s_x[g];
+  // combine helper: every warp of the group publishes one slot, all read all
+  auto xchg = [&](const Xch& mine, Xch* all) {
+    if (W > 1) {
+      if (lane == 0) xg[wsub] = mine;
+      group_bar(g, W * 32);
+#pragma unroll
+      for (int w = 0; w < W; ++w) all[w] = xg[w];
+      group_bar(g, W * 32);
+    } else {
+      all[0] = mine;
+    }
+  };
 
   const int64_t o = off[tr];
   const int64_t q = off[tr + 1] - o;
@@ -182,14 +215,15 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   QRec* R = qrec_all + o;
   double* DEP = depart ? depart + o : nullptr;
 
-  const bool valid = lane < N;
-  const int j = valid ? lane : 0;
+  const int jj = wsub * 32 + lane;  // instance index of this lane
+  const bool valid = jj < N;
+  const int j = valid ? jj : 0;
   const int ty = c_rep.inst_type[j];
   const double* tp = c_rep.type_p[ty];
   const double budget = c_rep.type_budget[ty];
   const double p7 = tp[6], p8 = tp[7];
-  const Heap heap{s_heap[threadIdx.x],
-                  reinterpret_cast<HEnt*>(heap_all) + tr * c_rep.heap_stride + c_rep.heap_off[j]};
+  const int64_t hbase = MULTI ? trace_heap[tr] : tr * c_rep.heap_stride;
+  const Heap heap{s_heap[threadIdx.x], reinterpret_cast<HEnt*>(heap_all) + hbase + c_rep.heap_off[j]};
   const int64_t cap_tok = c_rep.type_cap_tokens[ty];  // floor(floor(budget) / per_token)
   const int32_t cap = (int32_t)(c_rep.heap_off[j + 1] - c_rep.heap_off[j]) + kHS;
 
@@ -406,14 +440,28 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
 #endif
     }
     const unsigned eb = __ballot_sync(FULL, valid && lerr);
-    if (!eb) return false;
+    if (W == 1 && !eb) return false;
     // the earliest failing step event wins (heap order: time, then instance)
-    const uint64_t tk = (valid && lerr) ? okey(cold.err_t) : ~0ull;
-    const uint64_t mt = warp_min_u64(tk);
-    const int bl = __ffs(__ballot_sync(FULL, tk == mt)) - 1;
-    t_err = __shfl_sync(FULL, cold.err, bl);
-    t_err_req = __shfl_sync(FULL, cold.err_req, bl);
-    t_err_inst = bl;
+    Xch mine{~0ull, 0, -1, -1};
+    if (eb) {
+      const uint64_t tk = (valid && lerr) ? okey(cold.err_t) : ~0ull;
+      const uint64_t mt = warp_min_u64(tk);
+      const int bl = __ffs(__ballot_sync(FULL, tk == mt)) - 1;
+      mine.a = mt;
+      mine.b = (uint64_t)(wsub * 32 + bl);
+      mine.c = __shfl_sync(FULL, cold.err, bl);
+      mine.d = __shfl_sync(FULL, cold.err_req, bl);
+    }
+    Xch all[W];
+    xchg(mine, all);
+    int best = -1;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      if (all[w].c >= 0 && (best < 0 || all[w].a < all[best].a)) best = w;
+    if (best < 0) return false;
+    t_err = all[best].c;
+    t_err_req = all[best].d;
+    t_err_inst = (int32_t)all[best].b;
     t_err_val = 0.0;
     return true;
   };
@@ -476,15 +524,22 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
           chosen = (int)(rr_next % N);
           rr_next += 1;
         } else {  // smooth WRR: first strict maximum after adding the weights
-          if (valid) cold.wcur = __dadd_rn(cold.wcur, c_rep.wrr_weight[lane]);
+          if (valid) cold.wcur = __dadd_rn(cold.wcur, c_rep.wrr_weight[jj]);
           const uint64_t wk = valid ? okey(cold.wcur) : 0ull;
           const uint64_t mk = warp_max_u64(wk);
-          chosen = __ffs(__ballot_sync(FULL, valid && wk == mk)) - 1;
-          if (lane == chosen) cold.wcur = __dsub_rn(cold.wcur, c_rep.wrr_total);
+          const unsigned wb = __ballot_sync(FULL, valid && wk == mk);
+          Xch all[W];
+          xchg(Xch{wb ? mk : 0ull, (uint64_t)(wsub * 32 + __ffs(wb) - 1), wb ? 1 : 0, 0}, all);
+          int bw = -1;
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (all[w].c && (bw < 0 || all[w].a > all[bw].a)) bw = w;
+          chosen = (int)all[bw].b;
+          if (jj == chosen) cold.wcur = __dsub_rn(cold.wcur, c_rep.wrr_total);
         }
       }
       // ---- evaluate (scheduling.py:216-233) on the lanes that need it
-      const bool need = valid && (eval_all || lane == chosen);
+      const bool need = valid && (eval_all || jj == chosen);
       double w = INFINITY;
       bool cerr = false, eerr = false;
       if (need) {
@@ -506,20 +561,38 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       HS_T1(2, te0);
       HS_T0(tm0);
       const unsigned errb = __ballot_sync(FULL, need && (cerr || eerr));
-      if (errb) {  // the first instance in evaluation order raises
-        const int el = __ffs(errb) - 1;
-        const bool ce = __shfl_sync(FULL, cerr, el);
-        double cval = 0.0;
-        if (lane == el && ce) {  // recompute the non-positive total for the message
-          const double fl = py_floordiv(budget, i2d(pt * (Ia + Pa)));
-          int64_t b = (int64_t)fl;
-          if (b < 1) b = 1;
-          cval = __dadd_rn(prefill_time(tp, b, Ia), decode_time(tp, b, Ia, Pa));
+      bool any_err = errb != 0;
+      if (W > 1) {
+        Xch all[W];
+        xchg(Xch{0, 0, errb ? 1 : 0, 0}, all);
+        any_err = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) any_err |= all[w].c != 0;
+      }
+      if (any_err) {  // the first instance in evaluation order raises
+        Xch mine{0, 0, -1, 0};
+        if (errb) {
+          const int el = __ffs(errb) - 1;
+          const bool ce = __shfl_sync(FULL, cerr, el);
+          double cval = 0.0;
+          if (lane == el && ce) {  // recompute the non-positive total for the message
+            const double fl = py_floordiv(budget, i2d(pt * (Ia + Pa)));
+            int64_t b = (int64_t)fl;
+            if (b < 1) b = 1;
+            cval = __dadd_rn(prefill_time(tp, b, Ia), decode_time(tp, b, Ia, Pa));
+          }
+          mine = Xch{(uint64_t)__double_as_longlong(shfl_d(cval, el)), (uint64_t)(wsub * 32 + el), ce ? 1 : 0, 0};
         }
-        t_err = ce ? HS_TRACE_NONPOSITIVE_COST : HS_TRACE_EXP_OVERFLOW;
-        t_err_inst = el;
+        Xch all[W];
+        xchg(mine, all);
+        int bw = -1;
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if (all[w].c >= 0 && (bw < 0 || all[w].b < all[bw].b)) bw = w;
+        t_err = all[bw].c ? HS_TRACE_NONPOSITIVE_COST : HS_TRACE_EXP_OVERFLOW;
+        t_err_inst = (int32_t)all[bw].b;
         t_err_req = a;
-        t_err_val = shfl_d(cval, el);
+        t_err_val = __longlong_as_double((long long)all[bw].a);
         failed = true;
         break;
       }
@@ -527,13 +600,26 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
         // _min_max_choice (scheduling.py:299-312):
         // peak_s = max(L_s + w_s, max_{j != s} L_j), argmin with lowest index
         const uint64_t lk = valid ? okey(load) : 0ull;
-        const uint64_t m1 = warp_max_u64(lk);
+        uint64_t m1 = warp_max_u64(lk);
         const unsigned at_max = __ballot_sync(FULL, valid && lk == m1);
         uint64_t m2;
         if (__popc(at_max) >= 2) {
           m2 = m1;
         } else {
           m2 = warp_max_u64(lk == m1 ? 0ull : lk);
+        }
+        if (W > 1) {  // merge the per-warp top-2 multisets
+          Xch all[W];
+          xchg(Xch{m1, m2, 0, 0}, all);
+          m1 = all[0].a;
+          m2 = all[0].b;
+#pragma unroll
+          for (int w = 1; w < W; ++w) {
+            const uint64_t a1 = all[w].a, a2 = all[w].b;
+            const uint64_t lo1 = m1 < a1 ? m1 : a1, hi2 = m2 > a2 ? m2 : a2;
+            m1 = m1 > a1 ? m1 : a1;
+            m2 = lo1 > hi2 ? lo1 : hi2;
+          }
         }
         const uint64_t ok_ = (lk == m1) ? m2 : m1;
         const double others = ok_ == 0ull ? -INFINITY : from_okey(ok_);
@@ -543,19 +629,36 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
         const uint64_t pk = cand ? okey(peak) : ~0ull;
         const uint64_t mp = warp_min_u64(pk);
         const unsigned win = __ballot_sync(FULL, cand && pk == mp);
-        if (!win) {
-          t_err = HS_TRACE_NO_INSTANCE;
-          t_err_req = a;
-          t_err_inst = -1;
-          failed = true;
-          break;
+        if (W == 1) {
+          if (!win) {
+            t_err = HS_TRACE_NO_INSTANCE;
+            t_err_req = a;
+            t_err_inst = -1;
+            failed = true;
+            break;
+          }
+          chosen = __ffs(win) - 1;
+        } else {
+          Xch all[W];
+          xchg(Xch{win ? mp : ~0ull, (uint64_t)(wsub * 32 + __ffs(win) - 1), win ? 1 : 0, 0}, all);
+          int bw = -1;
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (all[w].c && (bw < 0 || all[w].a < all[bw].a)) bw = w;
+          if (bw < 0) {
+            t_err = HS_TRACE_NO_INSTANCE;
+            t_err_req = a;
+            t_err_inst = -1;
+            failed = true;
+            break;
+          }
+          chosen = (int)all[bw].b;
         }
-        chosen = __ffs(win) - 1;
       }
       HS_T1(3, tm0);
       HS_T0(tc0);
       // ---- commit (scheduling.py:335-346) and enqueue (simulator.py:323-327)
-      if (lane == chosen) {
+      if (jj == chosen) {
         load = __dadd_rn(load, w);
         run_i += Ia;
         run_p += Pa;
@@ -590,7 +693,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       if (lane == al) my_assign = (uint8_t)chosen;
       HS_T1(4, tc0);
     }
-    if (assign && lane < n_in && !failed) assign[o + base + lane] = my_assign;
+    if (assign && wsub == 0 && lane < n_in && !failed) assign[o + base + lane] = my_assign;
   }
   if (!failed && !is_static && advance(0.0, true)) failed = true;
   if (!failed && is_static) {
@@ -639,11 +742,21 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       cold.completion = clock;
     }
     const unsigned bb = __ballot_sync(FULL, bad);
-    if (bb) {  // the first instance (config order) whose plan fails raises
+    Xch mine{0, 0, -1, 0};
+    if (bb) {
       const int bl = __ffs(bb) - 1;
+      mine = Xch{0, (uint64_t)(wsub * 32 + bl), 1, __shfl_sync(FULL, bad_r, bl)};
+    }
+    Xch all[W];
+    xchg(mine, all);
+    int bw = -1;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      if (all[w].c > 0 && (bw < 0 || all[w].b < all[bw].b)) bw = w;
+    if (bw >= 0) {  // the first instance (config order) whose plan fails raises
       t_err = HS_TRACE_INFEASIBLE_REQUEST;
-      t_err_req = __shfl_sync(FULL, bad_r, bl);
-      t_err_inst = bl;
+      t_err_req = all[bw].d;
+      t_err_inst = (int32_t)all[bw].b;
       failed = true;
     }
   }
@@ -655,12 +768,17 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     m.residual_load = load;
     m.request_count = cold.req_count;
     m.token_count = cold.tok_count;
-    metrics[tr * N + lane] = m;
+    metrics[tr * (int64_t)n_max + jj] = m;
   }
   int64_t steps_all = n_steps;
 #pragma unroll
   for (int offs = 16; offs > 0; offs >>= 1) steps_all += __shfl_xor_sync(FULL, steps_all, offs);
-  if (lane == 0) {
+  if (W > 1) {
+    if (lane == 0) atomicAdd(&s_steps[g], (uint32_t)steps_all);
+    group_bar(g, W * 32);
+    steps_all = s_steps[g];
+  }
+  if (lane == 0 && wsub == 0) {
     hs_trace_result r;
     r.error = failed ? t_err : HS_TRACE_OK;
     r.err_instance = failed ? t_err_inst : -1;
@@ -671,21 +789,47 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   }
 }
 
+template <int W, bool MULTI>
+cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
+                     const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign, double* d_depart,
+                     hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec, uint64_t* d_heap,
+                     cudaStream_t st, const ReplayConst* d_deps, const int32_t* d_trace_dep,
+                     const int64_t* d_trace_heap, int n_max, int max_types) {
+  constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);
+  const int warps = W * G;
+  const size_t smem = (size_t)warps * 32 * max_types * sizeof(double);
+  if (smem > 16 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const unsigned blocks = (unsigned)((n_traces + G - 1) / G);
+  k_replay<W, MULTI><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
+                                                d_result, static_cast<QRec*>(d_qrec), d_heap, d_deps, d_trace_dep,
+                                                d_trace_heap, n_max, rc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                           const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
                           double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec,
-                          uint64_t* d_heap, cudaStream_t st) {
-  cudaError_t e = cudaSuccess;
+                          uint64_t* d_heap, cudaStream_t st, const ReplayConst* d_deps, const int32_t* d_trace_dep,
+                          const int64_t* d_trace_heap, int n_max, int max_types) {
   if (n_traces <= 0) return cudaSuccess;
-  const size_t smem = (size_t)kWarps * 32 * rc.n_types * sizeof(double);
-  if (smem > 16 * 1024) {
-    e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+  if (n_max <= 0) n_max = rc.N;
+  if (max_types <= 0) max_types = rc.n_types;
+  const int W = (n_max + 31) / 32;
+#define HS_LW(w, m)                                                                                              \
+  launch_w<w, m>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result, d_qrec, d_heap, \
+                 st, d_deps, d_trace_dep, d_trace_heap, n_max, max_types)
+  const bool multi = d_deps != nullptr;
+  switch (W) {
+    case 1: return multi ? HS_LW(1, true) : HS_LW(1, false);
+    case 2: return multi ? HS_LW(2, true) : HS_LW(2, false);
+    case 3: return multi ? HS_LW(3, true) : HS_LW(3, false);
+    case 4: return multi ? HS_LW(4, true) : HS_LW(4, false);
+    default: return cudaErrorInvalidValue;
   }
-  const unsigned blocks = (unsigned)((n_traces + kWarps - 1) / kWarps);
-  k_replay<<<blocks, kWarps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
-                                              d_result, static_cast<QRec*>(d_qrec), d_heap, rc);
-  return cudaGetLastError();
+#undef HS_LW
 }
 
 // min over all requests of (I + O): sizes the per-instance active-set heaps

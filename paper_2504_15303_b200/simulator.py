@@ -311,3 +311,36 @@ def replay_traces(cluster, config, params, policy: PolicyConfig, offsets, input_
                             None if arrival is None else np.ascontiguousarray(arrival, np.float64),
                             want_assign=want_assign, want_depart=want_depart)
     return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)
+
+
+def replay_deployments(cluster, configs, params, policy: PolicyConfig, trace_deployment, offsets, input_len,
+                       output_len, pred_output_len, arrival=None, want_assign=True, want_depart=False, engine=None,
+                       static=False) -> ReplayBatchResult:
+    """Replay trace t on deployment configs[trace_deployment[t]] (BASELINE
+    config 5: every top-k deployment re-scored by a full simulation), all
+    traces in one launch.  metrics is [T, max instances]."""
+    per_token = kv_bytes_per_token(cluster.model)
+    inst_all, offs = [], [0]
+    for cfg in configs:
+        handles = build_instances(cluster, cfg, params)
+        _check_scheduler(handles, policy)
+        if len(handles) > nat.HS_MAX_INSTANCES:
+            raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"{len(handles)} instances (max {nat.HS_MAX_INSTANCES})")
+        inst_all.append(engine_instances(handles, policy))
+        offs.append(offs[-1] + len(handles))
+    arr = (nat.hs_instance * max(offs[-1], 1))()
+    k = 0
+    for part, n in zip(inst_all, np.diff(offs)):
+        for j in range(n):
+            arr[k] = part[j]
+            k += 1
+    eng = engine or nat.engine_for()
+    pol = _policy_struct(policy, 0, per_token, 1 if static else 0)
+    a, d, m, r = eng.replay_deployments(arr, np.array(offs, np.int32), pol, np.asarray(trace_deployment, np.int32),
+                                        np.ascontiguousarray(offsets, np.int64),
+                                        np.ascontiguousarray(input_len, np.int32),
+                                        np.ascontiguousarray(output_len, np.int32),
+                                        np.ascontiguousarray(pred_output_len, np.int32),
+                                        None if arrival is None else np.ascontiguousarray(arrival, np.float64),
+                                        want_assign=want_assign, want_depart=want_depart)
+    return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)

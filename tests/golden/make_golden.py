@@ -386,6 +386,25 @@ def build_static_cases() -> list:
     return cases
 
 
+def build_wide_cases() -> list:
+    """Deployments with more than 32 instances (config-5 shapes): the
+    config-3 cluster at 70B with several per-machine degrees."""
+    cases = []
+    p3 = wl.config3()
+    # 72 instances: b200/h200 at t=2 (8 each x 4 machines), the rest t=4 / t=8
+    deg72 = {}
+    for name, count, _mem, acc in p3.machines:
+        deg72[name] = 2 if acc in ("b200", "h200") else (8 if acc in ("v100", "a10") else 4)
+    I, O = wl.trace_lengths(1500, seed=11)
+    cases.append(replay_case("wide72", p3, deg72, {"seed": 11}, I, O, 400.0, 3, ["OS", "RR", "MB"]))
+    deg40 = {n: (4 if acc in ("b200", "h200") else (16 if acc in ("v100", "a10", "l40s") else 8))
+             for n, c, m, acc in p3.machines}
+    I, O = wl.trace_lengths(1500, seed=12)
+    cases.append(replay_case("wide40_inf", p3, deg40, {"seed": 12}, I, O, math.inf, 0, ["OS", "SI"]))
+    cases.append(replay_case("wide40_static", p3, deg40, {"seed": 12}, I, O, math.inf, 0, ["OS"], mode="static"))
+    return cases
+
+
 def build_exp_vectors() -> dict:
     rng = np.random.default_rng(5)
     xs = np.concatenate([rng.uniform(0, 1, 3000), rng.uniform(0, 20, 3000), rng.uniform(0, 709.7, 3000),
@@ -396,7 +415,7 @@ def build_exp_vectors() -> dict:
 
 
 def main() -> None:
-    which = sys.argv[1:] or ["exp", "search", "replay", "static"]
+    which = sys.argv[1:] or ["exp", "search", "replay", "static", "wide"]
     if "exp" in which:
         (OUT / "exp_vectors.json").write_text(json.dumps(build_exp_vectors()))
     if "search" in which:
@@ -405,6 +424,8 @@ def main() -> None:
         (OUT / "replay_cases.json").write_text(json.dumps(build_replay_cases()))
     if "static" in which:
         (OUT / "static_cases.json").write_text(json.dumps(build_static_cases()))
+    if "wide" in which:
+        (OUT / "wide_cases.json").write_text(json.dumps(build_wide_cases()))
 
 
 if __name__ == "__main__":

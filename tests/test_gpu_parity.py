@@ -19,7 +19,7 @@ from paper_2504_15303_b200 import workloads as wl
 pytestmark = pytest.mark.gpu
 
 SEARCH = H.load("search_cases.json")
-REPLAY = H.load("replay_cases.json") + H.load("static_cases.json")
+REPLAY = H.load("replay_cases.json") + H.load("static_cases.json") + H.load("wide_cases.json")
 
 
 @pytest.fixture(scope="module")
@@ -244,3 +244,49 @@ def test_topk_is_head_of_reference_ranking(eng, case):
     top, nf, _ = planner.search_topk(t, k + 5, engine=eng)
     assert nf == k
     assert [float(x).hex() for x in top["total"]] == [r["total"] for r in case["ranked"]]
+
+
+def test_replay_deployments_mixed_widths_vs_oracle(eng):
+    """Config-5 shape: each trace on its own deployment (9 to 100 instances,
+    1 to 4 warps per trace) in one launch, vs the oracle trace by trace."""
+    p3 = wl.config3()
+    cluster = hs.ClusterSpec(hs.ModelSpec(**p3.model), hs.EngineOverheads(**p3.engine),
+                             tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in p3.machines),
+                             hs.WorkloadLimits(**p3.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in p3.params.items()}
+    rng = np.random.default_rng(17)
+    feas = {"b200": [2, 4, 8, 16], "h200": [2, 4, 8, 16], "h100": [4, 8, 16], "a100": [4, 8, 16],
+            "a800": [4, 8, 16], "l40s": [4, 8, 16], "v100": [8, 16], "a10": [8, 16]}
+    configs = []
+    for _ in range(6):
+        deg = {n: int(rng.choice(feas[acc])) for n, c, m, acc in p3.machines}
+        configs.append(hs.deployment_for(cluster.machines, deg))
+    configs.append(hs.deployment_for(cluster.machines, {n: feas[acc][0] for n, c, m, acc in p3.machines}))
+    configs.append(hs.deployment_for(cluster.machines, {n: 16 for n, c, m, acc in p3.machines}))
+    sizes = [len(hs.build_instances(cluster, c, params)) for c in configs]
+    assert max(sizes) > 64 and min(sizes) <= 32
+    T = 28
+    tdep = np.arange(T) % len(configs)
+    lens = [int(x) for x in rng.integers(200, 1500, T)]
+    Is, Os, Ts = [], [], []
+    for t, q in enumerate(lens):
+        I, O = wl.trace_lengths(q, seed=900 + t)
+        Is.append(I); Os.append(O); Ts.append(wl.arrivals(q, [200.0, 2000.0][t % 2], seed=t))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    I, O, Tm = np.concatenate(Is), np.concatenate(Os), np.concatenate(Ts)
+    pol = hs.PolicyConfig(policy="OS")
+    res = hs.replay_deployments(cluster, configs, params, pol, tdep, off, I, O, O, arrival=Tm, want_depart=True,
+                                engine=eng)
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    per_token = hs.kv_bytes_per_token(cluster.model)
+    for t in range(T):
+        handles = build_instances(cluster, configs[tdep[t]], params)
+        n = len(handles)
+        sl = slice(off[t], off[t + 1])
+        a, d, m, r = orc.replay(engine_instances(handles, pol), _policy_struct(pol, n, per_token),
+                                np.array([0, lens[t]], np.int64), I[sl], O[sl], O[sl], Tm[sl])
+        assert int(res.result[t]["error"]) == 0 == int(r[0]["error"])
+        assert np.array_equal(res.assign[sl], a), t
+        assert np.array_equal(res.depart[sl].view(np.uint64), d.view(np.uint64)), t
+        for f in ("completion_time", "residual_load", "peak_kv_usage"):
+            assert np.array_equal(res.metrics[t, :n][f].view(np.uint64), m[0][f].view(np.uint64)), (t, f)

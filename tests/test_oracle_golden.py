@@ -114,7 +114,7 @@ def test_oracle_literal_candidates_match_reference_samples():
     assert n_ok >= 20
 
 
-REPLAY = H.load("replay_cases.json") + H.load("static_cases.json")
+REPLAY = H.load("replay_cases.json") + H.load("static_cases.json") + H.load("wide_cases.json")
 REPLAY_PARAMS = [(c, k) for c in REPLAY for k in range(len(c["results"]))]
 
 
