@@ -54,6 +54,10 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", choices=["config34", "config5"], default="config34",
+                    help="config34 (default line): config-3 search + config-4 replay; config5: top-k search "
+                         "+ every top-k deployment replayed on its own copy of one trace")
+    ap.add_argument("--topk", type=int, default=1024)
     return ap.parse_args()
 
 
@@ -422,6 +426,93 @@ def engine_arm(args, rank, world, local_rank):
         tdist.barrier(device_ids=[local_rank])
 
 
+def config5_arm(args, rank, world, local_rank):
+    """BASELINE config 5: top-k deployments of the config-3 space, each
+    re-scored by a full continuous-batching simulation of one trace
+    (rate = inf, OS).  Units = feasible candidates ranked + requests."""
+    import torch
+    import paper_2504_15303_b200 as hs
+    from paper_2504_15303_b200 import _native as nat
+    from paper_2504_15303_b200 import planner
+    from paper_2504_15303_b200.distributed import shard_range
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    eng = nat.engine_for(local_rank)
+    ext = torch.cuda.ExternalStream(eng.stream, device=dev)
+    cluster, reqs, params, sI, sO = search_inputs(args.search_q)
+    from paper_2504_15303_b200 import workloads as wl
+    I1, O1 = wl.trace_lengths(args.q, seed=0)
+
+    def step():
+        t = planner.build_tables(cluster, reqs, params, engine=eng)
+        cands, nf, ms_topk = planner.search_topk(t, args.topk, rank, world, engine=eng)
+        if dist:  # one all-gather of the per-rank top-k lists
+            buf = torch.zeros(args.topk, 2, dtype=torch.int64, device=dev)
+            loc = np.zeros((args.topk, 2), np.int64)
+            loc[:, 1] = -1
+            loc[:len(cands), 0] = cands["total"].view(np.int64)
+            loc[:len(cands), 1] = cands["index"]
+            buf.copy_(torch.from_numpy(loc))
+            outs = [torch.zeros_like(buf) for _ in range(world)]
+            with torch.cuda.stream(ext):
+                tdist.all_gather(outs, buf)
+            parts = []
+            for o in outs:
+                h = o.cpu().numpy()
+                h = h[h[:, 1] >= 0]
+                p = np.zeros(len(h), nat.CAND_DTYPE)
+                p["total"] = h[:, 0].view(np.float64)
+                p["index"] = h[:, 1]
+                parts.append(p)
+            top = planner.merge_topk(parts, args.topk)
+            nf_all = torch.tensor([nf], dtype=torch.int64, device=dev)
+            tdist.all_reduce(nf_all)
+            nf = int(nf_all.item())
+        else:
+            top = cands
+        lo, hi = shard_range(len(top), rank, world)
+        configs = [planner.deployment_of(t, int(i)) for i in top["index"][lo:hi]]
+        n = hi - lo
+        off = np.arange(n + 1, dtype=np.int64) * args.q
+        I = np.tile(I1, n)
+        O = np.tile(O1, n)
+        res = hs.replay_deployments(cluster, configs, params, hs.PolicyConfig(), np.arange(n), off, I, O, O,
+                                    engine=eng, want_assign=False)
+        assert (res.result["error"] == 0).all()
+        return nf, ms_topk, res.kernel_ms, n
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        tdist.barrier(device_ids=[local_rank])
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for _ in range(args.steps):
+        nf, ms_topk, ms_rep, n = step()
+    e1.record(ext)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        ms = float(tt.item())
+    units = nf + args.topk * args.q
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": units / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
+            "config": {"workload": f"config5: top-{args.topk} of the config-3 space (70B), each deployment "
+                                   f"replayed on {args.q} requests (rate=inf, OS)",
+                       "feasible_candidates_ranked": nf, "requests": args.topk * args.q},
+            "breakdown": {"topk_ms": ms_topk, "replay_ms_rank0": ms_rep, "deployments_rank0": n}}), flush=True)
+
+
 def main():
     args = parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -435,7 +526,10 @@ def main():
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    engine_arm(args, rank, world, local_rank)
+    if args.workload == "config5":
+        config5_arm(args, rank, world, local_rank)
+    else:
+        engine_arm(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as tdist
         tdist.destroy_process_group()

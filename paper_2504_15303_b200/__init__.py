@@ -49,6 +49,7 @@ from .planner import (
     ThroughputEstimate,
     best_config,
     build_tables,
+    deployment_of,
     merge_topk,
     estimate_system_throughput,
     search_best,

@@ -349,3 +349,8 @@ def best_config(tables: SearchTables, index: int) -> ThroughputEstimate:
         total += est.machine_tokens_per_sec
     return ThroughputEstimate(config=_config_for(tables, digits), per_machine=tuple(per_machine),
                               system_tokens_per_sec=total)
+
+
+def deployment_of(tables: SearchTables, index: int) -> DeploymentConfig:
+    """The DeploymentConfig of candidate `index` (itertools.product order)."""
+    return _config_for(tables, tables.digits(index))

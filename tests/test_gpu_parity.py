@@ -290,3 +290,31 @@ def test_replay_deployments_mixed_widths_vs_oracle(eng):
         assert np.array_equal(res.depart[sl].view(np.uint64), d.view(np.uint64)), t
         for f in ("completion_time", "residual_load", "peak_kv_usage"):
             assert np.array_equal(res.metrics[t, :n][f].view(np.uint64), m[0][f].view(np.uint64)), (t, f)
+
+
+def test_config5_shape_topk_then_rescore(eng):
+    """Top-12 deployments of the config-3 space, each replayed (rate=inf, OS)
+    on the same 3000-request trace in one launch, vs the oracle."""
+    _case, _req, t = _config3_tables(eng)
+    top, _nf, _ = planner.search_topk(t, 12, engine=eng)
+    configs = [planner.deployment_of(t, int(i)) for i in top["index"]]
+    p3 = wl.config3()
+    cluster = t.cluster
+    params = {k: hs.LatencyParams(*v) for k, v in p3.params.items()}
+    I1, O1 = wl.trace_lengths(3000, seed=0)
+    n = len(configs)
+    off = np.arange(n + 1, dtype=np.int64) * 3000
+    I, O = np.tile(I1, n), np.tile(O1, n)
+    res = hs.replay_deployments(cluster, configs, params, hs.PolicyConfig(), np.arange(n), off, I, O, O,
+                                want_depart=True, engine=eng)
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    per_token = hs.kv_bytes_per_token(cluster.model)
+    for d in range(n):
+        handles = build_instances(cluster, configs[d], params)
+        sl = slice(off[d], off[d + 1])
+        a, dep, m, r = orc.replay(engine_instances(handles, hs.PolicyConfig()),
+                                  _policy_struct(hs.PolicyConfig(), len(handles), per_token),
+                                  np.array([0, 3000], np.int64), I1, O1, O1, None)
+        assert int(res.result[d]["error"]) == 0 == int(r[0]["error"])
+        assert np.array_equal(res.assign[sl], a)
+        assert np.array_equal(res.depart[sl].view(np.uint64), dep.view(np.uint64))
