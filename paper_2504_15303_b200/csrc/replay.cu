@@ -408,7 +408,20 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       if (!__any_sync(FULL, want)) break;
       // phase 1: lanes whose next step is an event (retirement due, or an
       // admission may succeed)
+#ifdef HS_TIMERS
+      __syncwarp();
+      HS_T0(tev);
+      {
+        const bool anyev = __any_sync(FULL, want && !(blocked && k < kr));
+        if (lane == 0 && anyev) atomicAdd(&g_timers[7], 1ull);
+      }
+#endif
       if (want && !(blocked && k < kr)) event_step();
+#ifdef HS_TIMERS
+      __syncwarp();
+      HS_T1(5, tev);
+      HS_T0(tpu);
+#endif
       // phase 2: every lane whose next steps are pure runs them together,
       // up to its next event or the arrival time.  Two steps per iteration:
       // their prices depend only on the cached length, so both are computed
@@ -418,25 +431,40 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       if (pure) {
         const uint32_t k0 = k;
         for (;;) {
-          const double cd1 = __dadd_rn(cd, 1.0);
+          // four prices side by side (they depend only on the cached length),
+          // then the serial clock additions; the exit predicates are
+          // evaluated after the chain and the state is taken at the first
+          // step that may not run (extra additions are discarded).
+          const double cd1 = __dadd_rn(cd, 1.0), cd2 = __dadd_rn(cd, 2.0), cd3 = __dadd_rn(cd, 3.0);
           const double c0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd), B), __dmul_rn(p7, cd)), p8);
           const double c1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd1), B), __dmul_rn(p7, cd1)), p8);
+          const double c2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd2), B), __dmul_rn(p7, cd2)), p8);
+          const double c3 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd3), B), __dmul_rn(p7, cd3)), p8);
           const double t1 = __dadd_rn(t_next, c0);
-          if (!(k + 1 < kr && (t1 < lim || drain))) {
-            t_next = t1;
-            cd = cd1;
-            k += 1;
+          const double t2 = __dadd_rn(t1, c1);
+          const double t3 = __dadd_rn(t2, c2);
+          const double t4 = __dadd_rn(t3, c3);
+          // step i+1 runs iff step i ran, k+i < kr and t_i < lim
+          const bool g1 = k + 1 < kr && (t1 < lim || drain);
+          const bool g2 = g1 && k + 2 < kr && (t2 < lim || drain);
+          const bool g3 = g2 && k + 3 < kr && (t3 < lim || drain);
+          if (!g3) {
+            const uint32_t n = 1u + (uint32_t)g1 + (uint32_t)g2;
+            t_next = g2 ? t3 : (g1 ? t2 : t1);
+            cd = g2 ? cd3 : (g1 ? cd2 : cd1);
+            k += n;
             break;
           }
-          t_next = __dadd_rn(t1, c1);
-          cd = __dadd_rn(cd1, 1.0);
-          k += 2;
+          t_next = t4;
+          cd = __dadd_rn(cd, 4.0);
+          k += 4;
           if (!(k < kr && (t_next < lim || drain))) break;
         }
         n_steps += k - k0;
       }
 #ifdef HS_TIMERS
-      if (lane == 0) atomicAdd(&g_timers[7], 1ull);
+      __syncwarp();
+      HS_T1(6, tpu);
 #endif
     }
     const unsigned eb = __ballot_sync(FULL, valid && lerr);
