@@ -72,41 +72,80 @@ struct HEnt {
 struct Heap {
   HEnt* s;  // shared part, kHS entries
   HEnt* g;  // global part (entry i >= kHS at g[i - kHS])
-  __device__ __forceinline__ HEnt get(int32_t i) const { return i < kHS ? s[i] : g[i - kHS]; }
-  __device__ __forceinline__ void set(int32_t i, HEnt v) const {
+  // Generic accessors (heap larger than kHS).  Kept out of line so nvcc
+  // cannot if-convert them into loads of both the shared and the global
+  // address, which would put a global round trip on every heap operation.
+  __device__ __noinline__ HEnt get_any(int32_t i) const {
+    if (i < kHS) return s[i];
+    return g[i - kHS];
+  }
+  __device__ __noinline__ void set_any(int32_t i, HEnt v) const {
     if (i < kHS) s[i] = v;
     else g[i - kHS] = v;
   }
+  __device__ __forceinline__ HEnt get(int32_t i, int32_t n) const { return n <= kHS ? s[i] : get_any(i); }
   __device__ __forceinline__ void push(int32_t& n, HEnt e) const {
     int32_t i = n++;
+    if (n <= kHS) {  // shared memory only
+      while (i > 0) {
+        const int32_t p = (i - 1) >> 1;
+        const HEnt hp = s[p];
+        if (hp.key <= e.key) break;
+        s[i] = hp;
+        i = p;
+      }
+      s[i] = e;
+      return;
+    }
     while (i > 0) {
       const int32_t p = (i - 1) >> 1;
-      const HEnt hp = get(p);
+      const HEnt hp = get_any(p);
       if (hp.key <= e.key) break;
-      set(i, hp);
+      set_any(i, hp);
       i = p;
     }
-    set(i, e);
+    set_any(i, e);
   }
   __device__ __forceinline__ void pop(int32_t& n) const {
-    const HEnt last = get(--n);
+    if (n <= kHS) {  // shared memory only
+      const HEnt last = s[--n];
+      int32_t i = 0;
+      for (;;) {
+        int32_t l = 2 * i + 1;
+        if (l >= n) break;
+        HEnt hl = s[l];
+        if (l + 1 < n) {
+          const HEnt hr = s[l + 1];
+          if (hr.key < hl.key) {
+            hl = hr;
+            ++l;
+          }
+        }
+        if (last.key <= hl.key) break;
+        s[i] = hl;
+        i = l;
+      }
+      if (n > 0) s[i] = last;
+      return;
+    }
+    const HEnt last = get_any(--n);
     int32_t i = 0;
     for (;;) {
       int32_t l = 2 * i + 1;
       if (l >= n) break;
-      HEnt hl = get(l);
+      HEnt hl = get_any(l);
       if (l + 1 < n) {
-        const HEnt hr = get(l + 1);
+        const HEnt hr = get_any(l + 1);
         if (hr.key < hl.key) {
           hl = hr;
           ++l;
         }
       }
       if (last.key <= hl.key) break;
-      set(i, hl);
+      set_any(i, hl);
       i = l;
     }
-    if (n > 0) set(i, last);
+    if (n > 0) set_any(i, last);
   }
 };
 
@@ -276,7 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       const double wr = topW;
       heap.pop(nact);
       if (nact > 0) {
-        topkey = heap.get(0).key;
+        topkey = heap.s[0].key;  // the root always lives in shared memory
         const int32_t r2 = (int32_t)(topkey & 0xffffffffu);
         topI = I[r2];
         topO = O[r2];
@@ -373,7 +412,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       int64_t m = INT64_MIN;
       int32_t cm = 0;
       for (int32_t h = 0; h < nact; ++h) {
-        const int64_t mk = heap.get(h).mk;
+        const int64_t mk = heap.get(h, nact).mk;
         if (mk > m) {
           m = mk;
           cm = 1;
@@ -416,7 +455,16 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
         if (lane == 0 && anyev) atomicAdd(&g_timers[7], 1ull);
       }
 #endif
+#ifdef HS_TIMERS
+      if (want && !(blocked && k < kr)) {
+        const long long te0 = clock64();
+        event_step();
+        atomicAdd(&g_timers[4], (unsigned long long)(clock64() - te0));
+        atomicAdd(&g_timers[3], 1ull);
+      }
+#else
       if (want && !(blocked && k < kr)) event_step();
+#endif
 #ifdef HS_TIMERS
       __syncwarp();
       HS_T1(5, tev);
@@ -683,7 +731,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
           chosen = (int)all[bw].b;
         }
       }
-      HS_T1(3, tm0);
+
       HS_T0(tc0);
       // ---- commit (scheduling.py:335-346) and enqueue (simulator.py:323-327)
       if (jj == chosen) {
@@ -719,7 +767,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
         }
       }
       if (lane == al) my_assign = (uint8_t)chosen;
-      HS_T1(4, tc0);
+
     }
     if (assign && wsub == 0 && lane < n_in && !failed) assign[o + base + lane] = my_assign;
   }
