@@ -33,7 +33,7 @@ int fail(int code, const std::string& msg) {
 enum Slot {
   S_I, S_O, S_P, S_T, S_OFF, S_DESC, S_TABLE, S_BLK_BEST, S_BLK_IDX, S_BLK_CNT, S_CAND, S_CNT,
   S_TOTAL, S_FIRSTBAD, S_FLAG, S_SELIDX, S_NSEL, S_KEYS, S_KEYS2, S_IDX2, S_CUBTMP, S_RANKED,
-  S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_QNEXT, S_HEAP, S_MINNEED, S_TK_HIST, S_TK_CNT, S_TK_KEY,
+  S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_HEAP, S_MINNEED, S_TK_HIST, S_TK_CNT, S_TK_KEY,
   S_TK_IDX, S_TK_KEY2, S_TK_IDX2, S_DEPS, S_TDEP, S_THEAP, N_SLOTS
 };
 

@@ -19,14 +19,6 @@ __device__ __forceinline__ uint64_t d2u(double d) { return (uint64_t)__double_as
 // Python float(int) for |v| < 2^63: correctly rounded (PyLong_AsDouble).
 __device__ __forceinline__ double i2d(int64_t v) { return __ll2double_rn(v); }
 
-// Python `int > float`, exact (Objects/floatobject.c float_richcompare).
-__device__ __forceinline__ bool int_gt_double(int64_t v, double b) {
-  if (b != b) return false;
-  if (b >= 9223372036854775808.0) return false;
-  if (b < -9223372036854775808.0) return true;
-  return v > (int64_t)floor(b);
-}
-
 // Saturating int64 helpers (values are non-negative byte/token counts; a
 // saturated value compares greater than any budget below 2^63).
 __device__ __forceinline__ int64_t sat_mul(int64_t a, int64_t b) {

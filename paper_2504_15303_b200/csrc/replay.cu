@@ -46,9 +46,10 @@ namespace hs {
 // Diagnostic build only (-DHS_TIMERS): per-warp cycle counts of the replay
 // phases, summed over the launch: [advance, price, evaluate, mapping, commit].
 __device__ unsigned long long g_timers[8];
+// accumulated in registers (tacc[]) and flushed once per lane at kernel end
 #define HS_T0(v) long long v = clock64()
 #define HS_T1(slot, v) \
-  do { if (lane == 0) atomicAdd(&g_timers[slot], (unsigned long long)(clock64() - v)); } while (0)
+  do { tacc[slot] += (unsigned long long)(clock64() - v); } while (0)
 #else
 #define HS_T0(v)
 #define HS_T1(slot, v)
@@ -182,9 +183,9 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t k) {
 
 // Rarely touched per-lane state lives in shared memory.
 struct Cold {
-  double completion, peak, wcur, err_t;
+  double completion, wcur, err_t;
   int64_t tok_count;
-  int32_t req_count, qtail, cnt_max, err, err_req, _pad;
+  int32_t req_count, cnt_max, err, err_req;
 };
 
 // Cross-warp exchange for traces spanning W > 1 warps: one slot per warp of
@@ -280,17 +281,18 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   double topW = 0.0;
   bool sched = false, dirty = true, ex_over = false, max_dirty = false, blocked = false, lerr = false;
   cold.completion = 0.0;
-  cold.peak = 0.0;
   cold.wcur = 0.0;
   cold.err_t = 0.0;
   cold.tok_count = 0;
   cold.req_count = 0;
-  cold.qtail = -1;
   cold.cnt_max = 0;
   cold.err = HS_TRACE_OK;
   cold.err_req = -1;
   uint32_t n_steps = 0;
   int64_t rr_next = 0;
+#ifdef HS_TIMERS
+  unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   int32_t t_err = HS_TRACE_OK, t_err_inst = -1;
   int64_t t_err_req = -1;
   double t_err_val = 0.0;
@@ -304,10 +306,21 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
 
   // A full STEP event (simulator.py:330-355): retirements due at this step,
   // FCFS admission, prefill for newcomers, one decode iteration.
+#ifdef HS_TIMERS
+#define HS_LT0(v) const long long v = clock64()
+#define HS_LT1(slot, v) tacc[slot] += (unsigned long long)(clock64() - v)
+#else
+#define HS_LT0(v)
+#define HS_LT1(slot, v)
+#endif
   auto event_step = [&]() {
     const double t = t_next;
     sched = false;
     ++n_steps;
+#ifdef HS_TIMERS
+    tacc[7] += 1;
+#endif
+    HS_LT0(tr0);
     while (nact > 0 && (uint32_t)(topkey >> 32) == k) {
       // retire in (departure step, admission order); payload was prefetched
       const int32_t r = (int32_t)(topkey & 0xffffffffu);
@@ -343,6 +356,8 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       cold.cnt_max = 0;
       max_dirty = false;
     }
+    HS_LT1(3, tr0);
+    HS_LT0(ta0);
     // admit FCFS (simulator.py:297-316)
     int64_t newly = 0, max_i_new = 0;
     while (qhead >= 0) {
@@ -402,6 +417,8 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     // quotient is monotone in the numerator, so the max of the quotients is
     // the quotient of the max reservation (divided once, at the end).
     if (newly && reserved > max_res) max_res = reserved;
+    HS_LT1(4, ta0);
+    HS_LT0(tc0_);
     if (nact == 0) {  // idle until the next dispatch (simulator.py:344-345)
       kr = 0xffffffffu;
       return;
@@ -436,6 +453,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     kr = (uint32_t)(topkey >> 32);
     t_next = __dadd_rn(t, c);
     sched = true;
+    HS_LT1(5, tc0_);
   };
 
   // Advance every lane's steps with t_next < t_limit (strict: steps at an
@@ -447,27 +465,10 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       if (!__any_sync(FULL, want)) break;
       // phase 1: lanes whose next step is an event (retirement due, or an
       // admission may succeed)
-#ifdef HS_TIMERS
-      __syncwarp();
-      HS_T0(tev);
-      {
-        const bool anyev = __any_sync(FULL, want && !(blocked && k < kr));
-        if (lane == 0 && anyev) atomicAdd(&g_timers[7], 1ull);
-      }
-#endif
-#ifdef HS_TIMERS
-      if (want && !(blocked && k < kr)) {
-        const long long te0 = clock64();
-        event_step();
-        atomicAdd(&g_timers[4], (unsigned long long)(clock64() - te0));
-        atomicAdd(&g_timers[3], 1ull);
-      }
-#else
+
       if (want && !(blocked && k < kr)) event_step();
-#endif
 #ifdef HS_TIMERS
       __syncwarp();
-      HS_T1(5, tev);
       HS_T0(tpu);
 #endif
       // phase 2: every lane whose next steps are pure runs them together,
@@ -837,6 +838,14 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     }
   }
 
+#ifdef HS_TIMERS
+  // warp-level phases (slots 0-2, 6) were timed by every lane: count lane 0;
+  // event-step parts (3-5, 7) are per lane
+  for (int sl = 0; sl < 8; ++sl) {
+    const bool warp_slot = sl <= 2 || sl == 6;
+    if (!warp_slot || lane == 0) atomicAdd(&g_timers[sl], tacc[sl]);
+  }
+#endif
   if (valid) {
     hs_inst_metrics m;
     m.completion_time = cold.completion;

@@ -55,7 +55,7 @@ def main():
     summ = {}
     for k in KEYS:
         if k in r:
-            summ[k] = r[k][0]
+            summ[k] = [r[k][0], r[k][1]]
             print(f"{k:90s} {r[k][0]} {r[k][1]}")
     if js:
         json.dump(summ, open(js, "w"), indent=1)

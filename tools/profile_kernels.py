@@ -67,11 +67,12 @@ def main():
             eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 1)
             eng.replay_device(inst, ps, T, d["off"], d["I"], d["O"], d["O"], d["T"], d["a"], d["m"], d["r"])
             eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 0)
-            names = ["advance", "price", "evaluate", "event_calls", "event_cycles_sum", "event_phase", "pure_phase"]
+            names = ["advance", "price", "evaluate", "ev_retire", "ev_admit", "ev_price", "pure_phase"]
             per = buf[:7].astype(float) / (T * q)
             print("cycles per arrival per warp:", {n: round(v, 1) for n, v in zip(names, per)})
-            print("event phases (with >= 1 event lane) per arrival:", int(buf[7]) / (T * q))
-            print("event_step calls per arrival:", int(buf[3]) / (T * q), " cycles per call:", int(buf[4]) / max(int(buf[3]), 1))
+            calls = max(int(buf[7]), 1)
+            print("event_step calls per arrival:", calls / (T * q), " cycles per call: retire %.0f admit %.0f price %.0f"
+                  % (buf[3] / calls, buf[4] / calls, buf[5] / calls))
     else:
         cluster, reqs, params, _I, _O = bench.search_inputs(10_000)
         t = planner.build_tables(cluster, reqs, params, engine=eng)
