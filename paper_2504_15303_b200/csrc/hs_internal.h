@@ -94,7 +94,7 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           int n_max = 0, int max_types = 0);
 constexpr int kQRecBytes = 24;  // replay.cu QRec
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
-constexpr int kHeapShared = 8;  // replay.cu kHS
+constexpr int kHeapShared = 16;  // replay.cu kHS
 
 int sm_count();
 

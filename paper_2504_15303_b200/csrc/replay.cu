@@ -65,7 +65,7 @@ constexpr unsigned FULL = 0xffffffffu;
 // request (orders retirements as the reference's active list does) and
 // mk = I - k_admit (the quantity whose max gives the cached length).
 // Entries [0, kHS) live in shared memory, the rest in global memory.
-constexpr int kHS = 8;
+constexpr int kHS = 16;
 struct HEnt {
   uint64_t key;
   int64_t mk;
