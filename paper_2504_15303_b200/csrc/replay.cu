@@ -883,10 +883,10 @@ cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
   constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);
   const int warps = W * G;
   const size_t smem = (size_t)warps * 32 * max_types * sizeof(double);
-  if (smem > 16 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  // static (heaps, per-lane state) + dynamic (price buffer) may exceed the
+  // 48 KB default: opt in for the dynamic part every time
+  cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   const unsigned blocks = (unsigned)((n_traces + G - 1) / G);
   k_replay<W, MULTI><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
                                                 d_result, static_cast<QRec*>(d_qrec), d_heap, d_deps, d_trace_dep,
