@@ -264,9 +264,20 @@ def engine_arm(args, rank, world, local_rank):
     # ---- replay inputs (trace shard)
     T_lo, T_hi = shard_range(args.traces, rank, world)
     nT = T_hi - T_lo
+    # inputs drawn on the device (rng.cu), bit-identical to the numpy streams
+    # of gen-trace (lengths seeded by trace index) and generate_arrivals
+    # (seed 42 + trace index); host copies for the e2e leg
+    from paper_2504_15303_b200 import streams
     t0 = time.time()
-    off, I, O, T = replay_inputs(T_lo, T_hi, args.q, args.rate)
+    tseeds = list(range(T_lo, T_hi))
+    lens = streams.gen_trace_lengths_device(tseeds, args.q, "lognormal:200:0.6", "lognormal:150:0.6", 4096, 4096,
+                                            engine=eng)
+    gen_lens_ms = eng.last_kernel_ms
+    arrs = streams.arrival_times_device([42 + t for t in tseeds], [args.q] * nT, args.rate, engine=eng)
+    gen_arr_ms = eng.last_kernel_ms if arrs is not None else 0.0
     gen_s = time.time() - t0
+    off = lens.offsets
+    I, O = lens.to_host()
     rc, config, rparams = replay_deployment()
     handles = build_instances(rc, config, rparams)
     N = len(handles)
@@ -274,10 +285,9 @@ def engine_arm(args, rank, world, local_rank):
     inst = engine_instances(handles, pol)
     ps = _policy_struct(pol, N, hs.kv_bytes_per_token(rc.model))
     nreq = int(off[-1])
-    d = {}
-    for name, arr in (("off", off), ("I", I), ("O", O), ("T", T)):
-        d[name] = eng.device_alloc(arr.nbytes)
-        eng.h2d(d[name], arr)
+    d = {"I": lens.ptrs[0], "O": lens.ptrs[1], "T": None if arrs is None else arrs.ptrs[0]}
+    d["off"] = eng.device_alloc(off.nbytes)
+    eng.h2d(d["off"], off)
     d["assign"] = eng.device_alloc(max(nreq, 1))
     d["metrics"] = eng.device_alloc(max(nT * N, 1) * nat.METRICS_DTYPE.itemsize)
     d["result"] = eng.device_alloc(max(nT, 1) * nat.RESULT_DTYPE.itemsize)
@@ -346,14 +356,22 @@ def engine_arm(args, rank, world, local_rank):
     if not args.no_e2e:
         hI = eng.host_array(I.shape, np.int32); hI[:] = I
         hO = eng.host_array(O.shape, np.int32); hO[:] = O
-        hT = eng.host_array(T.shape, np.float64); hT[:] = T
         rc_, config_, rparams_ = rc, config, rparams
+        aseeds = [42 + t for t in tseeds]
+        hA = eng.host_array((max(nreq, 1),), np.uint8)  # page-locked result buffer, reused every step
+        e2e_parts = {"replay_call_ms": [], "replay_pipeline_ms": []}
 
         def e2e_step():
             t = planner.build_tables(cluster, reqs, params, engine=eng)
             total, idx, nfeas, _ = planner.search_best(t, lo, hi, engine=eng)
-            r = hs.replay_traces(rc_, config_, rparams_, pol, off, hI, hO, hO, arrival=hT, want_assign=True,
+            # arrivals drawn on the device from the seeds, inside the call, as
+            # run_continuous draws them (simulator.py:112-124)
+            w0 = time.perf_counter()
+            r = hs.replay_traces(rc_, config_, rparams_, pol, off, hI, hO, hO, rate=args.rate,
+                                 arrival_seeds=aseeds, want_assign=True, assign_out=hA,
                                  want_depart=False, engine=eng)
+            e2e_parts["replay_call_ms"].append((time.perf_counter() - w0) * 1e3)
+            e2e_parts["replay_pipeline_ms"].append(eng.last_kernel_ms)
             assert (r.result["error"] == 0).all()
             return combine(total, idx, nfeas)
 
@@ -362,14 +380,16 @@ def engine_arm(args, rank, world, local_rank):
         e2e_ms, _ = timed(e2e_step, args.steps)
         M = len(tables.names)
         # predictions are the outputs (oracle predictor): the library copies that buffer once
-        h2d = sI.nbytes + sO.nbytes + off.nbytes + hI.nbytes + hO.nbytes + hT.nbytes
+        h2d = sI.nbytes + sO.nbytes + off.nbytes + hI.nbytes + hO.nbytes + nT * nat.PCG64_DTYPE.itemsize
         d2h = nreq + nT * N * nat.METRICS_DTYPE.itemsize + nT * nat.RESULT_DTYPE.itemsize + \
             M * nat.HS_MAX_DEGREES * nat.ENTRY_DTYPE.itemsize + 16
         if dist:
             h2d += 0
             d2h += world * 24
         e2e = {"value": units / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
-               "d2h_bytes_per_step": int(d2h * world), "ms_per_step": e2e_ms}
+               "d2h_bytes_per_step": int(d2h * world), "ms_per_step": e2e_ms,
+               "replay_call_ms": statistics.median(e2e_parts["replay_call_ms"][-args.steps:]),
+               "replay_pipeline_ms": statistics.median(e2e_parts["replay_pipeline_ms"][-args.steps:])}
 
     # ---- roofline of the dominant kernel (K3 replay)
     peaks = {}
@@ -399,17 +419,19 @@ def engine_arm(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (seeded numpy traces, gen-trace shapes)",
+            "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (gen-trace lognormal lengths + Poisson arrivals, numpy PCG64 streams drawn on the GPU)",
             "config": {"workload": "config3 search (5^16 candidates, 70B, 10k trace) + config4 replay "
                                    f"({args.traces} traces x {args.q} requests, 32 instances, {args.rate} req/s, OS)",
                        "candidates": P, "requests": R_total, "parallelism": f"shard{world}",
-                       "l2": "inputs larger than L2 (replay inputs %.1f GB)" % ((I.nbytes * 3 + T.nbytes) * world / 1e9)},
+                       "l2": "inputs larger than L2 (replay inputs %.1f GB)" % (I.nbytes * 5 * world / 1e9),
+                       "e2e_inputs": "host I/O lengths copied in; arrivals drawn on the device from per-trace seeds"},
             "breakdown": {"k1_table_ms": k1, "k2_search_ms": k2, "k3_replay_ms": k3,
                           "configs_per_s": P / (k2 / 1e3) if world == 1 else cand_local / (k2 / 1e3) * world,
                           "requests_per_s_kernel": nreq / (k3 / 1e3) * world,
                           "step_events_per_request": n_steps_ev / max(nreq, 1),
                           "best_total": best[0], "best_index": best[1], "n_feasible": best[2],
-                          "trace_gen_s": gen_s},
+                          "trace_gen_s": gen_s, "gen_lengths_kernel_ms": gen_lens_ms,
+                          "gen_arrivals_kernel_ms": gen_arr_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "k_replay",
                          "note": "replay is latency-bound (dependent event chains); see DESIGN.md"},

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define HS_ABI_VERSION 2
+#define HS_ABI_VERSION 3
 #define HS_MAX_DEGREES 32   /* power-of-two divisors of an accelerator count  */
 #define HS_MAX_MACHINES 64
 #define HS_MAX_INSTANCES 128 /* one lane per instance, up to 4 warps per trace */
@@ -182,6 +182,48 @@ typedef struct {
   const double* arrival;
 } hs_trace_batch;
 
+/* ---- synthetic workload streams (numpy Generator(PCG64)) ---------------
+ * The reference draws its synthetic inputs from numpy.random.default_rng(seed)
+ * (numpy 2.3, bit generator PCG64 / XSL-RR 128/64):
+ *   cli.py:160-193        gen-trace lengths: lognormal(mu, sigma) or
+ *                         integers(lo, hi + 1), then int(min(max(round(v), 1), cap))
+ *   simulator.py:112-124  arrivals: cumsum(exponential(1 / rate, q))
+ *   scheduling.py:87-95   predictor: int(min(max(round(normal(mean, sd)), 1), cap))
+ * hs_pcg64_state is numpy's pcg64_state: the 128-bit LCG state and increment
+ * plus the buffered upper half a 32-bit draw leaves behind. */
+typedef struct {
+  uint64_t state_hi, state_lo;
+  uint64_t inc_hi, inc_lo;
+  uint32_t has_uint32;
+  uint32_t uinteger;
+} hs_pcg64_state;
+
+typedef enum {
+  HS_DIST_LOGNORMAL_LEN = 0, /* int32: clamp(round(exp(p0 + p1 * N(0,1))), 1, cap) */
+  HS_DIST_UNIFORM_LEN = 1,   /* int32: clamp(integers(lo, hi + 1), 1, cap)          */
+  HS_DIST_EXP_CUMSUM = 2,    /* fp64:  running sum of p0 * Exp(1)                  */
+  HS_DIST_NORMAL_LEN = 3     /* int32: clamp(round(p0 + p1 * N(0,1)), 1, cap)       */
+} hs_dist_kind;
+
+typedef struct {
+  int32_t kind;  /* hs_dist_kind */
+  int32_t cap;   /* upper clamp of the *_LEN kinds (max_input_len / max_output_len) */
+  int64_t lo;    /* UNIFORM_LEN: inclusive bounds, lo <= hi */
+  int64_t hi;
+  double p0;     /* LOGNORMAL: mu; EXP_CUMSUM: scale (= 1 / rate); NORMAL: mean */
+  double p1;     /* LOGNORMAL: sigma; NORMAL: stddev */
+} hs_dist;
+
+/* Device generation of the seeded streams hs_replay_seeded consumes. */
+typedef struct {
+  const hs_pcg64_state* arrival_state;   /* [n_traces] or NULL (use batch->arrival) */
+  double arrival_scale;                  /* 1 / rate */
+  const hs_pcg64_state* predictor_state; /* [n_traces] or NULL (use batch->pred_output_len) */
+  double pred_mean, pred_stddev;         /* predictor mode "normal" */
+  int32_t pred_cap;                      /* limits.max_output_len */
+  int32_t _pad;
+} hs_replay_seeds;
+
 typedef struct hs_ctx hs_ctx;
 
 /* ---- context ---------------------------------------------------------- */
@@ -257,6 +299,35 @@ int hs_replay_deployments(hs_ctx* ctx, const hs_instance* instances, const int32
 int hs_replay_device(hs_ctx* ctx, const hs_instance* instances, const hs_policy* policy,
                      const hs_trace_batch* batch, uint8_t* assign, double* depart,
                      hs_inst_metrics* metrics, hs_trace_result* result);
+
+/* hs_replay with seeded device-side generation: when seeds->arrival_state
+ * is set, trace t's arrivals are cumsum(arrival_scale * Exp(1)) drawn from
+ * arrival_state[t] on the device (simulator.py:112-124; batch->arrival must
+ * be NULL); when seeds->predictor_state is set, its predicted output lengths
+ * are drawn on the device (scheduling.py:87-95, one normal per request in
+ * trace order; batch->pred_output_len is ignored).  Host buffers as hs_replay. */
+int hs_replay_seeded(hs_ctx* ctx, const hs_instance* instances, const hs_policy* policy,
+                     const hs_trace_batch* batch, const hs_replay_seeds* seeds, uint8_t* assign,
+                     double* depart, hs_inst_metrics* metrics, hs_trace_result* result);
+
+/* ---- seeded streams ---------------------------------------------------- */
+/* numpy.random.PCG64(SeedSequence(entropy)) initial state: entropy is the
+ * little-endian 32-bit words of a non-negative int seed (numpy
+ * bit_generator.pyx SeedSequence.generate_state + pcg64_set_seed). */
+int hs_pcg64_seed(const uint32_t* entropy, int32_t n_words, hs_pcg64_state* out);
+/* Batch form for integer seeds below 2^64: out[i] = PCG64(seeds[i]) (the
+ * entropy words of a seed are its low and, when non-zero, high 32 bits). */
+int hs_pcg64_seed_u64(const uint64_t* seeds, int64_t n, hs_pcg64_state* out);
+
+/* Draw stream t's values for each distribution in order: dists[j] fills
+ * out[j][offsets[t] .. offsets[t+1]) of its device buffer (int32 for the
+ * *_LEN kinds, fp64 for EXP_CUMSUM), continuing the same generator (as
+ * cmd_gen_trace draws inputs then outputs from one rng).  states (host, one
+ * per stream) are advanced in place.  bad_index (host, optional, one per
+ * stream) receives the first index whose length draw was not finite (the
+ * reference raises OverflowError on round(inf)) or -1. */
+int hs_rng_generate(hs_ctx* ctx, hs_pcg64_state* states, int32_t n_streams, const int64_t* offsets,
+                    const hs_dist* dists, int32_t n_dists, void* const* out, int64_t* bad_index);
 
 /* Device buffers for hs_replay_device. */
 int hs_device_alloc(hs_ctx* ctx, int64_t bytes, void** out);

@@ -22,13 +22,21 @@ def build() -> pathlib.Path:
     return LIB
 
 
+def _stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    srcs = list(HERE.glob("*.c")) + list(HERE.glob("*.h")) + [HERE.parent / "include" / "hetserve_b200.h"]
+    return any(f.exists() and f.stat().st_mtime > t for f in srcs)
+
+
 _lib = None
 
 
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
-        if not LIB.exists():
+        if _stale():
             build()
         L = C.CDLL(str(LIB))
         vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -53,6 +61,18 @@ def lib() -> C.CDLL:
         L.hs_oracle_rank.restype = C.c_int
         L.hs_oracle_replay.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, vp]
         L.hs_oracle_replay.restype = C.c_int
+        L.hs_oracle_log1p.argtypes = [dbl]
+        L.hs_oracle_log1p.restype = dbl
+        L.hs_oracle_pcg64_next64.argtypes = [vp]
+        L.hs_oracle_pcg64_next64.restype = C.c_uint64
+        L.hs_oracle_std_normal.argtypes = [vp]
+        L.hs_oracle_std_normal.restype = dbl
+        L.hs_oracle_std_exp.argtypes = [vp]
+        L.hs_oracle_std_exp.restype = dbl
+        L.hs_oracle_rng_fill.argtypes = [vp, vp, i64, vp]
+        L.hs_oracle_rng_fill.restype = i64
+        L.hs_oracle_rng_generate.argtypes = [vp, i32, vp, vp, i32, vp, vp]
+        L.hs_oracle_rng_generate.restype = C.c_int
         _lib = L
     return _lib
 
@@ -211,3 +231,36 @@ def best_monotone(table, nd):
         else:
             raise AssertionError("monotone search lost the maximum")
     return V, index, nfeas
+
+
+# ------------------------------------------------------- numpy PCG64 streams
+def log1p(x: float) -> float:
+    return lib().hs_oracle_log1p(float(x))
+
+
+def numpy_state(seed: int) -> np.ndarray:
+    """The initial state numpy itself computes for default_rng(seed)."""
+    from paper_2504_15303_b200._native import PCG64_DTYPE
+    st = np.random.PCG64(seed).state
+    out = np.zeros(1, PCG64_DTYPE)
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    out["state_hi"], out["state_lo"] = s >> 64, s & (2**64 - 1)
+    out["inc_hi"], out["inc_lo"] = inc >> 64, inc & (2**64 - 1)
+    out["has_uint32"], out["uinteger"] = st["has_uint32"], st["uinteger"]
+    return out
+
+
+def rng_generate(states: np.ndarray, offsets: np.ndarray, dists):
+    """hs_oracle_rng_generate with host outputs; returns (outs, bad)."""
+    from paper_2504_15303_b200._native import DIST_EXP_CUMSUM, hs_dist
+    n = len(offsets) - 1
+    total = int(offsets[-1])
+    outs = [np.zeros(max(total, 1), np.float64 if d.kind == DIST_EXP_CUMSUM else np.int32) for d in dists]
+    darr = (hs_dist * len(dists))(*dists)
+    oarr = (C.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+    bad = np.full(max(n, 1), -1, np.int64)
+    off = np.ascontiguousarray(offsets, np.int64)
+    rc = lib().hs_oracle_rng_generate(_p(states), n, _p(off), C.cast(darr, C.c_void_p), len(dists),
+                                      C.cast(oarr, C.c_void_p), _p(bad))
+    assert rc == 0, rc
+    return [o[:total] for o in outs], bad[:n]

@@ -93,6 +93,23 @@ class hs_trace_batch(C.Structure):
                 ("output_len", C.c_void_p), ("pred_output_len", C.c_void_p), ("arrival", C.c_void_p)]
 
 
+class hs_pcg64_state(C.Structure):
+    _fields_ = [("state_hi", C.c_uint64), ("state_lo", C.c_uint64), ("inc_hi", C.c_uint64), ("inc_lo", C.c_uint64),
+                ("has_uint32", C.c_uint32), ("uinteger", C.c_uint32)]
+
+
+class hs_dist(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("cap", C.c_int32), ("lo", C.c_int64), ("hi", C.c_int64), ("p0", C.c_double),
+                ("p1", C.c_double)]
+
+
+class hs_replay_seeds(C.Structure):
+    _fields_ = [("arrival_state", C.c_void_p), ("arrival_scale", C.c_double), ("predictor_state", C.c_void_p),
+                ("pred_mean", C.c_double), ("pred_stddev", C.c_double), ("pred_cap", C.c_int32), ("_pad", C.c_int32)]
+
+
+DIST_LOGNORMAL_LEN, DIST_UNIFORM_LEN, DIST_EXP_CUMSUM, DIST_NORMAL_LEN = 0, 1, 2, 3
+
 # numpy views of the structs (same layout) for bulk results
 ENTRY_DTYPE = np.dtype([("contribution", "<f8"), ("rate", "<f8"), ("budget", "<f8"), ("slack", "<f8"),
                         ("instance_count", "<i8"), ("bad_request", "<i8"), ("token_count", "<i8"),
@@ -100,6 +117,8 @@ ENTRY_DTYPE = np.dtype([("contribution", "<f8"), ("rate", "<f8"), ("budget", "<f
 CAND_DTYPE = np.dtype([("total", "<f8"), ("index", "<i8")])
 METRICS_DTYPE = np.dtype([("completion_time", "<f8"), ("peak_kv_usage", "<f8"), ("residual_load", "<f8"),
                           ("request_count", "<i8"), ("token_count", "<i8")])
+PCG64_DTYPE = np.dtype([("state_hi", "<u8"), ("state_lo", "<u8"), ("inc_hi", "<u8"), ("inc_lo", "<u8"),
+                        ("has_uint32", "<u4"), ("uinteger", "<u4")])
 RESULT_DTYPE = np.dtype([("error", "<i4"), ("err_instance", "<i4"), ("err_request", "<i8"), ("err_value", "<f8"),
                          ("n_steps", "<i8")])
 
@@ -110,6 +129,7 @@ EXPORTS = (
     "hs_replay_deployments",
     "hs_replay_device", "hs_device_alloc", "hs_device_free", "hs_memcpy_h2d", "hs_memcpy_d2h",
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
+    "hs_replay_seeded", "hs_pcg64_seed", "hs_pcg64_seed_u64", "hs_rng_generate",
 )
 
 _lib = None
@@ -150,6 +170,10 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_host_free": ([vp, vp], C.c_int),
             "hs_ctx_stream": ([vp], vp),
             "hs_probe_fp64": ([vp, C.POINTER(dbl)], C.c_int),
+            "hs_replay_seeded": ([vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+            "hs_pcg64_seed": ([vp, i32, vp], C.c_int),
+            "hs_pcg64_seed_u64": ([vp, i64, vp], C.c_int),
+            "hs_rng_generate": ([vp, vp, i32, vp, vp, i32, vp, vp], C.c_int),
         }
         for name, (args, res) in sig.items():
             try:
@@ -161,6 +185,14 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
         if path is None:
             _lib = lib
         return lib
+
+
+def _out_buf(out: np.ndarray | None, n: int, dtype) -> np.ndarray:
+    if out is None:
+        return np.zeros(max(n, 1), dtype)
+    if out.dtype != np.dtype(dtype) or not out.flags.c_contiguous or len(out) < n or not out.flags.writeable:
+        raise ValueError(f"output buffer must be a writable contiguous {np.dtype(dtype)} array of >= {n} elements")
+    return out
 
 
 def _ptr(a: np.ndarray | None):
@@ -276,6 +308,21 @@ class Engine:
                                        C.c_void_p(d_metrics), C.c_void_p(d_result))
         self.check(rc, "hs_replay_device")
 
+    # --------------------------------------------------------------- streams
+    def rng_generate(self, states: np.ndarray, offsets: np.ndarray, dists, outs) -> np.ndarray:
+        """hs_rng_generate: states (PCG64_DTYPE, advanced in place), device
+        output pointers one per hs_dist; returns the per-stream bad index."""
+        n = len(offsets) - 1
+        assert states.dtype == PCG64_DTYPE and states.flags.c_contiguous and len(states) >= n
+        off = np.ascontiguousarray(offsets, np.int64)
+        darr = (hs_dist * len(dists))(*dists)
+        oarr = (C.c_void_p * len(outs))(*[C.c_void_p(int(o)) if o else None for o in outs])
+        bad = np.full(max(n, 1), -1, np.int64)
+        rc = self.lib.hs_rng_generate(self.handle, _ptr(states), n, _ptr(off), C.cast(darr, C.c_void_p), len(dists),
+                                      C.cast(oarr, C.c_void_p), _ptr(bad))
+        self.check(rc, "hs_rng_generate")
+        return bad[:n]
+
     # ---------------------------------------------------------------- search
     def search_tables(self, model: hs_model, engine: hs_engine, limits: hs_limits, machines: np.ndarray,
                       params: np.ndarray, present: np.ndarray, I: np.ndarray, O: np.ndarray):
@@ -322,21 +369,65 @@ class Engine:
 
     # ---------------------------------------------------------------- replay
     def replay(self, instances, policy: hs_policy, offsets: np.ndarray, I: np.ndarray, O: np.ndarray,
-               P: np.ndarray, arrival: np.ndarray | None, want_assign: bool = True, want_depart: bool = True):
+               P: np.ndarray | None, arrival: np.ndarray | None, want_assign: bool = True, want_depart: bool = True,
+               seeds: hs_replay_seeds | None = None, assign_out: np.ndarray | None = None,
+               depart_out: np.ndarray | None = None):
+        """hs_replay, or hs_replay_seeded when `seeds` asks for device-drawn
+        arrivals / predictions (P may then be None).  assign_out / depart_out:
+        optional caller-owned (e.g. page-locked) result buffers."""
         T = len(offsets) - 1
         N = policy.n_instances
         total = int(offsets[-1])
-        batch = hs_trace_batch(T, offsets.ctypes.data, I.ctypes.data, O.ctypes.data, P.ctypes.data,
-                               None if arrival is None else arrival.ctypes.data)
-        assign = np.zeros(max(total, 1), np.uint8) if want_assign else None
-        depart = np.zeros(max(total, 1), np.float64) if want_depart else None
+        batch = hs_trace_batch(T, offsets.ctypes.data, I.ctypes.data, O.ctypes.data,
+                               None if P is None else P.ctypes.data, None if arrival is None else arrival.ctypes.data)
+        assign = _out_buf(assign_out, total, np.uint8) if want_assign else None
+        depart = _out_buf(depart_out, total, np.float64) if want_depart else None
         metrics = np.zeros(max(T * N, 1), METRICS_DTYPE)
         result = np.zeros(max(T, 1), RESULT_DTYPE)
-        rc = self.lib.hs_replay(self.handle, C.cast(instances, C.c_void_p), C.byref(policy), C.byref(batch),
-                                _ptr(assign), _ptr(depart), _ptr(metrics), _ptr(result))
-        self.check(rc, "hs_replay")
+        if seeds is None:
+            rc = self.lib.hs_replay(self.handle, C.cast(instances, C.c_void_p), C.byref(policy), C.byref(batch),
+                                    _ptr(assign), _ptr(depart), _ptr(metrics), _ptr(result))
+            self.check(rc, "hs_replay")
+        else:
+            rc = self.lib.hs_replay_seeded(self.handle, C.cast(instances, C.c_void_p), C.byref(policy),
+                                           C.byref(batch), C.byref(seeds), _ptr(assign), _ptr(depart),
+                                           _ptr(metrics), _ptr(result))
+            self.check(rc, "hs_replay_seeded")
         return (None if assign is None else assign[:total], None if depart is None else depart[:total],
                 metrics[: T * N].reshape(T, N), result[:T])
+
+
+def pcg64_state(seed: int) -> np.ndarray:
+    """numpy.random.PCG64(seed) initial state (SeedSequence(seed) entropy =
+    the seed's little-endian 32-bit words) via hs_pcg64_seed; host only."""
+    seed = int(seed)
+    if seed < 0:
+        raise ValueError("expected non-negative integer")
+    words = [(seed >> (32 * i)) & 0xFFFFFFFF for i in range(max(1, (seed.bit_length() + 31) // 32))]
+    ent = np.array(words, np.uint32)
+    out = np.zeros(1, PCG64_DTYPE)
+    lib = load_library()
+    rc = lib.hs_pcg64_seed(_ptr(ent), len(ent), _ptr(out))
+    if rc != HS_OK:
+        raise EngineError(rc, "hs_pcg64_seed: " + (lib.hs_last_error() or b"").decode())
+    return out
+
+
+def pcg64_states(seeds) -> np.ndarray:
+    """One PCG64 state per seed (PCG64_DTYPE array); one C call for seeds
+    below 2^64."""
+    seeds = [int(s) for s in seeds]
+    if any(s < 0 for s in seeds):
+        raise ValueError("expected non-negative integer")
+    if not all(s < 2**64 for s in seeds):
+        return np.concatenate([pcg64_state(s) for s in seeds])
+    arr = np.array(seeds, np.uint64)
+    out = np.zeros(len(seeds), PCG64_DTYPE)
+    lib = load_library()
+    rc = lib.hs_pcg64_seed_u64(_ptr(arr), len(arr), _ptr(out))
+    if rc != HS_OK:
+        raise EngineError(rc, "hs_pcg64_seed_u64: " + (lib.hs_last_error() or b"").decode())
+    return out
 
 
 _engines: dict = {}

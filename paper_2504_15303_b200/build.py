@@ -19,7 +19,7 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhetserve_b200.so"
-SOURCES = ["capi.cu", "search.cu", "replay.cu", "topk.cu"]
+SOURCES = ["capi.cu", "search.cu", "replay.cu", "topk.cu", "rng.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -34,7 +34,8 @@ enum Slot {
   S_I, S_O, S_P, S_T, S_OFF, S_DESC, S_TABLE, S_BLK_BEST, S_BLK_IDX, S_BLK_CNT, S_CAND, S_CNT,
   S_TOTAL, S_FIRSTBAD, S_FLAG, S_SELIDX, S_NSEL, S_KEYS, S_KEYS2, S_IDX2, S_CUBTMP, S_RANKED,
   S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_HEAP, S_MINNEED, S_TK_HIST, S_TK_CNT, S_TK_KEY,
-  S_TK_IDX, S_TK_KEY2, S_TK_IDX2, S_DEPS, S_TDEP, S_THEAP, N_SLOTS
+  S_TK_IDX, S_TK_KEY2, S_TK_IDX2, S_DEPS, S_TDEP, S_THEAP, S_RNG_ST, S_RNG_ST2, S_RNG_OFF, S_RNG_BAD,
+  N_SLOTS
 };
 
 }  // namespace
@@ -691,8 +692,21 @@ int hs_search_topk(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t 
   return HS_OK;
 }
 
-int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b, uint8_t* assign,
-              double* depart, hs_inst_metrics* metrics, hs_trace_result* result) {
+namespace {
+
+int check_dist(const hs_dist& d) {
+  if (d.kind < HS_DIST_LOGNORMAL_LEN || d.kind > HS_DIST_NORMAL_LEN) return fail(HS_ERR_ARG, "unknown distribution");
+  if (d.kind != HS_DIST_EXP_CUMSUM && d.cap < 1) return fail(HS_ERR_ARG, "length cap must be >= 1");
+  if (d.kind == HS_DIST_UNIFORM_LEN && d.lo > d.hi) return fail(HS_ERR_ARG, "uniform needs lo <= hi");
+  return HS_OK;
+}
+
+// hs_replay / hs_replay_seeded: host buffers, traces replayed in kPipe chunks
+// (copy of chunk i+1 overlaps the replay of chunk i); seeded arrivals and
+// predictions are drawn on the chunk's stream right before its replay.
+int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b,
+                const hs_replay_seeds* seeds, uint8_t* assign, double* depart, hs_inst_metrics* metrics,
+                hs_trace_result* result) {
   if (!c || !inst || !pol || !b || !metrics || !result || !b->offsets) return fail(HS_ERR_ARG, "null argument");
   int rc;
   if ((rc = use_device(c))) return rc;
@@ -701,15 +715,28 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
   const int64_t* off = b->offsets;
   if (off[0] != 0) return fail(HS_ERR_ARG, "offsets[0] must be 0");
   const int64_t total = off[T];
-  if (total > 0 && (!b->input_len || !b->output_len || !b->pred_output_len)) return fail(HS_ERR_ARG, "null trace");
+  const bool gen_arr = seeds && seeds->arrival_state;
+  const bool gen_pred = seeds && seeds->predictor_state;
+  if (gen_arr && b->arrival) return fail(HS_ERR_ARG, "seeded arrivals need batch->arrival = NULL");
+  if (gen_pred && seeds->pred_cap < 1) return fail(HS_ERR_ARG, "pred_cap must be >= 1");
+  if (total > 0 && (!b->input_len || !b->output_len || (!gen_pred && !b->pred_output_len)))
+    return fail(HS_ERR_ARG, "null trace");
   hs::ReplayConst base;
-  if ((rc = make_const(inst, pol, b->arrival != nullptr, &base))) return rc;
+  if ((rc = make_const(inst, pol, b->arrival != nullptr || gen_arr, &base))) return rc;
   int64_t max_q;
   if ((rc = check_offsets(off, T, &max_q))) return rc;
   if ((rc = ensure_pipeline(c))) return rc;
   const int N = pol->n_instances;
   // predictions identical to the outputs (oracle predictor): copy once
-  const bool p_is_o = b->pred_output_len == b->output_len;
+  const bool p_is_o = !gen_pred && b->pred_output_len == b->output_len;
+  hs_pcg64_state *dSA = nullptr, *dSP = nullptr;
+  if (gen_arr && (rc = ensure_t(c, S_RNG_ST, (size_t)(T > 0 ? T : 1), &dSA))) return rc;
+  if (gen_pred && (rc = ensure_t(c, S_RNG_ST2, (size_t)(T > 0 ? T : 1), &dSP))) return rc;
+  if (gen_arr && T > 0)
+    HS_CUDA(cudaMemcpyAsync(dSA, seeds->arrival_state, sizeof(hs_pcg64_state) * T, cudaMemcpyHostToDevice, c->stream));
+  if (gen_pred && T > 0)
+    HS_CUDA(cudaMemcpyAsync(dSP, seeds->predictor_state, sizeof(hs_pcg64_state) * T, cudaMemcpyHostToDevice,
+                            c->stream));
   int64_t* dOff;
   int32_t *dI, *dO, *dP;
   double* dT = nullptr;
@@ -729,7 +756,7 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
   } else if ((rc = ensure_t(c, S_P, tq, &dP))) {
     return rc;
   }
-  if (b->arrival && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
+  if ((b->arrival || gen_arr) && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
   if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
   if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
   HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
@@ -750,10 +777,10 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
     if (n > 0) {
       HS_CUDA(cudaMemcpyAsync(dI + a, b->input_len + a, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
       HS_CUDA(cudaMemcpyAsync(dO + a, b->output_len + a, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-      if (!p_is_o)
+      if (!p_is_o && !gen_pred)
         HS_CUDA(cudaMemcpyAsync(dP + a, b->pred_output_len + a, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
                                 c->stream));
-      if (dT) HS_CUDA(cudaMemcpyAsync(dT + a, b->arrival + a, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+      if (dT && !gen_arr) HS_CUDA(cudaMemcpyAsync(dT + a, b->arrival + a, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
     }
     HS_CUDA(cudaEventRecord(c->ev_copy[i], c->stream));
     HS_CUDA(cudaStreamWaitEvent(c->aux, c->ev_copy[i], 0));
@@ -781,6 +808,22 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
     HS_CUDA(cudaStreamWaitEvent(ks, c->ev_copy[i], 0));
     const size_t hb = (size_t)(t1 - t0 > 0 ? t1 - t0 : 1) * rci.heap_stride * hs::kHEntBytes;
     HS_CUDA(cudaMallocAsync(&heaps[i], hb, ks));
+    if (gen_arr) {
+      hs::RngConst g{};
+      g.n_dists = 1;
+      g.dist[0] = hs_dist{HS_DIST_EXP_CUMSUM, 0, 0, 0, seeds->arrival_scale, 0.0};
+      g.out[0] = dT;
+      HS_CUDA(hs::launch_rng_generate(g, dSA, dOff, t0, t1, nullptr, ks));
+      c->launches += 1;
+    }
+    if (gen_pred) {
+      hs::RngConst g{};
+      g.n_dists = 1;
+      g.dist[0] = hs_dist{HS_DIST_NORMAL_LEN, seeds->pred_cap, 0, 0, seeds->pred_mean, seeds->pred_stddev};
+      g.out[0] = dP;
+      HS_CUDA(hs::launch_rng_generate(g, dSP, dOff, t0, t1, nullptr, ks));
+      c->launches += 1;
+    }
     HS_CUDA(hs::launch_replay(rci, t1 - t0, dOff + t0, dI, dO, dP, dT, dA, dDep, dM + t0 * N, dR + t0, dQ,
                               static_cast<uint64_t*>(heaps[i]), ks));
     c->launches += 1;
@@ -803,6 +846,121 @@ int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs
   if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
   if (depart && total > 0)
     HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+
+}  // namespace
+
+int hs_replay(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b, uint8_t* assign,
+              double* depart, hs_inst_metrics* metrics, hs_trace_result* result) {
+  return replay_host(c, inst, pol, b, nullptr, assign, depart, metrics, result);
+}
+
+int hs_replay_seeded(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b,
+                     const hs_replay_seeds* seeds, uint8_t* assign, double* depart, hs_inst_metrics* metrics,
+                     hs_trace_result* result) {
+  if (!seeds) return fail(HS_ERR_ARG, "null seeds");
+  return replay_host(c, inst, pol, b, seeds, assign, depart, metrics, result);
+}
+
+// numpy bit_generator.pyx SeedSequence (pool of 4 words, hashmix/mix) and
+// pcg64.c pcg64_set_seed / pcg_setseq_128_srandom_r.
+int hs_pcg64_seed(const uint32_t* entropy, int32_t n_words, hs_pcg64_state* out) {
+  if (!out || n_words < 1 || !entropy) return fail(HS_ERR_ARG, "need at least one entropy word");
+  const uint32_t INIT_A = 0x43b0d7e5u, MULT_A = 0x931e8875u, INIT_B = 0x8b51f9ddu, MULT_B = 0x58f38dedu;
+  const uint32_t MIX_L = 0xca01f9ddu, MIX_R = 0x4973f715u;
+  uint32_t hc = INIT_A;
+  auto hashmix = [&](uint32_t v) {
+    v ^= hc;
+    hc *= MULT_A;
+    v *= hc;
+    v ^= v >> 16;
+    return v;
+  };
+  auto mix = [](uint32_t x, uint32_t y) {
+    uint32_t r = MIX_L * x - MIX_R * y;
+    return r ^ (r >> 16);
+  };
+  uint32_t pool[4];
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < n_words ? entropy[i] : 0u);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s]));
+  for (int s = 4; s < n_words; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(entropy[s]));
+  uint32_t w[8];
+  uint32_t hb = INIT_B;
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hb;
+    hb *= MULT_B;
+    v *= hb;
+    v ^= v >> 16;
+    w[i] = v;
+  }
+  const uint64_t s0 = w[0] | ((uint64_t)w[1] << 32), s1 = w[2] | ((uint64_t)w[3] << 32);
+  const uint64_t i0 = w[4] | ((uint64_t)w[5] << 32), i1 = w[6] | ((uint64_t)w[7] << 32);
+  typedef unsigned __int128 u128;
+  const u128 mult = ((u128)2549297995355413924ull << 64) | 4865540595714422341ull;
+  const u128 initstate = ((u128)s0 << 64) | s1, initseq = ((u128)i0 << 64) | i1;
+  const u128 inc = (initseq << 1) | 1u;
+  u128 st = 0;
+  st = st * mult + inc;
+  st += initstate;
+  st = st * mult + inc;
+  out->state_hi = (uint64_t)(st >> 64);
+  out->state_lo = (uint64_t)st;
+  out->inc_hi = (uint64_t)(inc >> 64);
+  out->inc_lo = (uint64_t)inc;
+  out->has_uint32 = 0;
+  out->uinteger = 0;
+  return HS_OK;
+}
+
+int hs_pcg64_seed_u64(const uint64_t* seeds, int64_t n, hs_pcg64_state* out) {
+  if (n < 0 || (n > 0 && (!seeds || !out))) return fail(HS_ERR_ARG, "null argument");
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t w[2] = {(uint32_t)seeds[i], (uint32_t)(seeds[i] >> 32)};
+    int rc = hs_pcg64_seed(w, w[1] ? 2 : 1, out + i);
+    if (rc) return rc;
+  }
+  return HS_OK;
+}
+
+int hs_rng_generate(hs_ctx* c, hs_pcg64_state* states, int32_t n_streams, const int64_t* offsets,
+                    const hs_dist* dists, int32_t n_dists, void* const* out, int64_t* bad_index) {
+  if (!c || !states || !offsets || !dists || !out) return fail(HS_ERR_ARG, "null argument");
+  if (n_streams < 0) return fail(HS_ERR_ARG, "n_streams < 0");
+  if (n_dists < 1 || n_dists > hs::kMaxDists) return fail(HS_ERR_ARG, "n_dists must be 1..4");
+  if (offsets[0] != 0) return fail(HS_ERR_ARG, "offsets[0] must be 0");
+  int rc;
+  for (int32_t t = 0; t < n_streams; ++t)
+    if (offsets[t + 1] < offsets[t]) return fail(HS_ERR_ARG, "offsets must be non-decreasing");
+  hs::RngConst g{};
+  g.n_dists = n_dists;
+  for (int32_t j = 0; j < n_dists; ++j) {
+    if ((rc = check_dist(dists[j]))) return rc;
+    if (offsets[n_streams] > 0 && !out[j]) return fail(HS_ERR_ARG, "null output buffer");
+    g.dist[j] = dists[j];
+    g.out[j] = out[j];
+  }
+  if (n_streams == 0) return HS_OK;
+  if ((rc = use_device(c))) return rc;
+  hs_pcg64_state* dS;
+  int64_t *dOff, *dBad;
+  if ((rc = ensure_t(c, S_RNG_ST, (size_t)n_streams, &dS)) || (rc = ensure_t(c, S_RNG_OFF, (size_t)n_streams + 1, &dOff)) ||
+      (rc = ensure_t(c, S_RNG_BAD, (size_t)n_streams, &dBad)))
+    return rc;
+  HS_CUDA(cudaMemcpyAsync(dS, states, sizeof(hs_pcg64_state) * n_streams, cudaMemcpyHostToDevice, c->stream));
+  HS_CUDA(cudaMemcpyAsync(dOff, offsets, sizeof(int64_t) * (n_streams + 1), cudaMemcpyHostToDevice, c->stream));
+  if ((rc = begin_timing(c))) return rc;
+  HS_CUDA(hs::launch_rng_generate(g, dS, dOff, 0, n_streams, dBad, c->stream));
+  c->launches += 1;
+  if ((rc = end_timing(c))) return rc;
+  HS_CUDA(cudaMemcpyAsync(states, dS, sizeof(hs_pcg64_state) * n_streams, cudaMemcpyDeviceToHost, c->stream));
+  if (bad_index)
+    HS_CUDA(cudaMemcpyAsync(bad_index, dBad, sizeof(int64_t) * n_streams, cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   return HS_OK;
 }

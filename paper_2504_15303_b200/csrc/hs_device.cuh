@@ -162,6 +162,84 @@ __device__ __forceinline__ double py_exp(double x, const uint64_t* tab, bool* ov
   return __fma_rn(scale, tmp, scale);
 }
 
+// glibc 2.39 log1p, FMA variant (sysdeps/ieee754/dbl-64/s_log1p.c compiled
+// with FMA contraction; what numpy's ziggurat tails call on an FMA x86-64
+// host).  Restated from the compiled variant's operation order: the
+// polynomial and the k*ln2 reconstruction are fused exactly where its
+// vfmadd/vfmsub instructions are.
+__device__ __forceinline__ double py_log1p(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01,
+               Lp3 = 2.857142874366239149e-01, Lp4 = 2.222219843214978396e-01,
+               Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  int32_t hx = __double2hiint(x), ax = hx & 0x7fffffff, hu = 0, k = 1;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3fda827a) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -__longlong_as_double(0x7ff0000000000000ll) : __longlong_as_double(0x7ff8000000000000ll);
+    if (ax < 0x3e200000) {
+      if (ax < 0x3c900000) return x;
+      return __fma_rn(-__dmul_rn(x, x), 0.5, x);
+    }
+    if (hx > 0 || hx < (int32_t)0xbfd2bec4) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  } else if (hx >= 0x7ff00000) {
+    return __dadd_rn(x, x);
+  }
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = __dadd_rn(1.0, x);
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = (k > 0) ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = __hiloint2double(hu | 0x3ff00000, __double2loint(u));
+    } else {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, __double2loint(u));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+  if (hu == 0) {
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      double dk = (double)k;
+      return __fma_rn(dk, ln2_hi, __fma_rn(dk, ln2_lo, c));
+    }
+    double R = __dmul_rn(__fma_rn(-f, 0.66666666666666666, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    double dk = (double)k;
+    return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, ln2_lo, c)), f));
+  }
+  double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+  double z = __dmul_rn(s, s);
+  double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+  double z2 = __dmul_rn(z, z);
+  double z4 = __dmul_rn(z2, z2);
+  double z6 = __dmul_rn(z2, z4);
+  double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+  R = __fma_rn(z4, R3, R);
+  R = __fma_rn(z6, R4, R);
+  double t = __dmul_rn(s, __dadd_rn(R, hfsq));
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  double dk = (double)k;
+  return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(__fma_rn(dk, ln2_lo, c), t)), f));
+}
+
 // warp helpers --------------------------------------------------------------
 __device__ __forceinline__ double shfl_d(double v, int src) {
   return __shfl_sync(0xffffffffu, v, src);

@@ -96,6 +96,18 @@ constexpr int kQRecBytes = 24;  // replay.cu QRec
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
 constexpr int kHeapShared = 16;  // replay.cu kHS
 
+// Seeded streams (rng.cu): up to kMaxDists distributions drawn in order from
+// each stream; out[j] is indexed by the stream offsets.
+constexpr int kMaxDists = 4;
+struct RngConst {
+  int32_t n_dists;
+  int32_t _pad;
+  hs_dist dist[kMaxDists];
+  void* out[kMaxDists];
+};
+cudaError_t launch_rng_generate(const RngConst& rc, hs_pcg64_state* d_states, const int64_t* d_off,
+                                int64_t s_begin, int64_t s_end, int64_t* d_bad, cudaStream_t st);
+
 int sm_count();
 
 }  // namespace hs

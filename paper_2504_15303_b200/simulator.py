@@ -24,6 +24,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native as nat
+from . import streams
 from .domain import (
     InfeasibleConfigError,
     InfeasibleRequestError,
@@ -210,12 +211,22 @@ def _run(scenario, static: bool, engine=None) -> SimMetrics:
     per_token = kv_bytes_per_token(scenario.cluster.model)
     I = np.fromiter((r.input_len for r in trace), np.int64, len(trace))
     O = np.fromiter((r.output_len for r in trace), np.int64, len(trace))
-    P = _predictor(scenario).predict_lengths(O)
-    for a in (I, O, P):
+    for a in (I, O):
         if len(a) and a.max() > 2**31 - 1:
             raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, "request lengths above 2^31 - 1")
-    T = arrival_times(len(trace), scenario.arrival_rate, scenario.seed)
     eng = engine or nat.engine_for()
+    # seeded draws on the device (rng.cu), bit-identical to the reference's
+    # numpy streams: predictor (scheduling.py:87-95), arrivals (simulator.py:112-124)
+    pred = _predictor(scenario)
+    cfg = pred._config
+    if cfg.mode == "normal":
+        P = streams.predict_lengths([cfg.seed], [len(trace)], cfg.mean, cfg.stddev,
+                                    scenario.cluster.limits.max_output_len, engine=eng).astype(np.int64)
+    else:
+        P = pred.predict_lengths(O)
+    if not math.isinf(scenario.arrival_rate) and scenario.arrival_rate <= 0:
+        raise SpecError(f"arrival rate must be positive, got {scenario.arrival_rate}")
+    T = streams.arrival_times([scenario.seed], [len(trace)], scenario.arrival_rate, engine=eng)
     offsets = np.array([0, len(trace)], np.int64)
     assign, depart, metrics, result = eng.replay(
         engine_instances(handles, policy), _policy_struct(policy, N, per_token, 1 if static else 0), offsets,
@@ -296,8 +307,17 @@ class ReplayBatchResult:
 
 
 def replay_traces(cluster, config, params, policy: PolicyConfig, offsets, input_len, output_len, pred_output_len,
-                  arrival=None, want_assign=True, want_depart=False, engine=None, static=False) -> ReplayBatchResult:
-    """Replay T traces (offsets [T+1]) on one deployment in one launch."""
+                  arrival=None, want_assign=True, want_depart=False, engine=None, static=False, rate=None,
+                  arrival_seeds=None, predictor_seeds=None, assign_out=None, depart_out=None) -> ReplayBatchResult:
+    """Replay T traces (offsets [T+1]) on one deployment in one launch.
+
+    Arrivals are either given (``arrival``, fp64 per request; None = rate
+    inf) or drawn on the device as generate_arrivals(trace_t, rate,
+    arrival_seeds[t]) (simulator.py:112-124).  With policy.predictor in
+    "normal" mode and ``predictor_seeds``, predictions are drawn on the
+    device as OutputLengthPredictor (scheduling.py:87-95) seeded per trace,
+    and pred_output_len may be None.  assign_out / depart_out: optional
+    caller-owned result buffers (e.g. Engine.host_array, page-locked)."""
     handles = build_instances(cluster, config, params)
     _check_scheduler(handles, policy)
     N = len(handles)
@@ -305,11 +325,27 @@ def replay_traces(cluster, config, params, policy: PolicyConfig, offsets, input_
         raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"{N} instances (max {nat.HS_MAX_INSTANCES})")
     per_token = kv_bytes_per_token(cluster.model)
     eng = engine or nat.engine_for()
+    seeds = keep = None
+    pred = policy.predictor
+    dev_pred = predictor_seeds is not None and pred.mode == "normal"
+    if dev_pred:
+        OutputLengthPredictor(pred, cluster.limits.max_output_len)  # the reference's argument checks
+    if (arrival_seeds is not None and rate is not None and not math.isinf(rate)) or dev_pred:
+        if arrival is not None and arrival_seeds is not None:
+            raise SpecError("give either arrival times or arrival seeds, not both")
+        seeds, keep = streams.replay_seeds(arrival_seeds, math.inf if rate is None else rate,
+                                           pred if dev_pred else None, predictor_seeds,
+                                           cluster.limits.max_output_len)
+    elif rate is not None and not math.isinf(rate) and arrival is None:
+        raise SpecError("a finite rate needs arrival times or arrival seeds")
+    P = None if dev_pred else np.ascontiguousarray(pred_output_len, np.int32)
     a, d, m, r = eng.replay(engine_instances(handles, policy), _policy_struct(policy, N, per_token, 1 if static else 0),
                             np.ascontiguousarray(offsets, np.int64), np.ascontiguousarray(input_len, np.int32),
-                            np.ascontiguousarray(output_len, np.int32), np.ascontiguousarray(pred_output_len, np.int32),
+                            np.ascontiguousarray(output_len, np.int32), P,
                             None if arrival is None else np.ascontiguousarray(arrival, np.float64),
-                            want_assign=want_assign, want_depart=want_depart)
+                            want_assign=want_assign, want_depart=want_depart, seeds=seeds, assign_out=assign_out,
+                            depart_out=depart_out)
+    del keep
     return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)
 
 

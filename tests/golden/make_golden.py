@@ -414,8 +414,56 @@ def build_exp_vectors() -> dict:
             "overflow": [H(x) for x in (709.8, 710.0, 1e5)]}
 
 
+STREAM_TRACES = [  # (seed, count, input_dist, output_dist, max_in, max_out)
+    (0, 2001, "lognormal:200:0.6", "lognormal:150:0.6", 4096, 4096),
+    (7, 1001, "uniform:1:4096", "lognormal:300:1.0", 4096, 2048),
+    (9, 999, "uniform:5:77", "uniform:1:9", 64, 8),
+    (3, 777, "lognormal:1000:2.5", "uniform:1:4294967296", 4096, 4096),
+    (11, 1, "uniform:3:3", "lognormal:50:0.1", 4096, 4096),
+    (12, 0, "lognormal:50:0.1", "lognormal:50:0.1", 4096, 4096),
+    (13, 300, "lognormal:1.7e308:0.5", "lognormal:10:0.5", 4096, 4096),  # overflows: round(inf)
+]
+STREAM_ARRIVALS = [(3000, 140.0, 42), (1000, 0.5, 1), (257, 1e6, 77), (5, float("inf"), 3)]
+STREAM_PREDICTORS = [(2000, 150.0, 60.0, 5, 4096), (999, 3.0, 40.0, 8, 16), (300, 1e4, 1.0, 2, 4096)]
+
+
+def build_stream_cases() -> dict:
+    """The reference's own seeded draws: cmd_gen_trace (cli.py:183-197),
+    generate_arrivals (simulator.py:112-124), OutputLengthPredictor.predict
+    (scheduling.py:87-95), one call per request in trace order."""
+    import argparse
+    import tempfile
+
+    from hetserve import cli as ref_cli
+
+    traces = []
+    for seed, count, di, do, mi, mo in STREAM_TRACES:
+        with tempfile.TemporaryDirectory() as tmp:
+            out = pathlib.Path(tmp) / "t.jsonl"
+            ns = argparse.Namespace(seed=seed, count=count, input_dist=di, output_dist=do, max_input_len=mi,
+                                    max_output_len=mo, out=str(out))
+            try:
+                ref_cli.cmd_gen_trace(ns)
+                reqs = hs.parse_trace(out.read_text())
+                traces.append(dict(seed=seed, count=count, input_dist=di, output_dist=do, max_in=mi, max_out=mo,
+                                   I=[r.input_len for r in reqs], O=[r.output_len for r in reqs], error=None))
+            except Exception as exc:  # noqa: BLE001
+                traces.append(dict(seed=seed, count=count, input_dist=di, output_dist=do, max_in=mi, max_out=mo,
+                                   I=None, O=None, error=f"{type(exc).__name__}: {exc}"))
+    arrivals = []
+    for n, rate, seed in STREAM_ARRIVALS:
+        trace = [hs.Request(f"r{k}", 1, 1, 1) for k in range(n)]
+        arrivals.append(dict(n=n, rate=H(rate), seed=seed, t=[H(t) for _, t in hs.generate_arrivals(trace, rate, seed)]))
+    preds = []
+    for n, mean, sd, seed, cap in STREAM_PREDICTORS:
+        pr = hs.OutputLengthPredictor(hs.PredictorConfig(mode="normal", mean=mean, stddev=sd, seed=seed), cap)
+        preds.append(dict(n=n, mean=H(mean), stddev=H(sd), seed=seed, cap=cap,
+                          p=[pr.predict(hs.Request(f"r{k}", 1, 7, 7)) for k in range(n)]))
+    return dict(traces=traces, arrivals=arrivals, predictors=preds)
+
+
 def main() -> None:
-    which = sys.argv[1:] or ["exp", "search", "replay", "static", "wide"]
+    which = sys.argv[1:] or ["exp", "search", "replay", "static", "wide", "streams"]
     if "exp" in which:
         (OUT / "exp_vectors.json").write_text(json.dumps(build_exp_vectors()))
     if "search" in which:
@@ -426,6 +474,8 @@ def main() -> None:
         (OUT / "static_cases.json").write_text(json.dumps(build_static_cases()))
     if "wide" in which:
         (OUT / "wide_cases.json").write_text(json.dumps(build_wide_cases()))
+    if "streams" in which:
+        (OUT / "stream_cases.json").write_text(json.dumps(build_stream_cases()))
 
 
 if __name__ == "__main__":

@@ -1,0 +1,163 @@
+"""Device-drawn numpy streams (rng.cu) vs the reference's own draws
+(tests/golden/stream_cases.json) and vs the C oracle, bit-exact; and the
+seeded replay (hs_replay_seeded) vs the replay of host-drawn inputs."""
+
+import json
+import math
+import pathlib
+
+import numpy as np
+import pytest
+
+import paper_2504_15303_b200 as hs
+from oracle import hs_oracle as orc
+from paper_2504_15303_b200 import _native as nat
+from paper_2504_15303_b200 import streams
+from paper_2504_15303_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.loads((pathlib.Path(__file__).parent / "golden" / "stream_cases.json").read_text())
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return nat.engine_for(0)
+
+
+@pytest.mark.parametrize("case", GOLD["traces"], ids=lambda c: f"seed{c['seed']}-{c['input_dist']}")
+def test_gen_trace_golden(eng, case):
+    args = (case["count"], case["input_dist"], case["output_dist"], case["max_in"], case["max_out"])
+    if case["error"]:
+        with pytest.raises(OverflowError, match="cannot convert float infinity to integer"):
+            streams.gen_trace_lengths([case["seed"]], *args, engine=eng)
+        return
+    I, O = streams.gen_trace_lengths([case["seed"]], *args, engine=eng)
+    assert I.tolist() == case["I"] and O.tolist() == case["O"]
+
+
+@pytest.mark.parametrize("case", GOLD["arrivals"], ids=lambda c: f"n{c['n']}")
+def test_arrivals_golden(eng, case):
+    T = streams.arrival_times([case["seed"]], [case["n"]], float.fromhex(case["rate"]), engine=eng)
+    assert [t.hex() for t in T.tolist()] == case["t"]
+
+
+@pytest.mark.parametrize("case", GOLD["predictors"], ids=lambda c: f"n{c['n']}")
+def test_predictor_golden(eng, case):
+    P = streams.predict_lengths([case["seed"]], [case["n"]], float.fromhex(case["mean"]),
+                                float.fromhex(case["stddev"]), case["cap"], engine=eng)
+    assert P.tolist() == case["p"]
+
+
+def _oracle(seeds, counts, dists):
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    st = np.concatenate([orc.numpy_state(s) for s in seeds])
+    outs, bad = orc.rng_generate(st, off, dists)
+    return outs, bad, st
+
+
+@pytest.mark.parametrize("kinds", ["lognormal", "uniform32", "uniform64", "normal", "expsum", "mixed"])
+def test_ragged_batch_vs_oracle(eng, kinds):
+    """200 ragged streams (incl. empty and length-1 ones) with the final
+    generator states compared too (continuation semantics)."""
+    rng = np.random.default_rng(17)
+    counts = [int(x) for x in rng.integers(0, 6000, 200)]
+    counts[3], counts[4], counts[5] = 0, 1, 33
+    seeds = [int(s) for s in rng.integers(0, 2**40, 200)]
+    mu = math.log(200) - 0.18
+    D = {
+        "lognormal": [nat.hs_dist(nat.DIST_LOGNORMAL_LEN, 4096, 0, 0, mu, 0.6),
+                      nat.hs_dist(nat.DIST_LOGNORMAL_LEN, 2048, 0, 0, math.log(1000) - 2.0, 2.0)],
+        "uniform32": [nat.hs_dist(nat.DIST_UNIFORM_LEN, 4096, 1, 4096, 0, 0),
+                      nat.hs_dist(nat.DIST_UNIFORM_LEN, 50, 3, 2**31 + 5, 0, 0)],
+        "uniform64": [nat.hs_dist(nat.DIST_UNIFORM_LEN, 2**31 - 1, 1, 2**32, 0, 0),
+                      nat.hs_dist(nat.DIST_UNIFORM_LEN, 2**31 - 1, 9, 2**50 + 3, 0, 0)],
+        "normal": [nat.hs_dist(nat.DIST_NORMAL_LEN, 4096, 0, 0, 150.0, 60.0),
+                   nat.hs_dist(nat.DIST_NORMAL_LEN, 16, 0, 0, 3.0, 40.0)],
+        "expsum": [nat.hs_dist(nat.DIST_EXP_CUMSUM, 0, 0, 0, 1.0 / 140.0, 0),
+                   nat.hs_dist(nat.DIST_EXP_CUMSUM, 0, 0, 0, 2.0, 0)],
+        "mixed": [nat.hs_dist(nat.DIST_UNIFORM_LEN, 4096, 1, 77, 0, 0),
+                  nat.hs_dist(nat.DIST_LOGNORMAL_LEN, 4096, 0, 0, mu, 0.6),
+                  nat.hs_dist(nat.DIST_UNIFORM_LEN, 4096, 1, 5, 0, 0),
+                  nat.hs_dist(nat.DIST_EXP_CUMSUM, 0, 0, 0, 0.01, 0)],
+    }[kinds]
+    want, wbad, wst = _oracle(seeds, counts, D)
+    st = nat.pcg64_states(seeds)
+    out = streams._generate(seeds, counts, D, engine=eng, states=st)
+    try:
+        got = out.to_host()
+    finally:
+        out.close()
+    for g, w in zip(got, want):
+        assert g.dtype == w.dtype and np.array_equal(g.view(np.uint8), w.view(np.uint8))
+    assert st.tobytes() == wst.tobytes()
+    assert np.array_equal(out.bad, wbad)
+
+
+def test_config4_scale_streams_vs_numpy(eng):
+    """Full-size streams (1e5 requests) for a few traces of the bench
+    workload, straight against numpy (workloads.py helpers)."""
+    q = wl.CONFIG4_Q
+    seeds = [0, 1, 4095]
+    I, O = streams.gen_trace_lengths(seeds, q, "lognormal:200:0.6", "lognormal:150:0.6", 4096, 4096, engine=eng)
+    T = streams.arrival_times([42 + s for s in seeds], [q] * 3, wl.CONFIG4_RATE, engine=eng)
+    for k, s in enumerate(seeds):
+        i, o = wl.trace_lengths(q, seed=s)
+        assert np.array_equal(I[k * q:(k + 1) * q], i) and np.array_equal(O[k * q:(k + 1) * q], o)
+        assert np.array_equal(T[k * q:(k + 1) * q], wl.arrivals(q, wl.CONFIG4_RATE, seed=42 + s))
+
+
+def _config4():
+    prof = wl.config4()
+    cluster = hs.ClusterSpec(hs.ModelSpec(**prof.model), hs.EngineOverheads(**prof.engine),
+                             tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+                             hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {a: 1 for a in wl.CONFIG4_TYPES})
+    return cluster, params, config
+
+
+@pytest.mark.parametrize("policy", ["OS", "MB"])
+def test_seeded_replay_equals_host_drawn_replay(eng, policy):
+    """hs_replay_seeded (arrivals + normal predictions drawn on the device,
+    per chunk) gives exactly the replay of the same draws made by numpy."""
+    cluster, params, config = _config4()
+    rng = np.random.default_rng(3)
+    lens = [int(x) for x in rng.integers(0, 3000, 40)]
+    lens[7] = 0
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    I = np.concatenate([wl.trace_lengths(q, seed=50 + t)[0] for t, q in enumerate(lens)])
+    O = np.concatenate([wl.trace_lengths(q, seed=50 + t)[1] for t, q in enumerate(lens)])
+    aseeds = [900 + t for t in range(len(lens))]
+    pseeds = [700 + t for t in range(len(lens))]
+    pc = hs.PredictorConfig(mode="normal", mean=150.0, stddev=60.0, seed=0)
+    pol = hs.PolicyConfig(policy=policy, theta=2.0, predictor=pc)
+    T = np.concatenate([wl.arrivals(q, 140.0, seed=s) for q, s in zip(lens, aseeds)])
+    P = np.concatenate([wl.predictions(O[off[t]:off[t + 1]], "normal", 150.0, 60.0, seed=s) for t, s in
+                        enumerate(pseeds)])
+    want = hs.replay_traces(cluster, config, params, pol, off, I, O, P, arrival=T, want_assign=True,
+                            want_depart=True, engine=eng)
+    got = hs.replay_traces(cluster, config, params, pol, off, I, O, None, want_assign=True, want_depart=True,
+                           engine=eng, rate=140.0, arrival_seeds=aseeds, predictor_seeds=pseeds)
+    assert (want.result["error"] == 0).all()
+    assert np.array_equal(got.assign, want.assign)
+    assert np.array_equal(got.depart.view(np.uint64), want.depart.view(np.uint64))
+    assert got.metrics.tobytes() == want.metrics.tobytes()
+    assert got.result.tobytes() == want.result.tobytes()
+
+
+def test_seeded_replay_rate_inf_draws_nothing(eng):
+    cluster, params, config = _config4()
+    I, O = wl.trace_lengths(500, seed=1)
+    off = np.array([0, 500], np.int64)
+    pol = hs.PolicyConfig()
+    a = hs.replay_traces(cluster, config, params, pol, off, I, O, O, arrival=None, want_depart=True, engine=eng)
+    b = hs.replay_traces(cluster, config, params, pol, off, I, O, O, want_depart=True, engine=eng, rate=math.inf,
+                         arrival_seeds=[5])
+    assert np.array_equal(a.depart, b.depart) and np.array_equal(a.assign, b.assign)
+
+
+def test_device_stream_launches_counted(eng):
+    n0 = eng.launch_count
+    streams.arrival_times([1, 2, 3], [10, 0, 5], 3.0, engine=eng)
+    assert eng.launch_count == n0 + 1

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(nat.EXPORTS) == declared
-    assert lib.hs_abi_version() == 2
+    assert lib.hs_abi_version() == 3
 
 
 def test_no_cuda_means_engine_unavailable_not_fallback():
@@ -48,6 +48,9 @@ def test_struct_layouts_match_header():
     assert C.sizeof(nat.hs_trace_result) == nat.RESULT_DTYPE.itemsize == 32
     assert C.sizeof(nat.hs_instance) == 88
     assert C.sizeof(nat.hs_machine) == 24
+    assert C.sizeof(nat.hs_pcg64_state) == nat.PCG64_DTYPE.itemsize == 40
+    assert C.sizeof(nat.hs_dist) == 40
+    assert C.sizeof(nat.hs_replay_seeds) == 48
 
 
 def test_domain_known_answers():
