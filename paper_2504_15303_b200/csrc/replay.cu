@@ -45,7 +45,7 @@ namespace hs {
 #ifdef HS_TIMERS
 // Diagnostic build only (-DHS_TIMERS): per-warp cycle counts of the replay
 // phases, summed over the launch: [advance, price, evaluate, mapping, commit].
-__device__ unsigned long long g_timers[8];
+__device__ unsigned long long g_timers[16];
 // accumulated in registers (tacc[]) and flushed once per lane at kernel end
 #define HS_T0(v) long long v = clock64()
 #define HS_T1(slot, v) \
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   uint32_t n_steps = 0;
   int64_t rr_next = 0;
 #ifdef HS_TIMERS
-  unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tacc[16] = {};
 #endif
   int32_t t_err = HS_TRACE_OK, t_err_inst = -1;
   int64_t t_err_req = -1;
@@ -316,6 +316,10 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   auto event_step = [&]() {
     const double t = t_next;
     sched = false;
+#ifdef HS_TIMERS
+    tacc[14] += nact > kHS ? 1 : 0;
+    tacc[15] += nact;
+#endif
     ++n_steps;
 #ifdef HS_TIMERS
     tacc[7] += 1;
@@ -428,6 +432,10 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     if (max_dirty || cold.cnt_max <= 0) {  // the last holder of the max retired: rescan
       int64_t m = INT64_MIN;
       int32_t cm = 0;
+#ifdef HS_TIMERS
+      tacc[10] += 1;
+      tacc[11] += nact;
+#endif
       for (int32_t h = 0; h < nact; ++h) {
         const int64_t mk = heap.get(h, nact).mk;
         if (mk > m) {
@@ -463,6 +471,10 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
     for (;;) {
       const bool want = valid && sched && (drain || t_next < t_limit) && !lerr;
       if (!__any_sync(FULL, want)) break;
+#ifdef HS_TIMERS
+      tacc[8] += 1;
+      tacc[12] += __popc(__ballot_sync(FULL, want && !(blocked && k < kr)));
+#endif
       // phase 1: lanes whose next step is an event (retirement due, or an
       // admission may succeed)
 
@@ -479,35 +491,47 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       const bool pure = valid && sched && !lerr && blocked && k < kr && (drain || t_next < t_limit);
       if (pure) {
         const uint32_t k0 = k;
+        // decode price of a step with cached length x (latency.py:95-97)
+        auto price = [&](double x) { return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, x), B), __dmul_rn(p7, x)), p8); };
+        // Blocks of four steps, software-pipelined: the four prices of the
+        // next block (they depend only on the cached length) are computed
+        // while this block's four clock additions -- the only serial part,
+        // in the reference's rounding order -- run.  Exit predicates are
+        // evaluated off the chain; the state is taken at the first step that
+        // may not run (extra additions are discarded).
+        double c0 = price(cd), c1 = price(__dadd_rn(cd, 1.0)), c2 = price(__dadd_rn(cd, 2.0)),
+               c3 = price(__dadd_rn(cd, 3.0));
         for (;;) {
-          // four prices side by side (they depend only on the cached length),
-          // then the serial clock additions; the exit predicates are
-          // evaluated after the chain and the state is taken at the first
-          // step that may not run (extra additions are discarded).
-          const double cd1 = __dadd_rn(cd, 1.0), cd2 = __dadd_rn(cd, 2.0), cd3 = __dadd_rn(cd, 3.0);
-          const double c0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd), B), __dmul_rn(p7, cd)), p8);
-          const double c1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd1), B), __dmul_rn(p7, cd1)), p8);
-          const double c2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd2), B), __dmul_rn(p7, cd2)), p8);
-          const double c3 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd3), B), __dmul_rn(p7, cd3)), p8);
+#ifdef HS_TIMERS
+          if (lane == __ffs(__activemask()) - 1) tacc[9] += 1;
+          tacc[13] += 1;
+#endif
           const double t1 = __dadd_rn(t_next, c0);
           const double t2 = __dadd_rn(t1, c1);
           const double t3 = __dadd_rn(t2, c2);
           const double t4 = __dadd_rn(t3, c3);
+          const double cd4 = __dadd_rn(cd, 4.0);
+          const double n0 = price(cd4), n1 = price(__dadd_rn(cd, 5.0)), n2 = price(__dadd_rn(cd, 6.0)),
+                       n3 = price(__dadd_rn(cd, 7.0));
           // step i+1 runs iff step i ran, k+i < kr and t_i < lim
           const bool g1 = k + 1 < kr && (t1 < lim || drain);
           const bool g2 = g1 && k + 2 < kr && (t2 < lim || drain);
           const bool g3 = g2 && k + 3 < kr && (t3 < lim || drain);
-          if (!g3) {
-            const uint32_t n = 1u + (uint32_t)g1 + (uint32_t)g2;
-            t_next = g2 ? t3 : (g1 ? t2 : t1);
-            cd = g2 ? cd3 : (g1 ? cd2 : cd1);
+          const bool g4 = g3 && k + 4 < kr && (t4 < lim || drain);
+          if (!g4) {
+            const uint32_t n = 1u + (uint32_t)g1 + (uint32_t)g2 + (uint32_t)g3;
+            t_next = g3 ? t4 : (g2 ? t3 : (g1 ? t2 : t1));
+            cd = __dadd_rn(cd, (double)n);
             k += n;
             break;
           }
           t_next = t4;
-          cd = __dadd_rn(cd, 4.0);
+          cd = cd4;
           k += 4;
-          if (!(k < kr && (t_next < lim || drain))) break;
+          c0 = n0;
+          c1 = n1;
+          c2 = n2;
+          c3 = n3;
         }
         n_steps += k - k0;
       }
@@ -841,8 +865,8 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
 #ifdef HS_TIMERS
   // warp-level phases (slots 0-2, 6) were timed by every lane: count lane 0;
   // event-step parts (3-5, 7) are per lane
-  for (int sl = 0; sl < 8; ++sl) {
-    const bool warp_slot = sl <= 2 || sl == 6;
+  for (int sl = 0; sl < 16; ++sl) {
+    const bool warp_slot = sl <= 2 || sl == 6 || sl == 8 || sl == 12;
     if (!warp_slot || lane == 0) atomicAdd(&g_timers[sl], tacc[sl]);
   }
 #endif
@@ -944,9 +968,9 @@ cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, i
 // diagnostic export of the timers build (not part of the ABI header)
 extern "C" int hs_debug_timers(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
-  cudaError_t e = cudaMemcpyFromSymbol(out, hs::g_timers, sizeof(unsigned long long) * 8);
+  cudaError_t e = cudaMemcpyFromSymbol(out, hs::g_timers, sizeof(unsigned long long) * 16);
   if (reset) {
-    unsigned long long z[8] = {};
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(hs::g_timers, z, sizeof(z));
   }
   return e == cudaSuccess ? 0 : 1;

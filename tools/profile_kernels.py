@@ -63,7 +63,7 @@ def main():
         if hasattr(eng.lib, "hs_debug_timers"):
             import ctypes
             import numpy as np
-            buf = np.zeros(8, np.uint64)
+            buf = np.zeros(16, np.uint64)
             eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 1)
             eng.replay_device(inst, ps, T, d["off"], d["I"], d["O"], d["O"], d["T"], d["a"], d["m"], d["r"])
             eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 0)
@@ -73,6 +73,11 @@ def main():
             calls = max(int(buf[7]), 1)
             print("event_step calls per arrival:", calls / (T * q), " cycles per call: retire %.0f admit %.0f price %.0f"
                   % (buf[3] / calls, buf[4] / calls, buf[5] / calls))
+            n = T * q
+            print("per arrival: outer passes %.2f, lanes in event phase per pass %.2f, pure-block passes %.2f, "
+                  "lane pure blocks %.2f, rescans %.4f (mean len %.1f), event steps with nact>16: %.3f, mean nact %.1f"
+                  % (buf[8] / n, buf[12] / max(buf[8], 1), buf[9] / n, buf[13] / n, buf[10] / n,
+                     buf[11] / max(buf[10], 1), buf[14] / calls, buf[15] / calls))
     else:
         cluster, reqs, params, _I, _O = bench.search_inputs(10_000)
         t = planner.build_tables(cluster, reqs, params, engine=eng)
