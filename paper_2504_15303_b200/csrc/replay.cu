@@ -188,6 +188,16 @@ struct Cold {
   int32_t req_count, cnt_max, err, err_req;
 };
 
+// One instance class of the deployment, staged in shared memory once per
+// trace group: lanes read their class by index from shared memory instead of
+// the constant bank, where per-lane indices serialise (the compiler
+// rematerialises these values rather than keeping them in registers).
+struct TypeRec {
+  double p[8];
+  double budget;
+  int64_t cap_tok;  // floor(floor(budget) / per_token)
+};
+
 // Cross-warp exchange for traces spanning W > 1 warps: one slot per warp of
 // the trace group, a named barrier per group (ids 1..4).
 struct Xch {
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   __shared__ HEnt s_heap[kWarps * 32][kHS];
   __shared__ Xch s_x[G][W];
   __shared__ uint32_t s_steps[G];
-  extern __shared__ double s_cost[];  // [kWarps][32 * n_types]
+  extern __shared__ double s_cost[];  // [kWarps][32 * n_types] prices, then [G][n_types] TypeRec
   for (int k = threadIdx.x; k < 256; k += blockDim.x) s_tab[k] = kExpTab[k];
   if (threadIdx.x < G) s_steps[threadIdx.x] = 0;
   __syncthreads();
@@ -231,6 +241,16 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   const int64_t pt = c_rep.per_token;
   const double theta = c_rep.theta;
   double* cost = s_cost + (size_t)wib * 32 * NT;
+  TypeRec* types = reinterpret_cast<TypeRec*>(s_cost + (size_t)(W * G) * 32 * NT) + (size_t)g * NT;
+  for (int k = wsub * 32 + lane; k < NT * 10; k += W * 32) {
+    const int t = k / 10, f = k - t * 10;
+    double* dst = reinterpret_cast<double*>(types + t) + f;
+    if (f < 8) *dst = c_rep.type_p[t][f];
+    else if (f == 8) *dst = c_rep.type_budget[t];
+    else *reinterpret_cast<int64_t*>(dst) = c_rep.type_cap_tokens[t];
+  }
+  if (W > 1) group_bar(g, W * 32);
+  else __syncwarp();
   Cold& cold = s_cold[threadIdx.x];
   Xch* xg = s_x[g];
   // combine helper: every warp of the group publishes one slot, all read all
@@ -259,12 +279,13 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   const bool valid = jj < N;
   const int j = valid ? jj : 0;
   const int ty = c_rep.inst_type[j];
-  const double* tp = c_rep.type_p[ty];
-  const double budget = c_rep.type_budget[ty];
+  const TypeRec& trec = types[ty];
+  const double* tp = trec.p;
+  const double budget = trec.budget;
   const double p7 = tp[6], p8 = tp[7];
   const int64_t hbase = MULTI ? trace_heap[tr] : tr * c_rep.heap_stride;
   const Heap heap{s_heap[threadIdx.x], reinterpret_cast<HEnt*>(heap_all) + hbase + c_rep.heap_off[j]};
-  const int64_t cap_tok = c_rep.type_cap_tokens[ty];  // floor(floor(budget) / per_token)
+  const int64_t cap_tok = trec.cap_tok;  // floor(floor(budget) / per_token)
   const int32_t cap = (int32_t)(c_rep.heap_off[j + 1] - c_rep.heap_off[j]) + kHS;
 
   // hot per-lane state (registers)
@@ -591,10 +612,10 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
         const int64_t Ia = __shfl_sync(FULL, cI, srcl);
         const int64_t Pa = __shfl_sync(FULL, cP, srcl);
         if (pair < n_in * NT) {
-          const double fl = py_floordiv(c_rep.type_budget[tyk], i2d(pt * (Ia + Pa)));
+          const double fl = py_floordiv(types[tyk].budget, i2d(pt * (Ia + Pa)));
           int64_t b = (int64_t)fl;
           if (b < 1) b = 1;
-          const double* ctp = c_rep.type_p[tyk];
+          const double* ctp = types[tyk].p;
           const double tot = __dadd_rn(prefill_time(ctp, b, Ia), decode_time(ctp, b, Ia, Pa));
           cost[pair] = (tot <= 0.0) ? -1.0 : __ddiv_rn(tot, i2d(b));
         }
@@ -906,7 +927,7 @@ cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
                      const int64_t* d_trace_heap, int n_max, int max_types) {
   constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);
   const int warps = W * G;
-  const size_t smem = (size_t)warps * 32 * max_types * sizeof(double);
+  const size_t smem = (size_t)warps * 32 * max_types * sizeof(double) + (size_t)G * max_types * sizeof(TypeRec);
   // static (heaps, per-lane state) + dynamic (price buffer) may exceed the
   // 48 KB default: opt in for the dynamic part every time
   cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
