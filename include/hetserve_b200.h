@@ -329,6 +329,46 @@ int hs_pcg64_seed_u64(const uint64_t* seeds, int64_t n, hs_pcg64_state* out);
 int hs_rng_generate(hs_ctx* ctx, hs_pcg64_state* states, int32_t n_streams, const int64_t* offsets,
                     const hs_dist* dists, int32_t n_dists, void* const* out, int64_t* bad_index);
 
+/* ---- live scheduler (the gateway's per-request path) -------------------
+ * Replaces scheduling.py:175-346 Scheduler on the host: evaluate / choose /
+ * complete / snapshot with the reference's arithmetic (CPython float //,
+ * sum(), glibc exp), checks and state transitions, the in-flight table keyed
+ * by the request id, one mutex (the reference's _lock), and an O(N) min-max
+ * (scheduling.py:299-312 is O(N^2)).  instances[j]: p, budget, wrr_weight;
+ * policy: policy, theta, per_token.  allowed: NULL = all, else n bytes. */
+typedef struct hs_scheduler hs_scheduler;
+
+typedef enum {
+  HS_SCHED_OK = 0,
+  HS_SCHED_NO_INSTANCE = 1,       /* SchedulingError("no instance available for scheduling")       */
+  HS_SCHED_ALREADY_IN_FLIGHT = 2, /* SchedulingError("request ... is already in flight")           */
+  HS_SCHED_NOT_IN_FLIGHT = 3,     /* SchedulingError("request ... is not in flight (double ...)")  */
+  HS_SCHED_NONPOSITIVE_COST = 4,  /* SpecError("non-positive batch time ...")  (value = the total) */
+  HS_SCHED_EXP_OVERFLOW = 5,      /* OverflowError("math range error")                              */
+  HS_SCHED_NEGATIVE_RUNNING = 6,  /* SpecError("running token sums went negative; ...")            */
+  HS_SCHED_ZERO_DIVISION = 7      /* ZeroDivisionError("float floor division by zero")             */
+} hs_sched_error;
+
+typedef struct {
+  int32_t error;    /* hs_sched_error */
+  int32_t instance; /* instance the error arose on, or -1 */
+  double value;
+} hs_sched_status;
+
+int hs_sched_create(const hs_instance* instances, int32_t n, const hs_policy* policy, hs_scheduler** out);
+int hs_sched_destroy(hs_scheduler* s);
+/* Scheduler.evaluate: weights[n] (+inf where not allowed); no state change. */
+int hs_sched_evaluate(hs_scheduler* s, int64_t input_len, int64_t predicted_output_len, const uint8_t* allowed,
+                      double* weights, hs_sched_status* status);
+/* Scheduler.choose: *chosen = instance index, dispatch bookkeeping committed. */
+int hs_sched_choose(hs_scheduler* s, const char* request_id, int32_t id_len, int64_t input_len,
+                    int64_t predicted_output_len, const uint8_t* allowed, int32_t* chosen, hs_sched_status* status);
+/* Scheduler.complete: subtracts exactly what choose recorded. */
+int hs_sched_complete(hs_scheduler* s, const char* request_id, int32_t id_len, hs_sched_status* status);
+/* Scheduler.snapshot / loads / running_totals (any pointer may be NULL). */
+int hs_sched_snapshot(hs_scheduler* s, double* loads, int64_t* running_totals, double* kv_usage, int64_t* oversized,
+                      int64_t* in_flight);
+
 /* Device buffers for hs_replay_device. */
 int hs_device_alloc(hs_ctx* ctx, int64_t bytes, void** out);
 int hs_device_free(hs_ctx* ctx, void* ptr);

@@ -56,7 +56,7 @@ from .planner import (
     search_optimal_config,
     search_topk,
 )
-from .scheduling import POLICIES, InstanceHandle, OutputLengthPredictor, PolicyConfig, PredictorConfig
+from .scheduling import POLICIES, InstanceHandle, OutputLengthPredictor, PolicyConfig, PredictorConfig, Scheduler
 from .simulator import (
     InstanceMetrics,
     ReplayBatchResult,

@@ -110,6 +110,14 @@ class hs_replay_seeds(C.Structure):
 
 DIST_LOGNORMAL_LEN, DIST_UNIFORM_LEN, DIST_EXP_CUMSUM, DIST_NORMAL_LEN = 0, 1, 2, 3
 
+
+class hs_sched_status(C.Structure):
+    _fields_ = [("error", C.c_int32), ("instance", C.c_int32), ("value", C.c_double)]
+
+
+(SCHED_OK, SCHED_NO_INSTANCE, SCHED_ALREADY_IN_FLIGHT, SCHED_NOT_IN_FLIGHT, SCHED_NONPOSITIVE_COST,
+ SCHED_EXP_OVERFLOW, SCHED_NEGATIVE_RUNNING, SCHED_ZERO_DIVISION) = range(8)
+
 # numpy views of the structs (same layout) for bulk results
 ENTRY_DTYPE = np.dtype([("contribution", "<f8"), ("rate", "<f8"), ("budget", "<f8"), ("slack", "<f8"),
                         ("instance_count", "<i8"), ("bad_request", "<i8"), ("token_count", "<i8"),
@@ -130,6 +138,8 @@ EXPORTS = (
     "hs_replay_device", "hs_device_alloc", "hs_device_free", "hs_memcpy_h2d", "hs_memcpy_d2h",
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
     "hs_replay_seeded", "hs_pcg64_seed", "hs_pcg64_seed_u64", "hs_rng_generate",
+    "hs_sched_create", "hs_sched_destroy", "hs_sched_evaluate", "hs_sched_choose", "hs_sched_complete",
+    "hs_sched_snapshot",
 )
 
 _lib = None
@@ -173,6 +183,12 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_replay_seeded": ([vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
             "hs_pcg64_seed": ([vp, i32, vp], C.c_int),
             "hs_pcg64_seed_u64": ([vp, i64, vp], C.c_int),
+            "hs_sched_create": ([vp, i32, vp, vp], C.c_int),
+            "hs_sched_destroy": ([vp], C.c_int),
+            "hs_sched_evaluate": ([vp, i64, i64, vp, vp, vp], C.c_int),
+            "hs_sched_choose": ([vp, C.c_char_p, i32, i64, i64, vp, vp, vp], C.c_int),
+            "hs_sched_complete": ([vp, C.c_char_p, i32, vp], C.c_int),
+            "hs_sched_snapshot": ([vp, vp, vp, vp, vp, vp], C.c_int),
             "hs_rng_generate": ([vp, vp, i32, vp, vp, i32, vp, vp], C.c_int),
         }
         for name, (args, res) in sig.items():

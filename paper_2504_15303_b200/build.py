@@ -19,7 +19,7 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhetserve_b200.so"
-SOURCES = ["capi.cu", "search.cu", "replay.cu", "topk.cu", "rng.cu"]
+SOURCES = ["capi.cu", "search.cu", "replay.cu", "topk.cu", "rng.cu", "scheduler.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,7 +36,7 @@ def build(verbose: bool = False, force: bool = False, timers: bool = False) -> p
     deps.append(PKG.parent / "include" / "hetserve_b200.h")
     if not force and lib.exists() and all(lib.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return lib
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off",
            "-Xptxas", "-v" if verbose else "-O3", "-cudart", "static", *(["-DHS_TIMERS"] if timers else []), "-o", str(lib) + ".tmp",
            *[str(CSRC / s) for s in SOURCES]]
     if verbose:

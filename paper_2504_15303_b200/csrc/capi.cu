@@ -57,6 +57,8 @@ struct hs_ctx {
 };
 
 namespace hs {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+
 int sm_count() {
   int dev = 0, n = 148;
   cudaGetDevice(&dev);

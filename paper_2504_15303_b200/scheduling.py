@@ -1,21 +1,28 @@
-"""Scheduler configuration types of the drop-in API.
+"""Scheduler types of the drop-in API, and the live scheduler.
 
-The scheduling decisions themselves run on the GPU inside the replay kernel
+Replayed traces are scheduled on the GPU inside the replay kernel
 (csrc/replay.cu).  This module keeps the reference's configuration surface
 (/root/reference/pkg/src/hetserve/scheduling.py:41-116): the policy record,
 the output-length predictor and the instance handle.  The predictor is
 evaluated host-side for a whole trace at once; its draws equal the
 reference's one-draw-per-dispatch stream because dispatch order is trace
 order and numpy's Generator produces the same sequence in bulk.
+
+``Scheduler`` (scheduling.py:175-346) is the live, per-request scheduler the
+reference's gateway calls; it runs natively (csrc/scheduler.cpp, hs_sched_*
+in include/hetserve_b200.h) with the reference's checks, messages and
+arithmetic and an O(N) min-max.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from .domain import KvBudget, LatencyParams, SpecError
+from .domain import KvBudget, LatencyParams, SchedulingError, SpecError, kv_bytes_per_token
 
 POLICIES = ("OS", "RR", "WRR", "SI", "MB")
 
@@ -89,3 +96,153 @@ class OutputLengthPredictor:
         else:
             v = np.rint(self._rng.normal(self._config.mean, self._config.stddev, size=n))
         return np.clip(v, 1, self._max_output_len).astype(np.int64)
+
+
+class Scheduler:
+    """scheduling.py:175-346 Scheduler over the native hs_sched_* engine:
+    choose() / complete() / evaluate() / snapshot() with the reference's
+    semantics; thread-safe (one native mutex, as the reference's _lock)."""
+
+    def __init__(self, instances: list, model, policy: PolicyConfig | None = None):
+        from . import _native as nat
+        if not instances:
+            raise SchedulingError("scheduler needs at least one instance")
+        policy = policy or PolicyConfig()
+        if policy.policy == "WRR" and len(policy.wrr_weights) != len(instances):
+            raise SpecError(
+                f"WRR needs one weight per instance ({len(instances)}), got {len(policy.wrr_weights)}"
+            )
+        for handle in instances:
+            if handle.budget.total_bytes <= 0:
+                raise SpecError(f"instance {handle.id!r} has a non-positive KV budget")
+        self._nat = nat
+        self._lib = nat.load_library()
+        self._handles = list(instances)
+        self._model = model
+        self._policy = policy
+        self._n = len(instances)
+        arr = (nat.hs_instance * self._n)()
+        for j, h in enumerate(instances):
+            p = h.params
+            for k, name in enumerate(("p1", "p2", "p3", "p4", "p5", "p6", "p7", "p8")):
+                arr[j].p[k] = float(getattr(p, name))
+            arr[j].budget = float(h.budget.total_bytes)
+            arr[j].wrr_weight = float(policy.wrr_weights[j]) if policy.policy == "WRR" else 0.0
+        pol = nat.hs_policy(nat.POLICY_CODE[policy.policy], self._n, float(policy.theta),
+                            int(kv_bytes_per_token(model)), 0, 0)
+        h = C.c_void_p()
+        rc = self._lib.hs_sched_create(C.cast(arr, C.c_void_p), self._n, C.byref(pol), C.byref(h))
+        if rc != nat.HS_OK:
+            raise nat.EngineError(rc, "hs_sched_create: " + (self._lib.hs_last_error() or b"").decode())
+        self._h = h
+        self._st = nat.hs_sched_status()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.hs_sched_destroy(h)
+            self._h = None
+
+    @property
+    def instances(self) -> list:
+        return list(self._handles)
+
+    @property
+    def policy(self) -> PolicyConfig:
+        return self._policy
+
+    # ------------------------------------------------------------ internals
+    def _allowed(self, allowed):
+        if allowed is None:
+            return None
+        a = (C.c_uint8 * self._n)()
+        for i in allowed:
+            if isinstance(i, int) and 0 <= i < self._n:
+                a[i] = 1
+        return a
+
+    def _raise(self, st, request=None, request_id=None):
+        nat = self._nat
+        code = st.error
+        if code == nat.SCHED_OK:
+            return
+        if code == nat.SCHED_NO_INSTANCE:
+            raise SchedulingError("no instance available for scheduling")
+        if code == nat.SCHED_ALREADY_IN_FLIGHT:
+            raise SchedulingError(f"request {request.id!r} is already in flight")
+        if code == nat.SCHED_NOT_IN_FLIGHT:
+            raise SchedulingError(f"request {request_id!r} is not in flight (double completion?)")
+        if code == nat.SCHED_NONPOSITIVE_COST:
+            raise SpecError(
+                f"non-positive batch time {st.value} for request {request.id!r}; latency parameters are corrupt"
+            )
+        if code == nat.SCHED_EXP_OVERFLOW:
+            raise OverflowError("math range error")
+        if code == nat.SCHED_NEGATIVE_RUNNING:
+            raise SpecError("running token sums went negative; completion applied twice?")
+        if code == nat.SCHED_ZERO_DIVISION:
+            raise ZeroDivisionError("float floor division by zero")
+        raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"scheduler status {code}")
+
+    # ------------------------------------------------------------------ API
+    def evaluate(self, request, allowed: set | None = None) -> list:
+        """Per-instance workload of this request (no state change)."""
+        w = (C.c_double * self._n)()
+        st = self._nat.hs_sched_status()
+        rc = self._lib.hs_sched_evaluate(self._h, int(request.input_len), int(request.predicted_output_len),
+                                         self._allowed(allowed), w, C.byref(st))
+        if rc != self._nat.HS_OK:
+            raise self._nat.EngineError(rc, "hs_sched_evaluate: " + (self._lib.hs_last_error() or b"").decode())
+        self._raise(st, request=request)
+        return list(w)
+
+    def choose(self, request, allowed: set | None = None) -> int:
+        """Pick an instance for the request and commit the dispatch bookkeeping."""
+        rid = str(request.id).encode("utf-8", "surrogatepass")
+        out = C.c_int32()
+        st = self._nat.hs_sched_status()
+        rc = self._lib.hs_sched_choose(self._h, rid, len(rid), int(request.input_len),
+                                       int(request.predicted_output_len), self._allowed(allowed), C.byref(out),
+                                       C.byref(st))
+        if rc != self._nat.HS_OK:
+            raise self._nat.EngineError(rc, "hs_sched_choose: " + (self._lib.hs_last_error() or b"").decode())
+        self._raise(st, request=request)
+        return int(out.value)
+
+    def complete(self, request_id: str) -> None:
+        """Fire the completion hook: subtract exactly what dispatch recorded."""
+        rid = str(request_id).encode("utf-8", "surrogatepass")
+        st = self._nat.hs_sched_status()
+        rc = self._lib.hs_sched_complete(self._h, rid, len(rid), C.byref(st))
+        if rc != self._nat.HS_OK:
+            raise self._nat.EngineError(rc, "hs_sched_complete: " + (self._lib.hs_last_error() or b"").decode())
+        self._raise(st, request_id=request_id)
+
+    def _snap(self):
+        n = self._n
+        loads, usage = (C.c_double * n)(), (C.c_double * n)()
+        running, over = (C.c_int64 * n)(), (C.c_int64 * n)()
+        inflight = C.c_int64()
+        self._lib.hs_sched_snapshot(self._h, loads, running, usage, over, C.byref(inflight))
+        return list(loads), list(running), list(usage), list(over), int(inflight.value)
+
+    def in_flight_count(self) -> int:
+        return self._snap()[4]
+
+    def snapshot(self) -> dict:
+        """Consistent view of loads, KV usage, and in-flight work per instance."""
+        loads, running, usage, over, inflight = self._snap()
+        ids = [h.id for h in self._handles]
+        return {
+            "loads": dict(zip(ids, loads)),
+            "kv_usage": dict(zip(ids, usage)),
+            "running_tokens": dict(zip(ids, running)),
+            "oversized": dict(zip(ids, over)),
+            "in_flight": inflight,
+        }
+
+    def loads(self) -> list:
+        return self._snap()[0]
+
+    def running_totals(self) -> list:
+        return self._snap()[1]

@@ -462,8 +462,98 @@ def build_stream_cases() -> dict:
     return dict(traces=traces, arrivals=arrivals, predictors=preds)
 
 
+def _sched_snapshot(sch) -> dict:
+    snap = sch.snapshot()
+    return {"loads": [H(v) for v in snap["loads"].values()], "kv_usage": [H(v) for v in snap["kv_usage"].values()],
+            "running": list(snap["running_tokens"].values()), "oversized": list(snap["oversized"].values()),
+            "in_flight": snap["in_flight"]}
+
+
+def sched_case(name, profile, degrees, policy, n_ops, seed, max_len=2000, allowed_p=0.3, complete_p=0.3,
+               evaluate_p=0.1, dup_p=0.03, bogus_p=0.03) -> dict:
+    """A seeded sequence of Scheduler.choose / complete / evaluate calls on
+    the reference's live scheduler (scheduling.py:175-346), recording every
+    result or exception and the snapshot after each call."""
+    cluster, params = ref_cluster(profile), ref_params(profile)
+    cfg = hs.deployment_for(cluster.machines, degrees)
+    handles = hs.build_instances(cluster, cfg, params)
+    n = len(handles)
+    if policy.get("wrr") == "auto":
+        policy = dict(policy, wrr=[1 + (7 * j) % 5 for j in range(n)])
+    pol = hs.PolicyConfig(policy=policy["policy"], theta=policy.get("theta", 2.0),
+                          wrr_weights=tuple(policy["wrr"]) if policy.get("wrr") else None)
+    sch = hs.Scheduler(handles, cluster.model, pol)
+    rng = random.Random(seed)
+    ops, live, next_id = [], [], 0
+    for _ in range(n_ops):
+        u = rng.random()
+        allowed = None
+        if rng.random() < allowed_p:
+            allowed = sorted(rng.sample(range(n + 2), rng.randint(0, min(n + 2, 4))))
+        if u < complete_p and (live or rng.random() < bogus_p * 10):
+            if live and rng.random() > bogus_p:
+                rid = live.pop(rng.randrange(len(live)))
+            else:
+                rid = f"ghost{next_id}"
+            op = {"op": "complete", "id": rid}
+            try:
+                sch.complete(rid)
+            except (hs.HetserveError, OverflowError, ZeroDivisionError) as exc:
+                op["error"], op["msg"] = type(exc).__name__, str(exc)
+        else:
+            if rng.random() < dup_p and live:
+                rid = rng.choice(live)
+            else:
+                rid = f"r{next_id}"
+                next_id += 1
+            I = rng.randint(1, max_len)
+            P = rng.randint(1, max_len)
+            req = hs.Request(rid, I, P, P)
+            kind = "evaluate" if u > 1.0 - evaluate_p else "choose"
+            op = {"op": kind, "id": rid, "I": I, "P": P, "allowed": allowed}
+            try:
+                if kind == "choose":
+                    op["chosen"] = sch.choose(req, set(allowed) if allowed is not None else None)
+                    live.append(rid)
+                else:
+                    op["weights"] = [H(w) for w in sch.evaluate(req, set(allowed) if allowed is not None else None)]
+            except (hs.HetserveError, OverflowError, ZeroDivisionError) as exc:
+                op["error"], op["msg"] = type(exc).__name__, str(exc)
+        op["snap"] = _sched_snapshot(sch)
+        ops.append(op)
+    return {"name": name, "profile": profile_desc(profile), "degrees": degrees, "policy": policy, "ops": ops}
+
+
+def build_sched_cases() -> list:
+    cases = []
+    p2 = wl.config2()
+    deg2 = {"v100": 2, "a800": 1, "h100": 1}
+    for pol in ({"policy": "OS"}, {"policy": "MB"}, {"policy": "RR"}, {"policy": "SI"},
+                {"policy": "WRR", "wrr": "auto"}, {"policy": "OS", "theta": 0.7}):
+        cases.append(sched_case(f"config2-{pol['policy']}-{pol.get('theta', 2.0)}", p2, deg2, pol, 400,
+                                seed=len(cases)))
+    p4 = wl.config4()
+    cases.append(sched_case("config4-OS", p4, {a: 1 for a in wl.CONFIG4_TYPES}, {"policy": "OS"}, 600, seed=77,
+                            max_len=4000))
+    # tiny budgets: oversized requests, exp overflow at high KV pressure, negative decode prices
+    tiny = tiny_profile([("a", 2, 30_000, "x"), ("b", 1, 40_000, "y")],
+                        params={("a", 1): (1e-5, 1e-4, 1e-5, 1e-3, 1e-6, 1e-4, 1e-7, 1e-4),
+                                ("a", 2): (1e-5, 1e-4, 1e-5, 1e-3, 1e-6, 1e-4, 1e-7, 1e-4),
+                                ("b", 1): (2e-5, 2e-4, 2e-5, 2e-3, 2e-6, 2e-4, 2e-7, 2e-4)})
+    cases.append(sched_case("tiny-OS-theta40", tiny, {"a": 1, "b": 1}, {"policy": "OS", "theta": 40.0}, 200, seed=5,
+                            max_len=900, complete_p=0.15))
+    cases.append(sched_case("tiny-MB-theta40", tiny, {"a": 1, "b": 1}, {"policy": "MB", "theta": 40.0}, 200, seed=8,
+                            max_len=900, complete_p=0.15))
+    neg = tiny_profile([("a", 1, 2_000_000, "x"), ("b", 1, 3_000_000, "y")],
+                       params={("a", 1): (1e-5, 1e-4, 1e-5, 1e-3, 1e-6, 1e-4, 1e-7, 1e-4),
+                               ("b", 1): (-1e-3, -1e-2, -1e-3, -1e-1, 1e-6, 1e-4, 1e-7, 1e-4)})
+    cases.append(sched_case("tiny-negative-RR", neg, {"a": 1, "b": 1}, {"policy": "RR"}, 60, seed=6, max_len=50))
+    cases.append(sched_case("tiny-negative-OS", neg, {"a": 1, "b": 1}, {"policy": "OS"}, 60, seed=7, max_len=50))
+    return cases
+
+
 def main() -> None:
-    which = sys.argv[1:] or ["exp", "search", "replay", "static", "wide", "streams"]
+    which = sys.argv[1:] or ["exp", "search", "replay", "static", "wide", "streams", "sched"]
     if "exp" in which:
         (OUT / "exp_vectors.json").write_text(json.dumps(build_exp_vectors()))
     if "search" in which:
@@ -476,6 +566,8 @@ def main() -> None:
         (OUT / "wide_cases.json").write_text(json.dumps(build_wide_cases()))
     if "streams" in which:
         (OUT / "stream_cases.json").write_text(json.dumps(build_stream_cases()))
+    if "sched" in which:
+        (OUT / "sched_cases.json").write_text(json.dumps(build_sched_cases()))
 
 
 if __name__ == "__main__":
