@@ -34,7 +34,7 @@
 // pass into shared memory; the state-dependent factor exp(theta * usage)
 // (capacity.py:98-106, scheduling.py:150-154) is cached per lane and
 // recomputed only after the lane's running tokens change.  The min-max
-// mapping (scheduling.py:299-312) is O(log N): top-2 of the loads and an
+// mapping (scheduling.py:299-312) is O(log N): the max of the loads and an
 // argmin of peaks via REDUX on order-preserving 64-bit keys.
 #include "hs_device.cuh"
 #include "hs_internal.h"
@@ -719,34 +719,22 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
         break;
       }
       if (eval_all) {
-        // _min_max_choice (scheduling.py:299-312):
-        // peak_s = max(L_s + w_s, max_{j != s} L_j), argmin with lowest index
-        const uint64_t lk = valid ? okey(load) : 0ull;
-        uint64_t m1 = warp_max_u64(lk);
-        const unsigned at_max = __ballot_sync(FULL, valid && lk == m1);
-        uint64_t m2;
-        if (__popc(at_max) >= 2) {
-          m2 = m1;
-        } else {
-          m2 = warp_max_u64(lk == m1 ? 0ull : lk);
-        }
-        if (W > 1) {  // merge the per-warp top-2 multisets
+        // _min_max_choice (scheduling.py:299-312): argmin (lowest index) of
+        // peak_s = max(L_s + w_s, max_{j != s} L_j).  Since w_s >= 0 and
+        // rounding is monotone, L_s + w_s >= L_s, so the max over j != s may
+        // include s itself: peak_s = max(L_s + w_s, max_j L_j) -- one max
+        // reduction instead of the top-2 of the loads.
+        uint64_t m1 = warp_max_u64(valid ? okey(load) : 0ull);
+        if (W > 1) {
           Xch all[W];
-          xchg(Xch{m1, m2, 0, 0}, all);
+          xchg(Xch{m1, 0, 0, 0}, all);
           m1 = all[0].a;
-          m2 = all[0].b;
 #pragma unroll
-          for (int w = 1; w < W; ++w) {
-            const uint64_t a1 = all[w].a, a2 = all[w].b;
-            const uint64_t lo1 = m1 < a1 ? m1 : a1, hi2 = m2 > a2 ? m2 : a2;
-            m1 = m1 > a1 ? m1 : a1;
-            m2 = lo1 > hi2 ? lo1 : hi2;
-          }
+          for (int w = 1; w < W; ++w) m1 = all[w].a > m1 ? all[w].a : m1;
         }
-        const uint64_t ok_ = (lk == m1) ? m2 : m1;
-        const double others = ok_ == 0ull ? -INFINITY : from_okey(ok_);
+        const double top = from_okey(m1);
         const double own = __dadd_rn(load, w);
-        const double peak = own > others ? own : others;
+        const double peak = own > top ? own : top;
         const bool cand = need && !isinf(w) && peak < INFINITY;
         const uint64_t pk = cand ? okey(peak) : ~0ull;
         const uint64_t mp = warp_min_u64(pk);
