@@ -362,8 +362,6 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
       }
       reserved -= Ir + Or;
       cold.completion = t;
-      cold.req_count += 1;
-      cold.tok_count += Ir + Or;
       if (DEP) DEP[r] = t;
       load = __dsub_rn(load, wr);  // Scheduler.complete: the recorded values
       run_i -= Ir;
@@ -773,6 +771,12 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
         run_i += Ia;
         run_p += Pa;
         dirty = true;
+        // InstanceMetrics request / token counts (simulator.py:338-341): in a
+        // replay that completes, every dispatched request retires exactly
+        // once, so they are accumulated here, off the retirement path (a
+        // failed trace reports an error instead of metrics)
+        cold.req_count += 1;
+        cold.tok_count += Ia + Oa;
         R[a].P = (int32_t)Pa;
         R[a].W = w;
         if (qhead < 0) {
@@ -843,8 +847,6 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
           const QRec rec = R[m];
           load = __dsub_rn(load, rec.W);
           if (DEP) DEP[m] = clock;
-          cold.tok_count += (int64_t)I[m] + O[m];
-          cold.req_count += 1;
           m = (m == qtail) ? -1 : rec.next;
         }
         r = stop;
