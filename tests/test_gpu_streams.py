@@ -161,3 +161,38 @@ def test_device_stream_launches_counted(eng):
     n0 = eng.launch_count
     streams.arrival_times([1, 2, 3], [10, 0, 5], 3.0, engine=eng)
     assert eng.launch_count == n0 + 1
+
+
+def test_rng_argument_validation(eng):
+    st = nat.pcg64_states([1])
+    off = np.array([0, 10], np.int64)
+    ptr = eng.device_alloc(80)
+    try:
+        bad_kind = nat.hs_dist(9, 10, 0, 0, 0.0, 0.0)
+        with pytest.raises(nat.EngineError, match="unknown distribution"):
+            eng.rng_generate(st, off, [bad_kind], [ptr])
+        with pytest.raises(nat.EngineError, match="lo <= hi"):
+            eng.rng_generate(st, off, [nat.hs_dist(nat.DIST_UNIFORM_LEN, 10, 5, 4, 0, 0)], [ptr])
+        with pytest.raises(nat.EngineError, match="cap must be >= 1"):
+            eng.rng_generate(st, off, [nat.hs_dist(nat.DIST_NORMAL_LEN, 0, 0, 0, 1.0, 1.0)], [ptr])
+        with pytest.raises(nat.EngineError, match="n_dists"):
+            eng.rng_generate(st, off, [nat.hs_dist(nat.DIST_EXP_CUMSUM, 0, 0, 0, 1.0, 0)] * 5, [ptr] * 5)
+        with pytest.raises(nat.EngineError, match="non-decreasing"):
+            eng.rng_generate(nat.pcg64_states([1, 2]), np.array([0, 5, 3], np.int64),
+                             [nat.hs_dist(nat.DIST_EXP_CUMSUM, 0, 0, 0, 1.0, 0)], [ptr])
+        # the state is untouched by a rejected call
+        assert st.tobytes() == nat.pcg64_states([1]).tobytes()
+    finally:
+        eng.device_free(ptr)
+
+
+def test_seeded_replay_rejects_arrivals_and_seeds_together(eng):
+    cluster, params, config = _config4()
+    I, O = wl.trace_lengths(50, seed=1)
+    off = np.array([0, 50], np.int64)
+    with pytest.raises(hs.SpecError, match="either arrival times or arrival seeds"):
+        hs.replay_traces(cluster, config, params, hs.PolicyConfig(), off, I, O, O, arrival=np.zeros(50),
+                         rate=3.0, arrival_seeds=[1], engine=eng)
+    with pytest.raises(hs.SpecError, match="arrival rate must be positive"):
+        hs.replay_traces(cluster, config, params, hs.PolicyConfig(), off, I, O, O, rate=-1.0, arrival_seeds=[1],
+                         engine=eng)
