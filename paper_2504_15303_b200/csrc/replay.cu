@@ -186,6 +186,7 @@ struct Cold {
   double completion, wcur, err_t;
   int64_t tok_count;
   int32_t req_count, cnt_max, err, err_req;
+  int32_t ty, _pad;  // instance class (read from here: a per-lane constant-bank index serialises)
 };
 
 // One instance class of the deployment, staged in shared memory once per
@@ -278,7 +279,8 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   const int jj = wsub * 32 + lane;  // instance index of this lane
   const bool valid = jj < N;
   const int j = valid ? jj : 0;
-  const int ty = c_rep.inst_type[j];
+  cold.ty = c_rep.inst_type[j];
+  const int& ty = cold.ty;
   const TypeRec& trec = types[ty];
   const double* tp = trec.p;
   const double budget = trec.budget;
