@@ -318,3 +318,64 @@ def test_config5_shape_topk_then_rescore(eng):
         assert int(res.result[d]["error"]) == 0 == int(r[0]["error"])
         assert np.array_equal(res.assign[sl], a)
         assert np.array_equal(res.depart[sl].view(np.uint64), dep.view(np.uint64))
+
+
+def test_config4_full_size_traces_vs_oracle(eng):
+    """Bench-scale parity: 48 full config-4 traces (1e5 requests each, 140
+    req/s, OS, 32 instances) -- the bench's exact inputs for traces 0..47,
+    drawn on the device -- vs the literal C oracle, every assignment and
+    departure time bit for bit."""
+    from paper_2504_15303_b200 import streams
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    prof = wl.config4()
+    cluster = hs.ClusterSpec(hs.ModelSpec(**prof.model), hs.EngineOverheads(**prof.engine),
+                             tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+                             hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {a: 1 for a in wl.CONFIG4_TYPES})
+    nT, q = 48, wl.CONFIG4_Q
+    seeds = list(range(nT))
+    I, O = streams.gen_trace_lengths(seeds, q, "lognormal:200:0.6", "lognormal:150:0.6", 4096, 4096, engine=eng)
+    T = streams.arrival_times([42 + s for s in seeds], [q] * nT, wl.CONFIG4_RATE, engine=eng)
+    off = np.arange(nT + 1, dtype=np.int64) * q
+    pol = hs.PolicyConfig()
+    res = hs.replay_traces(cluster, config, params, pol, off, I, O, O, arrival=T, want_assign=True,
+                           want_depart=True, engine=eng)
+    handles = build_instances(cluster, config, params)
+    a, d, m, r = orc.replay(engine_instances(handles, pol), _policy_struct(pol, 32, hs.kv_bytes_per_token(cluster.model)),
+                            off, I, O, O, T, nthreads=16)
+    assert (res.result["error"] == 0).all() and (r["error"] == 0).all()
+    assert np.array_equal(res.result["n_steps"], r["n_steps"])
+    assert np.array_equal(res.assign, a)
+    assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64))
+    for f in ("completion_time", "peak_kv_usage", "residual_load"):
+        assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
+
+
+def test_config5_full_size_rescore_vs_oracle(eng):
+    """BASELINE config 5 at full size for a slice: the top-1024 deployments of
+    the config-3 space, the first 16 of them each replayed on the 1e5-request
+    trace (rate = inf, OS) in one launch, vs the oracle."""
+    _case, _req, t = _config3_tables(eng)
+    top, _nf, _ = planner.search_topk(t, 1024, engine=eng)
+    assert len(top) == 1024
+    configs = [planner.deployment_of(t, int(i)) for i in top["index"][:16]]
+    p3 = wl.config3()
+    params = {k: hs.LatencyParams(*v) for k, v in p3.params.items()}
+    q = wl.CONFIG4_Q
+    I1, O1 = wl.trace_lengths(q, seed=0)
+    n = len(configs)
+    off = np.arange(n + 1, dtype=np.int64) * q
+    res = hs.replay_deployments(t.cluster, configs, params, hs.PolicyConfig(), np.arange(n), off, np.tile(I1, n),
+                                np.tile(O1, n), np.tile(O1, n), want_depart=True, engine=eng)
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    per_token = hs.kv_bytes_per_token(t.cluster.model)
+    for d in range(n):
+        handles = build_instances(t.cluster, configs[d], params)
+        sl = slice(off[d], off[d + 1])
+        a, dep, m, r = orc.replay(engine_instances(handles, hs.PolicyConfig()),
+                                  _policy_struct(hs.PolicyConfig(), len(handles), per_token),
+                                  np.array([0, q], np.int64), I1, O1, O1, None)
+        assert int(res.result[d]["error"]) == 0 == int(r[0]["error"])
+        assert np.array_equal(res.assign[sl], a)
+        assert np.array_equal(res.depart[sl].view(np.uint64), dep.view(np.uint64))
