@@ -78,7 +78,8 @@ enum hs_trace_error {
   HS_TRACE_EXP_OVERFLOW = 3,       /* scheduling.py:154 math.exp OverflowError      */
   HS_TRACE_NO_INSTANCE = 4,        /* scheduling.py:310-311 SchedulingError         */
   HS_TRACE_NEGATIVE_RUNNING = 5,   /* capacity.py:50-52 SpecError                   */
-  HS_TRACE_CAPACITY = 6            /* engine limit: active-set bound exceeded        */
+  HS_TRACE_CAPACITY = 6,           /* engine limit: active-set bound exceeded        */
+  HS_TRACE_STALLED = 7             /* engine: streamed inputs did not arrive in time */
 };
 
 /* core.py:45-56 ModelSpec */

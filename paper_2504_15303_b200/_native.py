@@ -23,7 +23,7 @@ ENTRY_OK, ENTRY_INFEASIBLE_CONFIG, ENTRY_MISSING_PARAMS, ENTRY_INFEASIBLE_REQUES
     ENTRY_BAD_DEGREE = range(6)
 POLICY_CODE = {"OS": 0, "RR": 1, "WRR": 2, "SI": 3, "MB": 4}
 TRACE_OK, TRACE_INFEASIBLE_REQUEST, TRACE_NONPOSITIVE_COST, TRACE_EXP_OVERFLOW, TRACE_NO_INSTANCE, \
-    TRACE_NEGATIVE_RUNNING, TRACE_CAPACITY = range(7)
+    TRACE_NEGATIVE_RUNNING, TRACE_CAPACITY, TRACE_STALLED = range(8)
 
 LIB_PATH = pathlib.Path(os.environ.get("HS_LIB", pathlib.Path(__file__).resolve().parent / "libhetserve_b200.so"))
 

@@ -1,10 +1,12 @@
 // capi.cu -- the C ABI (include/hetserve_b200.h): context, device memory,
 // argument validation, and the host side of each entry point.  No torch
 // types cross this boundary; the Python shim binds it with ctypes.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,7 +37,7 @@ enum Slot {
   S_TOTAL, S_FIRSTBAD, S_FLAG, S_SELIDX, S_NSEL, S_KEYS, S_KEYS2, S_IDX2, S_CUBTMP, S_RANKED,
   S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_HEAP, S_MINNEED, S_TK_HIST, S_TK_CNT, S_TK_KEY,
   S_TK_IDX, S_TK_KEY2, S_TK_IDX2, S_DEPS, S_TDEP, S_THEAP, S_RNG_ST, S_RNG_ST2, S_RNG_OFF, S_RNG_BAD,
-  N_SLOTS
+  S_PROGRESS, N_SLOTS
 };
 
 }  // namespace
@@ -706,6 +708,22 @@ int check_dist(const hs_dist& d) {
 // hs_replay / hs_replay_seeded: host buffers, traces replayed in kPipe chunks
 // (copy of chunk i+1 overlaps the replay of chunk i); seeded arrivals and
 // predictions are drawn on the chunk's stream right before its replay.
+// cuStreamWriteValue32 (driver API, through the runtime's entry-point
+// query): the copy stream publishes "phase p resident" without a kernel, so
+// the replay kernel can wait on it even while it occupies every SM.
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+  static const WriteValue32Fn fn = []() -> WriteValue32Fn {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<WriteValue32Fn>(p);
+  }();
+  return fn;
+}
+
 int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b,
                 const hs_replay_seeds* seeds, uint8_t* assign, double* depart, hs_inst_metrics* metrics,
                 hs_trace_result* result) {
@@ -762,6 +780,103 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
   if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
   if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
   HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
+  // Streamed replay (equal-length traces, the batched-replay shape): every
+  // trace is launched once the first of kPhases phases of every trace is
+  // resident; the copy stream then moves phase p of all traces with one 2-D
+  // copy per array and publishes p + 1 to a progress word the kernel reads
+  // before it consumes a request block of that phase.  The PCIe transfer
+  // hides under the replay instead of delaying the last chunk.  Heaps are
+  // sized from phase 0's min(I + O); a trace that outgrows that estimate
+  // reports CAPACITY and the call is redone on the exactly-sized path below.
+  const int64_t sq = T > 0 ? off[1] : 0;
+  bool equal = T > 0 && sq >= 256 && sq % 32 == 0 && !std::getenv("HS_NO_STREAM");
+  for (int64_t t = 1; equal && t <= T; ++t) equal = off[t] == t * sq;
+  const WriteValue32Fn wv = equal ? write_value32() : nullptr;
+  if (wv) {
+    constexpr int64_t kPhases = 8;
+    const int64_t L = ((sq + kPhases - 1) / kPhases + 31) / 32 * 32;
+    const int64_t nphase = (sq + L - 1) / L;
+    uint32_t* dProg;
+    int32_t* d_min;
+    if ((rc = ensure_t(c, S_PROGRESS, 1, &dProg)) || (rc = ensure_t(c, S_MINNEED, kPipe, &d_min))) return rc;
+    auto copy_phase = [&](int64_t p) -> int {
+      const int64_t a = p * L, w = (sq - a) < L ? (sq - a) : L;
+      const size_t s4 = (size_t)sq * 4, s8 = (size_t)sq * 8;
+      HS_CUDA(cudaMemcpy2DAsync(dI + a, s4, b->input_len + a, s4, (size_t)w * 4, (size_t)T, cudaMemcpyHostToDevice,
+                                c->stream));
+      HS_CUDA(cudaMemcpy2DAsync(dO + a, s4, b->output_len + a, s4, (size_t)w * 4, (size_t)T, cudaMemcpyHostToDevice,
+                                c->stream));
+      if (!p_is_o && !gen_pred)
+        HS_CUDA(cudaMemcpy2DAsync(dP + a, s4, b->pred_output_len + a, s4, (size_t)w * 4, (size_t)T,
+                                  cudaMemcpyHostToDevice, c->stream));
+      if (dT && !gen_arr)
+        HS_CUDA(cudaMemcpy2DAsync(dT + a, s8, b->arrival + a, s8, (size_t)w * 8, (size_t)T, cudaMemcpyHostToDevice,
+                                  c->stream));
+      if (wv((CUstream)c->stream, (CUdeviceptr)dProg, (cuuint32_t)(p + 1), 0) != CUDA_SUCCESS)
+        return fail(HS_ERR_CUDA, "cuStreamWriteValue32 failed");
+      return HS_OK;
+    };
+    cudaStream_t ks = c->ks[0];
+    if ((rc = begin_timing(c))) return rc;
+    HS_CUDA(cudaMemsetAsync(dProg, 0, sizeof(uint32_t), c->stream));
+    HS_CUDA(cudaEventRecord(c->ev_min[1], c->stream));  // offsets + generator states are on the device
+    HS_CUDA(cudaStreamWaitEvent(ks, c->ev_min[1], 0));
+    if (gen_arr) {  // drawn while phase 0 is in flight
+      hs::RngConst g{};
+      g.n_dists = 1;
+      g.dist[0] = hs_dist{HS_DIST_EXP_CUMSUM, 0, 0, 0, seeds->arrival_scale, 0.0};
+      g.out[0] = dT;
+      HS_CUDA(hs::launch_rng_generate(g, dSA, dOff, 0, T, nullptr, ks));
+      c->launches += 1;
+    }
+    if (gen_pred) {
+      hs::RngConst g{};
+      g.n_dists = 1;
+      g.dist[0] = hs_dist{HS_DIST_NORMAL_LEN, seeds->pred_cap, 0, 0, seeds->pred_mean, seeds->pred_stddev};
+      g.out[0] = dP;
+      HS_CUDA(hs::launch_rng_generate(g, dSP, dOff, 0, T, nullptr, ks));
+      c->launches += 1;
+    }
+    if ((rc = copy_phase(0))) return rc;
+    HS_CUDA(cudaMemsetAsync(d_min, 0x7f, sizeof(int32_t), c->stream));
+    HS_CUDA(hs::launch_min_need_2d(dI, dO, T, L < sq ? L : sq, sq, d_min, c->stream));
+    c->launches += 1;
+    HS_CUDA(cudaMemcpyAsync(c->pinned_min, d_min, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaEventRecord(c->ev_copy[0], c->stream));
+    HS_CUDA(cudaEventSynchronize(c->ev_copy[0]));
+    hs::ReplayConst rs = base;
+    size_heaps(rs, inst, c->pinned_min[0], sq);
+    HS_CUDA(cudaStreamWaitEvent(ks, c->ev_copy[0], 0));
+    void* heap = nullptr;
+    HS_CUDA(cudaMallocAsync(&heap, (size_t)T * rs.heap_stride * hs::kHEntBytes, ks));
+    HS_CUDA(hs::launch_replay(rs, T, dOff, dI, dO, dP, dT, dA, dDep, dM, dR, dQ, static_cast<uint64_t*>(heap), ks,
+                              nullptr, nullptr, nullptr, 0, 0, dProg, (int)L));
+    c->launches += 1;
+    HS_CUDA(cudaFreeAsync(heap, ks));
+    HS_CUDA(cudaEventRecord(c->ev_done[0], ks));
+    for (int64_t p = 1; p < nphase; ++p)
+      if ((rc = copy_phase(p))) return rc;
+    HS_CUDA(cudaStreamWaitEvent(c->stream, c->ev_done[0], 0));
+    if ((rc = end_timing(c))) return rc;
+    HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * N, cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
+    if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
+    if (depart && total > 0)
+      HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    bool redo = false;
+    for (int64_t t = 0; t < T; ++t) redo |= result[t].error == HS_TRACE_CAPACITY;
+    if (!redo) return HS_OK;
+    // phase-0 sizing was too small for some trace: exact sizing below (the
+    // device already holds every input; the chunked path copies them again)
+    // (the generator kernel advanced the device copies of the states: restore them)
+    if (gen_arr)
+      HS_CUDA(cudaMemcpyAsync(dSA, seeds->arrival_state, sizeof(hs_pcg64_state) * T, cudaMemcpyHostToDevice,
+                              c->stream));
+    if (gen_pred)
+      HS_CUDA(cudaMemcpyAsync(dSP, seeds->predictor_state, sizeof(hs_pcg64_state) * T, cudaMemcpyHostToDevice,
+                              c->stream));
+  }
   // Chunks of traces: copy chunk i on the copy stream while earlier chunks
   // replay on their own streams; each chunk sizes its heaps exactly from
   // its own min(I + O).

@@ -84,6 +84,8 @@ cudaError_t launch_topk_pass(const FeasSpace& fs, bool upload, int mode, int64_t
                              cudaStream_t st);
 cudaError_t launch_invert_keys(uint64_t* d_key, int64_t n, cudaStream_t st);
 cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st);
+cudaError_t launch_min_need_2d(const int32_t* d_I, const int32_t* d_O, int64_t rows, int64_t width, int64_t pitch,
+                               int32_t* d_out, cudaStream_t st);
 // deps / trace_dep / trace_heap: per-trace deployments (config 5); when
 // deps is null every trace uses rc and trace t's heap starts at t*stride.
 cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
@@ -91,7 +93,8 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result,
                           void* d_qrec, uint64_t* d_heap, cudaStream_t st, const ReplayConst* d_deps = nullptr,
                           const int32_t* d_trace_dep = nullptr, const int64_t* d_trace_heap = nullptr,
-                          int n_max = 0, int max_types = 0);
+                          int n_max = 0, int max_types = 0, const uint32_t* d_progress = nullptr,
+                          int phase_len = 0);
 constexpr int kQRecBytes = 24;  // replay.cu QRec
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
 constexpr int kHeapShared = 16;  // replay.cu kHS

@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
              hs_trace_result* __restrict__ result, QRec* __restrict__ qrec_all, uint64_t* __restrict__ heap_all,
              const ReplayConst* __restrict__ deps, const int32_t* __restrict__ trace_dep,
-             const int64_t* __restrict__ trace_heap, int n_max, const __grid_constant__ ReplayConst c_one) {
+             const int64_t* __restrict__ trace_heap, int n_max, const uint32_t* progress, int32_t phase_len,
+             const __grid_constant__ ReplayConst c_one) {
   constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);  // trace groups per block
   __shared__ uint64_t s_tab[256];
   __shared__ Cold s_cold[kWarps * 32];
@@ -593,13 +594,39 @@ __global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
   uint8_t my_assign = 0;
   for (int64_t base = 0; base < q && !failed; base += 32) {
     const int n_in = (int)((q - base) < 32 ? (q - base) : 32);
+    if (progress) {
+      // streamed inputs (host path): phase p of every trace is resident once
+      // *progress > p (the copy stream publishes it after the phase's copies)
+      const uint32_t need = (uint32_t)((base + n_in - 1) / phase_len);
+      bool stalled = false;
+      if (lane == 0) {
+        const long long t0 = clock64();
+        uint32_t have;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(have) : "l"(progress) : "memory");
+        while (have <= need) {
+          __nanosleep(256);
+          if (clock64() - t0 > 20000000000ll) {  // ~10 s: report instead of hanging the device
+            stalled = true;
+            break;
+          }
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(have) : "l"(progress) : "memory");
+        }
+      }
+      if (__shfl_sync(FULL, stalled, 0)) {
+        t_err = HS_TRACE_STALLED;
+        t_err_req = base;
+        t_err_inst = -1;
+        failed = true;
+        break;
+      }
+    }
     int32_t cI = 0, cO = 0, cP = 0;
     double cT = 0.0;
-    if (lane < n_in) {
-      cI = I[base + lane];
-      cO = O[base + lane];
-      cP = P[base + lane];
-      cT = T ? T[base + lane] : 0.0;
+    if (lane < n_in) {  // L2-coherent loads: streamed inputs arrive while the kernel runs
+      cI = __ldcg(I + base + lane);
+      cO = __ldcg(O + base + lane);
+      cP = __ldcg(P + base + lane);
+      cT = T ? __ldcg(T + base + lane) : 0.0;
     }
     // price (arrival, class) pairs: scheduling.py:119-147
     __syncwarp();
@@ -916,7 +943,8 @@ cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
                      const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign, double* d_depart,
                      hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec, uint64_t* d_heap,
                      cudaStream_t st, const ReplayConst* d_deps, const int32_t* d_trace_dep,
-                     const int64_t* d_trace_heap, int n_max, int max_types) {
+                     const int64_t* d_trace_heap, int n_max, int max_types, const uint32_t* d_progress,
+                     int phase_len) {
   constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);
   const int warps = W * G;
   const size_t smem = (size_t)warps * 32 * max_types * sizeof(double) + (size_t)G * max_types * sizeof(TypeRec);
@@ -927,7 +955,7 @@ cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
   const unsigned blocks = (unsigned)((n_traces + G - 1) / G);
   k_replay<W, MULTI><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
                                                 d_result, static_cast<QRec*>(d_qrec), d_heap, d_deps, d_trace_dep,
-                                                d_trace_heap, n_max, rc);
+                                                d_trace_heap, n_max, d_progress, phase_len, rc);
   return cudaGetLastError();
 }
 
@@ -935,14 +963,15 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
                           double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec,
                           uint64_t* d_heap, cudaStream_t st, const ReplayConst* d_deps, const int32_t* d_trace_dep,
-                          const int64_t* d_trace_heap, int n_max, int max_types) {
+                          const int64_t* d_trace_heap, int n_max, int max_types, const uint32_t* d_progress,
+                          int phase_len) {
   if (n_traces <= 0) return cudaSuccess;
   if (n_max <= 0) n_max = rc.N;
   if (max_types <= 0) max_types = rc.n_types;
   const int W = (n_max + 31) / 32;
 #define HS_LW(w, m)                                                                                              \
   launch_w<w, m>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result, d_qrec, d_heap, \
-                 st, d_deps, d_trace_dep, d_trace_heap, n_max, max_types)
+                 st, d_deps, d_trace_dep, d_trace_heap, n_max, max_types, d_progress, phase_len)
   const bool multi = d_deps != nullptr;
   switch (W) {
     case 1: return multi ? HS_LW(1, true) : HS_LW(1, false);
@@ -972,6 +1001,33 @@ cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, i
   const int cap = sm_count() * 8;
   if (blocks > cap) blocks = cap;
   k_min_need<<<blocks, 256, 0, st>>>(d_I, d_O, n, d_out);
+  return cudaGetLastError();
+}
+
+// the same over the first `width` requests of each of `rows` equal-length
+// traces (row pitch `pitch`): the streamed host path sizes its heaps from the
+// first phase of every trace
+__global__ void k_min_need_2d(const int32_t* __restrict__ I, const int32_t* __restrict__ O, int64_t rows,
+                              int64_t width, int64_t pitch, int32_t* out) {
+  int32_t m = INT32_MAX;
+  const int64_t n = rows * width;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k / width, e = r * pitch + (k - r * width);
+    const int64_t v = (int64_t)I[e] + O[e];
+    const int32_t vv = v > INT32_MAX ? INT32_MAX : (int32_t)v;
+    m = vv < m ? vv : m;
+  }
+  m = __reduce_min_sync(FULL, (unsigned)m);
+  if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+}
+
+cudaError_t launch_min_need_2d(const int32_t* d_I, const int32_t* d_O, int64_t rows, int64_t width, int64_t pitch,
+                               int32_t* d_out, cudaStream_t st) {
+  if (rows <= 0 || width <= 0) return cudaSuccess;
+  int blocks = (int)((rows * width + 255) / 256);
+  const int cap = sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  k_min_need_2d<<<blocks, 256, 0, st>>>(d_I, d_O, rows, width, pitch, d_out);
   return cudaGetLastError();
 }
 

@@ -196,3 +196,35 @@ def test_seeded_replay_rejects_arrivals_and_seeds_together(eng):
     with pytest.raises(hs.SpecError, match="arrival rate must be positive"):
         hs.replay_traces(cluster, config, params, hs.PolicyConfig(), off, I, O, O, rate=-1.0, arrival_seeds=[1],
                          engine=eng)
+
+
+@pytest.mark.parametrize("seeded", [False, True])
+def test_streamed_replay_equals_chunked(eng, seeded, monkeypatch):
+    """Equal-length traces take the streamed host path (phase-wise 2-D copies
+    published through a progress word the kernel waits on); it must give
+    exactly what the chunked path (HS_NO_STREAM) gives."""
+    cluster, params, config = _config4()
+    nT, q = 96, 4096
+    I = np.concatenate([wl.trace_lengths(q, seed=300 + t)[0] for t in range(nT)])
+    O = np.concatenate([wl.trace_lengths(q, seed=300 + t)[1] for t in range(nT)])
+    off = np.arange(nT + 1, dtype=np.int64) * q
+    pc = hs.PredictorConfig(mode="normal", mean=150.0, stddev=60.0, seed=0)
+    pol = hs.PolicyConfig(policy="OS", predictor=pc if seeded else hs.PredictorConfig())
+    if seeded:
+        kw = dict(rate=140.0, arrival_seeds=[7 + t for t in range(nT)], predictor_seeds=[9 + t for t in range(nT)])
+        P = None
+    else:
+        kw = dict(arrival=np.concatenate([wl.arrivals(q, 140.0, seed=7 + t) for t in range(nT)]))
+        P = O
+    got = hs.replay_traces(cluster, config, params, pol, off, I, O, P, want_assign=True, want_depart=True,
+                           engine=eng, **kw)
+    launches = eng.launch_count
+    monkeypatch.setenv("HS_NO_STREAM", "1")
+    want = hs.replay_traces(cluster, config, params, pol, off, I, O, P, want_assign=True, want_depart=True,
+                            engine=eng, **kw)
+    assert eng.launch_count - launches >= 8  # the chunked path: one replay launch per chunk
+    assert (want.result["error"] == 0).all()
+    assert np.array_equal(got.assign, want.assign)
+    assert np.array_equal(got.depart.view(np.uint64), want.depart.view(np.uint64))
+    assert got.metrics.tobytes() == want.metrics.tobytes()
+    assert got.result.tobytes() == want.result.tobytes()
