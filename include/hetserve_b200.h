@@ -253,6 +253,16 @@ int hs_search_tables(hs_ctx* ctx, const hs_model* model, const hs_engine* engine
                      const int32_t* input_len, const int32_t* output_len, int64_t n_requests,
                      hs_entry* table, int32_t* n_degrees);
 
+/* planner.py:51-118 for ONE instance with an explicit KV budget (one warp):
+ * plan_static_batches -> batch b is [stops[b-1], stops[b]) (stops[-1] = 0),
+ * time_batches -> times[b] (estimate_batch_time, when params != NULL), and
+ * estimate_instance_throughput -> entry->rate, with entry->status /
+ * bad_request / zero_div_int as hs_search_tables reports them.  I, O, stops,
+ * times are host arrays (stops / times with room for q entries). */
+int hs_plan_instance(hs_ctx* ctx, double budget, int64_t per_token, const double* params, const int32_t* I,
+                     const int32_t* O, int64_t q, int64_t* stops, double* times, int64_t* n_batches,
+                     hs_entry* entry);
+
 /* Exhaustive argmax over candidate indices [begin, end) of the product
  * space defined by (table, n_degrees): best = max total, ties -> lowest
  * index (planner.py:227).  *n_feasible receives the number of feasible

@@ -13,6 +13,8 @@ there is no CPU fallback.
 """
 
 from .domain import (
+    RunningTokens,
+    kv_usage,
     ClusterSpec,
     DeploymentConfig,
     EngineOverheads,
@@ -43,6 +45,7 @@ from .domain import (
     prefill_time,
 )
 from .planner import (
+    BatchPlan,
     MachineEstimate,
     SearchOutcome,
     SearchTables,
@@ -50,13 +53,28 @@ from .planner import (
     best_config,
     build_tables,
     deployment_of,
+    estimate_batch_time,
+    estimate_instance_throughput,
     merge_topk,
     estimate_system_throughput,
+    plan_static_batches,
+    time_batches,
     search_best,
     search_optimal_config,
     search_topk,
 )
-from .scheduling import POLICIES, InstanceHandle, OutputLengthPredictor, PolicyConfig, PredictorConfig, Scheduler
+from .scheduling import (
+    POLICIES,
+    InstanceHandle,
+    OutputLengthPredictor,
+    PolicyConfig,
+    PredictorConfig,
+    Scheduler,
+    ideal_batch_size,
+    per_request_cost,
+    request_oversized,
+    workload,
+)
 from .simulator import (
     InstanceMetrics,
     ReplayBatchResult,

@@ -139,7 +139,7 @@ EXPORTS = (
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
     "hs_replay_seeded", "hs_pcg64_seed", "hs_pcg64_seed_u64", "hs_rng_generate",
     "hs_sched_create", "hs_sched_destroy", "hs_sched_evaluate", "hs_sched_choose", "hs_sched_complete",
-    "hs_sched_snapshot",
+    "hs_sched_snapshot", "hs_plan_instance",
 )
 
 _lib = None
@@ -189,6 +189,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_sched_choose": ([vp, C.c_char_p, i32, i64, i64, vp, vp, vp], C.c_int),
             "hs_sched_complete": ([vp, C.c_char_p, i32, vp], C.c_int),
             "hs_sched_snapshot": ([vp, vp, vp, vp, vp, vp], C.c_int),
+            "hs_plan_instance": ([vp, dbl, i64, vp, vp, vp, i64, vp, vp, vp, vp], C.c_int),
             "hs_rng_generate": ([vp, vp, i32, vp, vp, i32, vp, vp], C.c_int),
         }
         for name, (args, res) in sig.items():
@@ -338,6 +339,22 @@ class Engine:
                                       C.cast(oarr, C.c_void_p), _ptr(bad))
         self.check(rc, "hs_rng_generate")
         return bad[:n]
+
+    def plan_instance(self, budget: float, per_token: int, params8, I: np.ndarray, O: np.ndarray):
+        """hs_plan_instance: (stops int64[nb], times float64[nb] or None, entry)."""
+        I = np.ascontiguousarray(I, np.int32)
+        O = np.ascontiguousarray(O, np.int32)
+        q = len(I)
+        stops = np.zeros(max(q, 1), np.int64)
+        times = np.zeros(max(q, 1), np.float64) if params8 is not None else None
+        pr = None if params8 is None else np.ascontiguousarray(params8, np.float64)
+        nb = C.c_int64()
+        entry = np.zeros(1, ENTRY_DTYPE)
+        rc = self.lib.hs_plan_instance(self.handle, float(budget), int(per_token), _ptr(pr), _ptr(I), _ptr(O), q,
+                                       _ptr(stops), _ptr(times), C.byref(nb), _ptr(entry))
+        self.check(rc, "hs_plan_instance")
+        n = int(nb.value)
+        return stops[:n], None if times is None else times[:n], entry[0]
 
     # ---------------------------------------------------------------- search
     def search_tables(self, model: hs_model, engine: hs_engine, limits: hs_limits, machines: np.ndarray,

@@ -37,7 +37,7 @@ enum Slot {
   S_TOTAL, S_FIRSTBAD, S_FLAG, S_SELIDX, S_NSEL, S_KEYS, S_KEYS2, S_IDX2, S_CUBTMP, S_RANKED,
   S_ASSIGN, S_DEPART, S_METRICS, S_RESULT, S_WREC, S_HEAP, S_MINNEED, S_TK_HIST, S_TK_CNT, S_TK_KEY,
   S_TK_IDX, S_TK_KEY2, S_TK_IDX2, S_DEPS, S_TDEP, S_THEAP, S_RNG_ST, S_RNG_ST2, S_RNG_OFF, S_RNG_BAD,
-  S_PROGRESS, N_SLOTS
+  S_PROGRESS, S_STOPS, S_TIMES, S_NB, S_PENTRY, N_SLOTS
 };
 
 }  // namespace
@@ -487,6 +487,46 @@ int hs_search_tables(hs_ctx* c, const hs_model* model, const hs_engine* engine, 
   HS_CUDA(cudaMemcpyAsync(out.data(), dT, sizeof(hs_entry) * n, cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   for (int k = 0; k < n; ++k) table[slot[k]] = out[k];
+  return HS_OK;
+}
+
+int hs_plan_instance(hs_ctx* c, double budget, int64_t per_token, const double* params, const int32_t* I,
+                     const int32_t* O, int64_t q, int64_t* stops, double* times, int64_t* n_batches,
+                     hs_entry* entry) {
+  if (!c || !entry || !n_batches || (q > 0 && (!I || !O || !stops))) return fail(HS_ERR_ARG, "null argument");
+  if (q < 0) return fail(HS_ERR_ARG, "q < 0");
+  if (per_token <= 0) return fail(HS_ERR_ARG, "per_token must be positive");
+  if (params && q > 0 && !times) return fail(HS_ERR_ARG, "times is null");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  const size_t qq = (size_t)(q > 0 ? q : 1);
+  int32_t *dI, *dO;
+  int64_t *dS, *dNb;
+  double* dTm;
+  hs_entry* dE;
+  if ((rc = ensure_t(c, S_I, qq, &dI)) || (rc = ensure_t(c, S_O, qq, &dO)) || (rc = ensure_t(c, S_STOPS, qq, &dS)) ||
+      (rc = ensure_t(c, S_TIMES, qq, &dTm)) || (rc = ensure_t(c, S_NB, 1, &dNb)) || (rc = ensure_t(c, S_PENTRY, 1, &dE)))
+    return rc;
+  if (q > 0) {
+    HS_CUDA(cudaMemcpyAsync(dI, I, sizeof(int32_t) * q, cudaMemcpyHostToDevice, c->stream));
+    HS_CUDA(cudaMemcpyAsync(dO, O, sizeof(int32_t) * q, cudaMemcpyHostToDevice, c->stream));
+  }
+  hs::PlanParams pp{};
+  pp.has = params != nullptr;
+  if (params) std::memcpy(pp.p, params, sizeof(pp.p));
+  if ((rc = begin_timing(c))) return rc;
+  HS_CUDA(hs::launch_plan_instance(budget, per_token, pp, dI, dO, q, dS, dTm, dNb, dE, c->stream));
+  c->launches += 1;
+  if ((rc = end_timing(c))) return rc;
+  HS_CUDA(cudaMemcpyAsync(n_batches, dNb, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaMemcpyAsync(entry, dE, sizeof(hs_entry), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t nb = *n_batches;
+  if (nb > 0) {
+    HS_CUDA(cudaMemcpyAsync(stops, dS, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, c->stream));
+    if (params) HS_CUDA(cudaMemcpyAsync(times, dTm, sizeof(double) * nb, cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+  }
   return HS_OK;
 }
 

@@ -69,9 +69,18 @@ struct ReplayConst {
   double wrr_weight[kMaxReplayInst];
 };
 
+struct PlanParams {
+  double p[8];
+  int32_t has;  // time the batches (estimate_batch_time) and compute the rate
+  int32_t _pad;
+};
+
 // launchers (return cudaError_t as int)
 cudaError_t launch_table_build(const EntryDesc* d_desc, int n, const SearchConst& sc, const int32_t* d_I,
                                const int32_t* d_O, hs_entry* d_out, cudaStream_t st);
+cudaError_t launch_plan_instance(double budget, int64_t per_token, const PlanParams& pp, const int32_t* d_I,
+                                 const int32_t* d_O, int64_t q, int64_t* d_stops, double* d_times, int64_t* d_nb,
+                                 hs_entry* d_out, cudaStream_t st);
 // workspace: 3 * blocks doubles/int64s
 cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, int blocks,
                                double* d_blk_best, int64_t* d_blk_idx, int64_t* d_blk_cnt,

@@ -29,6 +29,65 @@
 namespace hs {
 
 // ----------------------------------------------------------------- K1
+// planner.py:51-87 plan_static_batches for one instance, warp-cooperative:
+// each round tests 32 extensions of the current batch at once (warp prefix
+// sum of inputs, prefix max of outputs / inputs, one ballot for the first
+// extension that no longer fits).  on_batch(stop, width, max_I, max_O) is
+// called, warp-uniformly, for every batch in order.  Returns the index of a
+// request that does not fit alone (planner.py:78-84), or -1.
+template <class F>
+__device__ __forceinline__ int64_t scan_batches(const int32_t* __restrict__ I, const int32_t* __restrict__ O,
+                                                int64_t q, int64_t cap, int lane, F&& on_batch) {
+  int64_t start = 0;
+  while (start < q) {
+    int64_t sumI = 0, maxO = 0, maxI = 0;  // carries of the batch so far
+    int64_t pos = start, stop = start, bMO = 0, bMI = 0;
+    for (;;) {
+      const int64_t idx = pos + lane;
+      const bool valid = idx < q;
+      int64_t s = valid ? (int64_t)I[idx] : 0;
+      int64_t mo = valid ? (int64_t)O[idx] : 0;
+      int64_t mi = s;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        int64_t ts = __shfl_up_sync(0xffffffffu, s, off);
+        int64_t to = __shfl_up_sync(0xffffffffu, mo, off);
+        int64_t ti = __shfl_up_sync(0xffffffffu, mi, off);
+        if (lane >= off) {
+          s += ts;
+          mo = mo > to ? mo : to;
+          mi = mi > ti ? mi : ti;
+        }
+      }
+      const int64_t candI = sumI + s;
+      const int64_t candMO = maxO > mo ? maxO : mo;
+      const int64_t candMI = maxI > mi ? maxI : mi;
+      const int64_t width = idx - start + 1;
+      const int64_t tokens = sat_add(candI, sat_mul(width, candMO));
+      const bool fail = !valid || tokens > cap;
+      const unsigned bal = __ballot_sync(0xffffffffu, fail);
+      if (bal) {
+        const int f = __ffs(bal) - 1;
+        stop = pos + f;
+        const int src = f > 0 ? f - 1 : 0;
+        const int64_t sMO = __shfl_sync(0xffffffffu, candMO, src);
+        const int64_t sMI = __shfl_sync(0xffffffffu, candMI, src);
+        bMO = f > 0 ? sMO : maxO;
+        bMI = f > 0 ? sMI : maxI;
+        break;
+      }
+      sumI = __shfl_sync(0xffffffffu, candI, 31);
+      maxO = __shfl_sync(0xffffffffu, candMO, 31);
+      maxI = __shfl_sync(0xffffffffu, candMI, 31);
+      pos += 32;
+    }
+    if (stop == start) return start;
+    on_batch(stop, stop - start, bMI, bMO);
+    start = stop;
+  }
+  return -1;
+}
+
 __global__ void __launch_bounds__(128) k_table_build(const EntryDesc* __restrict__ desc, int n, SearchConst sc,
                                                      const int32_t* __restrict__ I, const int32_t* __restrict__ O,
                                                      hs_entry* __restrict__ out) {
@@ -72,62 +131,16 @@ __global__ void __launch_bounds__(128) k_table_build(const EntryDesc* __restrict
     } else {
       PySum tot;
       tot.init();
-      int64_t start = 0;
-      const int64_t pt = sc.per_token;
       // planner.py:69-74 per_token*sum(I) + width*per_token*max(O) > budget,
       // exactly: the integer pt*X exceeds B iff X > floor(floor(B) / pt)
-      const int64_t cap = budget >= 9.2e18 ? INT64_MAX : (int64_t)floor(budget) / pt;
-      while (start < q) {
-        int64_t sumI = 0, maxO = 0, maxI = 0;  // carries of the batch so far
-        int64_t pos = start, stop = start, bMO = 0, bMI = 0;
-        for (;;) {
-          const int64_t idx = pos + lane;
-          const bool valid = idx < q;
-          int64_t s = valid ? (int64_t)I[idx] : 0;
-          int64_t mo = valid ? (int64_t)O[idx] : 0;
-          int64_t mi = s;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            int64_t ts = __shfl_up_sync(0xffffffffu, s, off);
-            int64_t to = __shfl_up_sync(0xffffffffu, mo, off);
-            int64_t ti = __shfl_up_sync(0xffffffffu, mi, off);
-            if (lane >= off) {
-              s += ts;
-              mo = mo > to ? mo : to;
-              mi = mi > ti ? mi : ti;
-            }
-          }
-          const int64_t candI = sumI + s;
-          const int64_t candMO = maxO > mo ? maxO : mo;
-          const int64_t candMI = maxI > mi ? maxI : mi;
-          const int64_t width = idx - start + 1;
-          const int64_t tokens = sat_add(candI, sat_mul(width, candMO));
-          const bool fail = !valid || tokens > cap;
-          const unsigned bal = __ballot_sync(0xffffffffu, fail);
-          if (bal) {
-            const int f = __ffs(bal) - 1;
-            stop = pos + f;
-            const int src = f > 0 ? f - 1 : 0;
-            const int64_t sMO = __shfl_sync(0xffffffffu, candMO, src);
-            const int64_t sMI = __shfl_sync(0xffffffffu, candMI, src);
-            bMO = f > 0 ? sMO : maxO;
-            bMI = f > 0 ? sMI : maxI;
-            break;
-          }
-          sumI = __shfl_sync(0xffffffffu, candI, 31);
-          maxO = __shfl_sync(0xffffffffu, candMO, 31);
-          maxI = __shfl_sync(0xffffffffu, candMI, 31);
-          pos += 32;
-        }
-        if (stop == start) {  // planner.py:78-84
-          r.status = HS_ENTRY_INFEASIBLE_REQUEST;
-          r.bad_request = start;
-          break;
-        }
-        const int64_t b = stop - start;
+      const int64_t cap = budget >= 9.2e18 ? INT64_MAX : (int64_t)floor(budget) / sc.per_token;
+      const int64_t bad = scan_batches(I, O, q, cap, lane, [&](int64_t, int64_t b, int64_t bMI, int64_t bMO) {
         // planner.py:90-101 estimate_batch_time
         tot.add(__dadd_rn(prefill_time(d.p, b, bMI), decode_time(d.p, b, bMI, bMO)));
-        start = stop;
+      });
+      if (bad >= 0) {  // planner.py:78-84
+        r.status = HS_ENTRY_INFEASIBLE_REQUEST;
+        r.bad_request = bad;
       }
       if (r.status == HS_ENTRY_OK) {
         const double total = tot.result();  // planner.py:46-48 sum(per_batch_time)
@@ -142,6 +155,62 @@ __global__ void __launch_bounds__(128) k_table_build(const EntryDesc* __restrict
     }
   }
   if (lane == 0) out[e] = r;
+}
+
+// planner.py:51-118 for one instance with an explicit KV budget (one warp):
+// plan_static_batches (batch stops), time_batches (per-batch seconds, when
+// params are given) and estimate_instance_throughput (token_count / total).
+__global__ void k_plan_instance(double budget, int64_t per_token, PlanParams pp, const int32_t* __restrict__ I,
+                                const int32_t* __restrict__ O, int64_t q, int64_t* __restrict__ stops,
+                                double* __restrict__ times, int64_t* __restrict__ n_batches, hs_entry* out) {
+  const int lane = threadIdx.x & 31;
+  hs_entry r{};
+  r.bad_request = -1;
+  r.status = HS_ENTRY_OK;
+  r.budget = budget;
+  r.instance_count = 1;
+  int64_t tok = 0;
+  for (int64_t k = lane; k < q; k += 32) tok += (int64_t)I[k] + O[k];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tok += __shfl_xor_sync(0xffffffffu, tok, off);
+  r.token_count = tok;
+  const int64_t cap = budget >= 9.2e18 ? INT64_MAX : (int64_t)floor(budget) / per_token;
+  PySum tot;
+  tot.init();
+  int64_t nb = 0;
+  const int64_t bad = scan_batches(I, O, q, cap, lane, [&](int64_t stop, int64_t b, int64_t bMI, int64_t bMO) {
+    if (pp.has) {
+      const double t = __dadd_rn(prefill_time(pp.p, b, bMI), decode_time(pp.p, b, bMI, bMO));
+      tot.add(t);
+      if (lane == 0) times[nb] = t;
+    }
+    if (lane == 0) stops[nb] = stop;
+    ++nb;
+  });
+  if (bad >= 0) {
+    r.status = HS_ENTRY_INFEASIBLE_REQUEST;
+    r.bad_request = bad;
+  } else if (pp.has) {
+    const double total = tot.result();
+    if (tot.n == 0 || total == 0.0) {
+      r.status = HS_ENTRY_ZERO_DIVISION;
+      r.zero_div_int = tot.n == 0;
+    } else {
+      r.rate = __ddiv_rn(i2d(tok), total);
+      r.contribution = r.rate;
+    }
+  }
+  if (lane == 0) {
+    *out = r;
+    *n_batches = nb;
+  }
+}
+
+cudaError_t launch_plan_instance(double budget, int64_t per_token, const PlanParams& pp, const int32_t* d_I,
+                                 const int32_t* d_O, int64_t q, int64_t* d_stops, double* d_times, int64_t* d_nb,
+                                 hs_entry* d_out, cudaStream_t st) {
+  k_plan_instance<<<1, 32, 0, st>>>(budget, per_token, pp, d_I, d_O, q, d_stops, d_times, d_nb, d_out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_table_build(const EntryDesc* d_desc, int n, const SearchConst& sc, const int32_t* d_I,

@@ -284,3 +284,32 @@ def decode_time(params, batch_size: int, input_len: int, output_len: int) -> flo
     """Closed form of sum_{k=1..O} decode_iteration_time(I + k, b)."""
     s = output_len * input_len + output_len * (output_len + 1) / 2.0
     return (params.p5 * batch_size + params.p7) * s + (params.p6 * batch_size + params.p8) * output_len
+
+
+# ------------------------------------------------------ capacity.py helpers
+@dataclass
+class RunningTokens:
+    """capacity.py:34-55: live token sums of an instance's unfinished requests."""
+
+    input_sum: int = 0
+    predicted_output_sum: int = 0
+
+    def add(self, input_len: int, predicted_output_len: int) -> None:
+        self.input_sum += input_len
+        self.predicted_output_sum += predicted_output_len
+
+    def remove(self, input_len: int, predicted_output_len: int) -> None:
+        self.input_sum -= input_len
+        self.predicted_output_sum -= predicted_output_len
+        if self.input_sum < 0 or self.predicted_output_sum < 0:
+            raise SpecError("running token sums went negative; completion applied twice?")
+
+    def total(self) -> int:
+        return self.input_sum + self.predicted_output_sum
+
+
+def kv_usage(running, model, budget) -> float:
+    """capacity.py:98-106 (unclamped)."""
+    if budget.total_bytes <= 0:
+        raise SpecError(f"kv_usage needs a positive budget, got {budget.total_bytes}")
+    return kv_bytes_per_token(model) * running.total() / budget.total_bytes

@@ -33,8 +33,10 @@ from .domain import (
     InfeasibleRequestError,
     MachinePlacement,
     SpecError,
+    decode_time,
     enumerate_tp_degrees,
     kv_bytes_per_token,
+    prefill_time,
 )
 
 MAX_MATERIALISED = 1 << 22  # candidates search_optimal_config will turn into objects
@@ -209,6 +211,71 @@ def _entry_exception(cluster, requests, name: str, t: int, e) -> Exception:
     if st == nat.ENTRY_ZERO_DIVISION:
         return ZeroDivisionError("division by zero" if int(e["zero_div_int"]) else "float division by zero")
     raise AssertionError(f"entry status {st} is not an error")
+
+
+# ------------------------------------------------- single-instance planning
+@dataclass(frozen=True)
+class BatchPlan:
+    """planner.py:36-48: contiguous batches (half-open index ranges) and,
+    once timed, their seconds."""
+
+    batches: tuple = ()
+    per_batch_time: tuple = ()
+
+    @property
+    def total_time(self) -> float:
+        return sum(self.per_batch_time)
+
+
+def _plan_on_device(requests, budget, model, params, engine):
+    I, O = _lengths(requests)
+    per_token = kv_bytes_per_token(model)
+    p8 = None if params is None else [float(getattr(params, f"p{k}")) for k in range(1, 9)]
+    eng = engine or nat.engine_for()
+    stops, times, e = eng.plan_instance(float(budget.total_bytes), per_token, p8, I, O)
+    if int(e["status"]) == nat.ENTRY_INFEASIBLE_REQUEST:
+        r = requests[int(e["bad_request"])]
+        raise InfeasibleRequestError(
+            f"request {r.id!r} needs {per_token * (r.input_len + r.output_len):.0f} KV bytes alone, "
+            f"budget is {budget.total_bytes:.0f}",
+            request_id=r.id,
+        )
+    starts = [0] + [int(x) for x in stops[:-1]]
+    batches = tuple(zip(starts, (int(x) for x in stops)))
+    return batches, times, e
+
+
+def plan_static_batches(requests, budget, model, engine=None) -> BatchPlan:
+    """planner.py:51-87 on the GPU (K1's warp-cooperative greedy scan): the
+    largest KV-feasible contiguous batches, in order."""
+    batches, _times, _e = _plan_on_device(list(requests), budget, model, None, engine)
+    return BatchPlan(batches=batches)
+
+
+def estimate_batch_time(batch, params) -> float:
+    """planner.py:90-101 for one batch (host scalar helper)."""
+    if not batch:
+        raise SpecError("cannot time an empty batch")
+    b = len(batch)
+    max_i = max(r.input_len for r in batch)
+    max_o = max(r.output_len for r in batch)
+    return prefill_time(params, b, max_i) + decode_time(params, b, max_i, max_o)
+
+
+def time_batches(plan: BatchPlan, requests, params) -> BatchPlan:
+    """planner.py:104-106 (host scalar helper over the plan's batches)."""
+    requests = list(requests)
+    return BatchPlan(batches=plan.batches,
+                     per_batch_time=tuple(estimate_batch_time(requests[s:e], params) for s, e in plan.batches))
+
+
+def estimate_instance_throughput(requests, budget, model, params, engine=None) -> float:
+    """planner.py:109-118 on the GPU: plan, time and sum the static batches of
+    one instance (K1's scan with an explicit KV budget, hs_plan_instance)."""
+    _batches, _times, e = _plan_on_device(list(requests), budget, model, params, engine)
+    if int(e["status"]) == nat.ENTRY_ZERO_DIVISION:
+        raise ZeroDivisionError("division by zero" if int(e["zero_div_int"]) else "float division by zero")
+    return float(e["rate"])
 
 
 def _machine_estimate(name: str, t: int, e) -> MachineEstimate:

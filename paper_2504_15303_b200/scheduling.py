@@ -98,6 +98,42 @@ class OutputLengthPredictor:
         return np.clip(v, 1, self._max_output_len).astype(np.int64)
 
 
+def ideal_batch_size(request, budget, model) -> int:
+    """scheduling.py:119-128."""
+    if budget.total_bytes <= 0:
+        raise SpecError(f"ideal_batch_size needs a positive budget, got {budget.total_bytes}")
+    per_request = kv_bytes_per_token(model) * (request.input_len + request.predicted_output_len)
+    return max(1, int(budget.total_bytes // per_request))
+
+
+def request_oversized(request, budget, model) -> bool:
+    """scheduling.py:131-133."""
+    per_request = kv_bytes_per_token(model) * (request.input_len + request.predicted_output_len)
+    return per_request > budget.total_bytes
+
+
+def per_request_cost(params, request, batch_size: int) -> float:
+    """scheduling.py:136-147."""
+    from .domain import decode_time, prefill_time
+    if batch_size < 1:
+        raise SpecError(f"batch_size must be >= 1, got {batch_size}")
+    total = prefill_time(params, batch_size, request.input_len) + decode_time(
+        params, batch_size, request.input_len, request.predicted_output_len
+    )
+    if total <= 0:
+        raise SpecError(
+            f"non-positive batch time {total} for request {request.id!r}; latency parameters are corrupt"
+        )
+    return total / batch_size
+
+
+def workload(cost: float, usage: float, theta: float) -> float:
+    """scheduling.py:150-154."""
+    if theta <= 0:
+        raise SpecError(f"theta must be > 0, got {theta}")
+    return cost * math.exp(theta * usage)
+
+
 class Scheduler:
     """scheduling.py:175-346 Scheduler over the native hs_sched_* engine:
     choose() / complete() / evaluate() / snapshot() with the reference's

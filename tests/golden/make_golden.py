@@ -552,8 +552,45 @@ def build_sched_cases() -> list:
     return cases
 
 
+PLAN_CASES = [  # (name, seed, n, lo, hi, budget bytes, params scale) on a 7B model
+    ("typical", 1, 3000, 20, 900, 8.0e9, 1.0),
+    ("tight", 2, 500, 100, 4000, 4.5e9, 0.5),
+    ("one_batch", 3, 64, 1, 30, 1e13, 2.0),
+    ("empty", 4, 0, 1, 2, 1e9, 1.0),
+    ("infeasible", 5, 200, 10, 3300, 3.0e9, 1.0),
+    ("zero_time", 6, 40, 5, 50, 5e9, 0.0),
+    ("negative_budget", 7, 10, 5, 50, -1.0, 1.0),
+    ("ragged_budget", 8, 2000, 1, 2000, 1234567.89 * 4096, 1.7),
+]
+
+
+def build_plan_cases() -> list:
+    """planner.py:51-118 single-instance functions of the reference:
+    plan_static_batches, time_batches, estimate_instance_throughput."""
+    model = hs.ModelSpec(**wl.MODEL_7B)
+    out = []
+    for name, seed, n, lo, hi, budget, scale in PLAN_CASES:
+        rng = random.Random(seed)
+        reqs = [hs.Request(f"q{k}", rng.randint(lo, hi), rng.randint(lo, hi), 1) for k in range(n)]
+        params = hs.LatencyParams(*(scale * x for x in wl.RANK_BASE))
+        kb = hs.KvBudget(total_bytes=budget)
+        case = {"name": name, "seed": seed, "n": n, "lo": lo, "hi": hi, "budget": H(budget), "scale": H(scale)}
+        try:
+            plan = hs.plan_static_batches(reqs, kb, model)
+            case["batches"] = [list(b) for b in plan.batches]
+            case["times"] = [H(t) for t in hs.time_batches(plan, reqs, params).per_batch_time]
+        except (hs.HetserveError, ZeroDivisionError) as exc:
+            case["plan_error"] = [type(exc).__name__, str(exc)]
+        try:
+            case["rate"] = H(hs.estimate_instance_throughput(reqs, kb, model, params))
+        except (hs.HetserveError, ZeroDivisionError) as exc:
+            case["rate_error"] = [type(exc).__name__, str(exc)]
+        out.append(case)
+    return out
+
+
 def main() -> None:
-    which = sys.argv[1:] or ["exp", "search", "replay", "static", "wide", "streams", "sched"]
+    which = sys.argv[1:] or ["exp", "search", "replay", "static", "wide", "streams", "sched", "plan"]
     if "exp" in which:
         (OUT / "exp_vectors.json").write_text(json.dumps(build_exp_vectors()))
     if "search" in which:
@@ -568,6 +605,8 @@ def main() -> None:
         (OUT / "stream_cases.json").write_text(json.dumps(build_stream_cases()))
     if "sched" in which:
         (OUT / "sched_cases.json").write_text(json.dumps(build_sched_cases()))
+    if "plan" in which:
+        (OUT / "plan_cases.json").write_text(json.dumps(build_plan_cases()))
 
 
 if __name__ == "__main__":

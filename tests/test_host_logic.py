@@ -159,3 +159,53 @@ def test_workload_generators_match_reference_semantics():
     want = [t for _r, t in ref.generate_arrivals(trace, 37.5, 11)]
     assert wl.arrivals(3000, 37.5, 11).tolist() == want
     assert hs.simulator.arrival_times(3000, math.inf, 0).tolist() == [0.0] * 3000
+
+
+def test_scalar_helpers_match_reference():
+    """capacity.py / scheduling.py scalar helpers (host), against the
+    reference itself where it is importable."""
+    if not REF.exists():
+        pytest.skip("reference not present")
+    import sys
+    sys.path.insert(0, str(REF))
+    import hetserve as ref
+    import random
+    from paper_2504_15303_b200 import workloads as wl
+    rng = random.Random(3)
+    for mod in (hs, ref):
+        assert mod.ideal_batch_size and mod.per_request_cost and mod.workload and mod.kv_usage
+    for _ in range(300):
+        I, P = rng.randint(1, 5000), rng.randint(1, 5000)
+        budget = rng.uniform(-1e9, 1e11)
+        params = tuple(rng.uniform(-1e-4, 1e-3) for _ in range(8))
+        ours, theirs = [], []
+        for mod, out in ((hs, ours), (ref, theirs)):
+            model = mod.ModelSpec(**wl.MODEL_7B)
+            kb = mod.KvBudget(total_bytes=budget)
+            req = mod.Request("x", I, P, P)
+            lp = mod.LatencyParams(*params)
+            for fn in (lambda: mod.ideal_batch_size(req, kb, model),
+                       lambda: mod.request_oversized(req, kb, model),
+                       lambda: mod.per_request_cost(lp, req, rng_b),
+                       lambda: mod.workload(abs(params[0]) * 1e3, I / 5000, 2.0 + params[1]),
+                       lambda: mod.kv_usage(_running(mod, I, P), model, kb)):
+                try:
+                    v = fn()
+                    out.append(("ok", v.hex() if isinstance(v, float) else v))
+                except Exception as exc:  # noqa: BLE001
+                    out.append((type(exc).__name__, str(exc)))
+        assert ours == theirs
+    rt = hs.RunningTokens()
+    rt.add(3, 4)
+    rt.remove(3, 4)
+    with pytest.raises(hs.SpecError, match="completion applied twice"):
+        rt.remove(1, 0)
+
+
+rng_b = 7
+
+
+def _running(mod, i, p):
+    r = mod.RunningTokens()
+    r.add(i, p)
+    return r
