@@ -886,9 +886,16 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
     HS_CUDA(cudaEventSynchronize(c->ev_copy[0]));
     hs::ReplayConst rs = base;
     size_heaps(rs, inst, c->pinned_min[0], sq);
+    const size_t heap_bytes = (size_t)T * rs.heap_stride * hs::kHEntBytes;
+    size_t free_b = 0, total_b = 0;
+    HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (heap_bytes > free_b / 10 * 8) {  // all heaps at once do not fit: the chunked path below
+      HS_CUDA(cudaStreamSynchronize(c->stream));
+      goto chunked;
+    }
     HS_CUDA(cudaStreamWaitEvent(ks, c->ev_copy[0], 0));
     void* heap = nullptr;
-    HS_CUDA(cudaMallocAsync(&heap, (size_t)T * rs.heap_stride * hs::kHEntBytes, ks));
+    HS_CUDA(cudaMallocAsync(&heap, heap_bytes, ks));
     HS_CUDA(hs::launch_replay(rs, T, dOff, dI, dO, dP, dT, dA, dDep, dM, dR, dQ, static_cast<uint64_t*>(heap), ks,
                               nullptr, nullptr, nullptr, 0, 0, dProg, (int)L));
     c->launches += 1;
@@ -917,6 +924,7 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
       HS_CUDA(cudaMemcpyAsync(dSP, seeds->predictor_state, sizeof(hs_pcg64_state) * T, cudaMemcpyHostToDevice,
                               c->stream));
   }
+chunked:
   // Chunks of traces: copy chunk i on the copy stream while earlier chunks
   // replay on their own streams; each chunk sizes its heaps exactly from
   // its own min(I + O).
