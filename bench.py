@@ -467,6 +467,17 @@ def config5_arm(args, rank, world, local_rank):
     cluster, reqs, params, sI, sO = search_inputs(args.search_q)
     from paper_2504_15303_b200 import workloads as wl
     I1, O1 = wl.trace_lengths(args.q, seed=0)
+    tiles = {}
+
+    def tiled(n):
+        # every deployment replays the same trace: tiled once into page-locked buffers
+        if n not in tiles:
+            ti = eng.host_array((max(n * args.q, 1),), np.int32)
+            to = eng.host_array((max(n * args.q, 1),), np.int32)
+            ti[: n * args.q] = np.tile(I1, n)
+            to[: n * args.q] = np.tile(O1, n)
+            tiles[n] = (ti[: n * args.q], to[: n * args.q])
+        return tiles[n]
 
     def step():
         t = planner.build_tables(cluster, reqs, params, engine=eng)
@@ -499,8 +510,7 @@ def config5_arm(args, rank, world, local_rank):
         configs = [planner.deployment_of(t, int(i)) for i in top["index"][lo:hi]]
         n = hi - lo
         off = np.arange(n + 1, dtype=np.int64) * args.q
-        I = np.tile(I1, n)
-        O = np.tile(O1, n)
+        I, O = tiled(n)
         res = hs.replay_deployments(cluster, configs, params, hs.PolicyConfig(), np.arange(n), off, I, O, O,
                                     engine=eng, want_assign=False)
         assert (res.result["error"] == 0).all()

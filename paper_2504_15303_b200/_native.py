@@ -125,6 +125,8 @@ ENTRY_DTYPE = np.dtype([("contribution", "<f8"), ("rate", "<f8"), ("budget", "<f
 CAND_DTYPE = np.dtype([("total", "<f8"), ("index", "<i8")])
 METRICS_DTYPE = np.dtype([("completion_time", "<f8"), ("peak_kv_usage", "<f8"), ("residual_load", "<f8"),
                           ("request_count", "<i8"), ("token_count", "<i8")])
+INSTANCE_DTYPE = np.dtype([("p", "<f8", (8,)), ("budget", "<f8"), ("wrr_weight", "<f8"), ("type", "<i4"),
+                           ("_pad", "<i4")])
 PCG64_DTYPE = np.dtype([("state_hi", "<u8"), ("state_lo", "<u8"), ("inc_hi", "<u8"), ("inc_lo", "<u8"),
                         ("has_uint32", "<u4"), ("uinteger", "<u4")])
 RESULT_DTYPE = np.dtype([("error", "<i4"), ("err_instance", "<i4"), ("err_request", "<i8"), ("err_value", "<f8"),

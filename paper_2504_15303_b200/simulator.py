@@ -123,20 +123,27 @@ def _params_tuple(p) -> tuple:
 
 
 def engine_instances(handles, policy: PolicyConfig):
-    """hs_instance array: classes = bit-identical (params, budget)."""
+    """hs_instance array: classes = bit-identical (params, budget), numbered in
+    order of first appearance (the key is the bit pattern, so -0.0 and 0.0
+    stay distinct classes)."""
     n = len(handles)
     arr = (nat.hs_instance * max(n, 1))()
-    classes = {}
+    if n == 0:
+        return arr
+    pb = np.empty((n, 9), np.float64)
     for j, h in enumerate(handles):
-        pt = _params_tuple(h.params)
-        b = float(h.budget.total_bytes)
-        key = (tuple(x.hex() for x in pt), b.hex())
-        ty = classes.setdefault(key, len(classes))
-        for k in range(8):
-            arr[j].p[k] = pt[k]
-        arr[j].budget = b
-        arr[j].wrr_weight = float(policy.wrr_weights[j]) if policy.policy == "WRR" else 0.0
-        arr[j].type = ty
+        pb[j, :8] = _params_tuple(h.params)
+        pb[j, 8] = float(h.budget.total_bytes)
+    keys = np.ascontiguousarray(pb).view(np.uint64)
+    _, first, inverse = np.unique(keys, axis=0, return_index=True, return_inverse=True)
+    rank = np.empty(len(first), np.int64)
+    rank[np.argsort(first, kind="stable")] = np.arange(len(first))
+    view = np.frombuffer(arr, dtype=nat.INSTANCE_DTYPE, count=n)
+    view["p"] = pb[:, :8]
+    view["budget"] = pb[:, 8]
+    view["type"] = rank[np.asarray(inverse).reshape(-1)]
+    if policy.policy == "WRR":
+        view["wrr_weight"] = [float(policy.wrr_weights[j]) for j in range(n)]
     return arr
 
 
