@@ -410,6 +410,12 @@ def engine_arm(args, rank, world, local_rank):
     fp64_peak = eng.probe_fp64()
     cand_local = hi - lo
     k2_fp64 = 2.0 * cand_local / (k2 / 1e3)
+    # K3 against the FP64 pipe with the reference-literal op count of SURVEY
+    # section 8(d): OS scoring ~67 FP64 ops per instance per dispatch
+    # (divides, floordiv, prefill, decode, exp, min-max) + ~15 per step event
+    steps_per_req = n_steps_ev / max(nreq, 1)
+    k3_ops_per_dispatch = N * 67 + 15 * steps_per_req
+    k3_fp64 = k3_ops_per_dispatch * nreq / (k3 / 1e3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -438,6 +444,11 @@ def engine_arm(args, rank, world, local_rank):
             "roofline_k2": {"bound": "fp64", "achieved": k2_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
                             "frac": k2_fp64 / fp64_peak, "kernel": "k_search_best",
                             "peak_source": "hs_probe_fp64 DADD throughput measured in this run"},
+            "roofline_k3_fp64": {"bound": "fp64", "achieved": k3_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
+                                 "frac": k3_fp64 / fp64_peak, "kernel": "k_replay",
+                                 "ops_per_dispatch": k3_ops_per_dispatch,
+                                 "note": "reference-literal FP64 op count (SURVEY.md 8d: N*67 per dispatch + 15 per "
+                                         "step event); the kernel executes fewer (per-class pricing, O(N) min-max)"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "e2e": e2e,
