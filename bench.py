@@ -518,12 +518,11 @@ def config5_arm(args, rank, world, local_rank):
         else:
             top = cands
         lo, hi = shard_range(len(top), rank, world)
-        configs = [planner.deployment_of(t, int(i)) for i in top["index"][lo:hi]]
         n = hi - lo
         off = np.arange(n + 1, dtype=np.int64) * args.q
         I, O = tiled(n)
-        res = hs.replay_deployments(cluster, configs, params, hs.PolicyConfig(), np.arange(n), off, I, O, O,
-                                    engine=eng, want_assign=False)
+        res = hs.replay_candidates(t, params, top["index"][lo:hi], hs.PolicyConfig(), np.arange(n), off, I, O, O,
+                                   engine=eng, want_assign=False)
         assert (res.result["error"] == 0).all()
         return nf, ms_topk, res.kernel_ms, n
 

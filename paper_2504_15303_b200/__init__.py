@@ -82,6 +82,7 @@ from .simulator import (
     SimMetrics,
     build_instances,
     generate_arrivals,
+    replay_candidates,
     replay_deployments,
     replay_traces,
     run_continuous,

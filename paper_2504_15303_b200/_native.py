@@ -16,6 +16,7 @@ import numpy as np
 HS_MAX_DEGREES = 32
 HS_MAX_MACHINES = 64
 HS_MAX_INSTANCES = 128
+HS_MAX_CLASSES = 32
 
 # enums (hetserve_b200.h)
 HS_OK, HS_ERR_ARG, HS_ERR_CUDA, HS_ERR_UNSUPPORTED, HS_ERR_NOMEM = 0, 1, 2, 3, 4

@@ -387,3 +387,72 @@ def replay_deployments(cluster, configs, params, policy: PolicyConfig, trace_dep
                                         None if arrival is None else np.ascontiguousarray(arrival, np.float64),
                                         want_assign=want_assign, want_depart=want_depart)
     return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)
+
+
+def replay_candidates(tables, params_by_machine_tp, indices, policy: PolicyConfig, trace_deployment, offsets,
+                      input_len, output_len, pred_output_len, arrival=None, want_assign=True, want_depart=False,
+                      engine=None) -> ReplayBatchResult:
+    """BASELINE config 5 (search -> re-score): replay trace t on
+    candidate indices[trace_deployment[t]] of a search's tables, every
+    deployment in one launch.  The instance arrays are assembled straight from
+    the K1 table (budgets, instance counts per (machine, degree)) with numpy,
+    instead of DeploymentConfig / InstanceHandle objects per candidate; the
+    results equal replay_deployments on [deployment_of(tables, i) ...]."""
+    if policy.policy == "WRR":
+        raise SpecError("WRR weights are per instance: use replay_deployments")
+    idx = np.asarray(indices, np.int64)
+    M = len(tables.names)
+    nd = np.asarray(tables.n_degrees, np.int64)
+    ent = tables.entries
+    digs = np.empty((len(idx), M), np.int64)
+    x = idx.copy()
+    for m in range(M - 1, -1, -1):
+        digs[:, m] = x % nd[m]
+        x //= nd[m]
+    rows = np.arange(M)[None, :]
+    if M > nat.HS_MAX_CLASSES or (ent["status"][rows, digs] != nat.ENTRY_OK).any():
+        # not a set of feasible candidates: the object path raises the reference's errors
+        from .planner import deployment_of
+        configs = [deployment_of(tables, int(i)) for i in idx]
+        return replay_deployments(tables.cluster, configs, params_by_machine_tp, policy, trace_deployment, offsets,
+                                  input_len, output_len, pred_output_len, arrival, want_assign, want_depart, engine)
+    p8 = np.zeros((M, nat.HS_MAX_DEGREES, 8), np.float64)
+    for m, name in enumerate(tables.names):
+        for d, t in enumerate(tables.degrees[m]):
+            pr = params_by_machine_tp.get((name, t))
+            if pr is not None:
+                p8[m, d] = _params_tuple(pr)
+    counts = ent["instance_count"][rows, digs].astype(np.int64)  # [K, M]
+    n_per = counts.sum(axis=1)
+    if len(n_per) and n_per.max() > nat.HS_MAX_INSTANCES:
+        raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"{int(n_per.max())} instances (max {nat.HS_MAX_INSTANCES})")
+    inst_off = np.concatenate([[0], np.cumsum(n_per)]).astype(np.int32)
+    flat = counts.reshape(-1)
+    total = int(flat.sum())
+    arr = (nat.hs_instance * max(total, 1))()
+    view = np.frombuffer(arr, dtype=nat.INSTANCE_DTYPE, count=max(total, 1))[:total]
+    view["p"] = np.repeat(p8[rows, digs].reshape(-1, 8), flat, axis=0)
+    view["budget"] = np.repeat(ent["budget"][rows, digs].reshape(-1), flat)
+    # instance classes = bit-identical (params, budget) within each deployment,
+    # numbered densely per deployment (as engine_instances does)
+    key = np.concatenate([p8, ent["budget"][:, :, None].astype(np.float64)], axis=2)  # [M, D, 9]
+    _, gid = np.unique(np.ascontiguousarray(key).view(np.uint64).reshape(-1, 9), axis=0, return_inverse=True)
+    g = np.asarray(gid).reshape(M, nat.HS_MAX_DEGREES)[rows, digs]  # [K, M] global class ids
+    order = np.argsort(g, axis=1, kind="stable")
+    gs = np.take_along_axis(g, order, axis=1)
+    dense_sorted = np.concatenate([np.zeros((len(idx), 1), np.int64),
+                                   np.cumsum(gs[:, 1:] != gs[:, :-1], axis=1)], axis=1)
+    dense = np.empty_like(dense_sorted)
+    np.put_along_axis(dense, order, dense_sorted, axis=1)
+    view["type"] = np.repeat(dense.reshape(-1).astype(np.int32), flat)
+    per_token = kv_bytes_per_token(tables.cluster.model)
+    eng = engine or nat.engine_for()
+    pol = _policy_struct(policy, 0, per_token, 0)
+    a, d, m, r = eng.replay_deployments(arr, inst_off, pol, np.asarray(trace_deployment, np.int32),
+                                        np.ascontiguousarray(offsets, np.int64),
+                                        np.ascontiguousarray(input_len, np.int32),
+                                        np.ascontiguousarray(output_len, np.int32),
+                                        np.ascontiguousarray(pred_output_len, np.int32),
+                                        None if arrival is None else np.ascontiguousarray(arrival, np.float64),
+                                        want_assign=want_assign, want_depart=want_depart)
+    return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)

@@ -379,3 +379,27 @@ def test_config5_full_size_rescore_vs_oracle(eng):
         assert int(res.result[d]["error"]) == 0 == int(r[0]["error"])
         assert np.array_equal(res.assign[sl], a)
         assert np.array_equal(res.depart[sl].view(np.uint64), dep.view(np.uint64))
+
+
+def test_replay_candidates_equals_object_path(eng):
+    """replay_candidates (instance arrays assembled from the K1 table with
+    numpy) == replay_deployments on deployment_of(...) objects, bit for bit."""
+    _case, _req, t = _config3_tables(eng)
+    top, _nf, _ = planner.search_topk(t, 40, engine=eng)
+    idx = top["index"]
+    p3 = wl.config3()
+    params = {k: hs.LatencyParams(*v) for k, v in p3.params.items()}
+    q = 2048
+    I1, O1 = wl.trace_lengths(q, seed=5)
+    n = len(idx)
+    off = np.arange(n + 1, dtype=np.int64) * q
+    I, O = np.tile(I1, n), np.tile(O1, n)
+    for pol in (hs.PolicyConfig(), hs.PolicyConfig(policy="MB"), hs.PolicyConfig(policy="RR")):
+        a = hs.replay_candidates(t, params, idx, pol, np.arange(n), off, I, O, O, want_depart=True, engine=eng)
+        b = hs.replay_deployments(t.cluster, [planner.deployment_of(t, int(i)) for i in idx], params, pol,
+                                  np.arange(n), off, I, O, O, want_depart=True, engine=eng)
+        assert (b.result["error"] == 0).all()
+        assert np.array_equal(a.assign, b.assign)
+        assert np.array_equal(a.depart.view(np.uint64), b.depart.view(np.uint64))
+        assert a.metrics.tobytes() == b.metrics.tobytes()
+        assert a.result.tobytes() == b.result.tobytes()
