@@ -129,7 +129,7 @@ int build_space(const hs_entry* table, const int32_t* nd, int32_t M, hs::SpaceDe
                 int64_t* P) {
   if (M < 1 || M > HS_MAX_MACHINES) return fail(HS_ERR_ARG, "n_machines out of range");
   std::memset(sd, 0, sizeof(*sd));
-  const int off = M >= 3 ? 0 : 3 - M;
+  const int off = M >= 4 ? 0 : 4 - M;
   sd->M = M + off;
   for (int v = 0; v < off; ++v) {
     sd->D[v] = 1;
@@ -540,7 +540,7 @@ int hs_search_best(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
   int64_t P;
   if ((rc = build_space(table, n_degrees, M, &sd, &m_off, &P))) return rc;
   if (begin < 0 || end > P || begin > end) return fail(HS_ERR_ARG, "index range outside the candidate space");
-  const int64_t Din = (int64_t)sd.D[sd.M - 3] * sd.D[sd.M - 2] * sd.D[sd.M - 1];
+  const int64_t Din = (int64_t)sd.D[sd.M - 4] * sd.D[sd.M - 3] * sd.D[sd.M - 2] * sd.D[sd.M - 1];
   const int64_t items = (end - begin) / Din + 2;
   int blocks = hs::sm_count() * 8;
   const int64_t need_blocks = (items + 255) / 256;

@@ -26,10 +26,10 @@ struct SearchConst {
   int64_t q;
 };
 
-// Product space for K2: machines padded to M >= 3 (leading virtual
+// Product space for K2: machines padded to M >= 4 (leading virtual
 // machines with one degree and contribution +0.0 leave every total
 // unchanged: (0.0 + 0.0) + C0 == 0.0 + C0).
-constexpr int kMaxM = HS_MAX_MACHINES + 2;
+constexpr int kMaxM = HS_MAX_MACHINES + 3;
 struct SpaceDesc {
   int32_t M;
   int32_t D[kMaxM];

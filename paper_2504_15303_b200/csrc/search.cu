@@ -225,12 +225,12 @@ cudaError_t launch_table_build(const EntryDesc* d_desc, int n, const SearchConst
 // ----------------------------------------------------------------- K2
 __constant__ SpaceDesc c_space;
 
-// Levels of the product space (SpaceDesc is padded to M >= 3):
-//   outer  machines 0 .. M-4   odometer, once per item (prefix sums kept)
-//   mid    machine  M-3        runtime loop, contributions in shared memory
+// Levels of the product space (SpaceDesc is padded to M >= 4):
+//   outer  machines 0 .. M-5   odometer, once per item (prefix sums kept)
+//   mid    machines M-4, M-3   runtime loops, contributions in shared memory
 //   inner1 machine  M-2        compile-time radix D1 (registers)
 //   inner2 machine  M-1        compile-time radix DL (registers)
-// An item = one outer prefix = D2*D1*DL candidates.  Per candidate the fast
+// An item = one outer prefix = D3*D2*D1*DL candidates.  Per candidate the fast
 // path issues one DADD (prefix + last contribution, the reference's own
 // left-to-right order) and one DSETP.GT.OR into the `hit` predicate.
 // h |= (v > b) as one DSETP.GT.OR per candidate (left to nvcc, a run of
@@ -251,23 +251,28 @@ struct Radix {
 // candidates outside [lo, hi) (item-relative) are skipped.
 __device__ __noinline__ void item_scan(const double* sC, int M, double s, bool prefix_ok, int64_t base, int64_t lo,
                                        int64_t hi, double& best, int64_t& bidx, int64_t& cnt, bool count) {
-  const int D2 = c_space.D[M - 3], D1 = c_space.D[M - 2], DL = c_space.D[M - 1];
+  const int D3 = c_space.D[M - 4], D2 = c_space.D[M - 3], D1 = c_space.D[M - 2], DL = c_space.D[M - 1];
+  const double* C3 = &sC[(M - 4) * HS_MAX_DEGREES];
   const double* C2 = &sC[(M - 3) * HS_MAX_DEGREES];
   const double* C1 = &sC[(M - 2) * HS_MAX_DEGREES];
   const double* CL = &sC[(M - 1) * HS_MAX_DEGREES];
   int64_t c = 0;
-  for (int d2 = 0; d2 < D2; ++d2) {
-    const double s2 = __dadd_rn(s, C2[d2]);
-    for (int d1 = 0; d1 < D1; ++d1) {
-      const double v1 = __dadd_rn(s2, C1[d1]);
-      for (int dl = 0; dl < DL; ++dl, ++c) {
-        if (c < lo || c >= hi) continue;
-        const double v = __dadd_rn(v1, CL[dl]);
-        const bool ok = prefix_ok && C2[d2] != -INFINITY && C1[d1] != -INFINITY && CL[dl] != -INFINITY;
-        if (count && ok) ++cnt;
-        if (ok && v > best) {
-          best = v;
-          bidx = base + c;
+  for (int d3 = 0; d3 < D3; ++d3) {
+    const double s3 = __dadd_rn(s, C3[d3]);
+    for (int d2 = 0; d2 < D2; ++d2) {
+      const double s2 = __dadd_rn(s3, C2[d2]);
+      for (int d1 = 0; d1 < D1; ++d1) {
+        const double v1 = __dadd_rn(s2, C1[d1]);
+        for (int dl = 0; dl < DL; ++dl, ++c) {
+          if (c < lo || c >= hi) continue;
+          const double v = __dadd_rn(v1, CL[dl]);
+          const bool ok = prefix_ok && C3[d3] != -INFINITY && C2[d2] != -INFINITY && C1[d1] != -INFINITY &&
+                          CL[dl] != -INFINITY;
+          if (count && ok) ++cnt;
+          if (ok && v > best) {
+            best = v;
+            bidx = base + c;
+          }
         }
       }
     }
@@ -284,9 +289,11 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
   const int M = c_space.M;
   for (int k = threadIdx.x; k < M * HS_MAX_DEGREES; k += blockDim.x) sC[k] = c_space.C[k];
   __syncthreads();
-  const int D2 = c_space.D[M - 3];
-  const int64_t Din = (int64_t)D2 * c_space.D[M - 2] * c_space.D[M - 1];
-  const int64_t inner_ok = c_space.okcnt[M - 3] * c_space.okcnt[M - 2] * c_space.okcnt[M - 1];
+  const int D3 = c_space.D[M - 4], D2 = c_space.D[M - 3];
+  const int64_t Din = (int64_t)D3 * D2 * c_space.D[M - 2] * c_space.D[M - 1];
+  const int64_t inner_ok =
+      c_space.okcnt[M - 4] * c_space.okcnt[M - 3] * c_space.okcnt[M - 2] * c_space.okcnt[M - 1];
+  const double* C3 = &sC[(M - 4) * HS_MAX_DEGREES];
   const double* C2 = &sC[(M - 3) * HS_MAX_DEGREES];
   constexpr int R1 = D1 > 0 ? D1 : 1, RL = DL > 0 ? DL : 1;
   double C1[R1], CL[RL];
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
   int64_t it_end = it + chunk;
   if (it_end > item_end) it_end = item_end;
   if (it < it_end) {
-    const int nouter = M - 3;  // machines 0 .. nouter-1
+    const int nouter = M - 4;  // machines 0 .. nouter-1
     int32_t dig[kMaxM];
     double ps[kMaxM];  // ps[i] = left-to-right sum of machines 0..i
     int64_t x = it;
@@ -324,24 +331,30 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
       } else {
         unsigned hit = 0;
         if (Radix<D1, DL>::kStatic) {
-          for (int d2 = 0; d2 < D2; ++d2) {
-            const double s2 = __dadd_rn(s, C2[d2]);
+          for (int d3 = 0; d3 < D3; ++d3) {
+            const double s3 = __dadd_rn(s, C3[d3]);
+            for (int d2 = 0; d2 < D2; ++d2) {
+              const double s2 = __dadd_rn(s3, C2[d2]);
 #pragma unroll
-            for (int d1 = 0; d1 < R1; ++d1) {
-              const double v1 = __dadd_rn(s2, C1[d1]);
+              for (int d1 = 0; d1 < R1; ++d1) {
+                const double v1 = __dadd_rn(s2, C1[d1]);
 #pragma unroll
-              for (int dl = 0; dl < RL; ++dl) gt_or(__dadd_rn(v1, CL[dl]), best, hit);
+                for (int dl = 0; dl < RL; ++dl) gt_or(__dadd_rn(v1, CL[dl]), best, hit);
+              }
             }
           }
         } else {
           const int rD1 = c_space.D[M - 2], rDL = c_space.D[M - 1];
           const double* g1 = &sC[(M - 2) * HS_MAX_DEGREES];
           const double* gl = &sC[(M - 1) * HS_MAX_DEGREES];
-          for (int d2 = 0; d2 < D2; ++d2) {
-            const double s2 = __dadd_rn(s, C2[d2]);
-            for (int d1 = 0; d1 < rD1; ++d1) {
-              const double v1 = __dadd_rn(s2, g1[d1]);
-              for (int dl = 0; dl < rDL; ++dl) gt_or(__dadd_rn(v1, gl[dl]), best, hit);
+          for (int d3 = 0; d3 < D3; ++d3) {
+            const double s3 = __dadd_rn(s, C3[d3]);
+            for (int d2 = 0; d2 < D2; ++d2) {
+              const double s2 = __dadd_rn(s3, C2[d2]);
+              for (int d1 = 0; d1 < rD1; ++d1) {
+                const double v1 = __dadd_rn(s2, g1[d1]);
+                for (int dl = 0; dl < rDL; ++dl) gt_or(__dadd_rn(v1, gl[dl]), best, hit);
+              }
             }
           }
         }
@@ -472,7 +485,7 @@ cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, 
   if (e != cudaSuccess) return e;
   const int threads = 256;
   const int M = sd.M;
-  const int64_t Din = (int64_t)sd.D[M - 3] * sd.D[M - 2] * sd.D[M - 1];
+  const int64_t Din = (int64_t)sd.D[M - 4] * sd.D[M - 3] * sd.D[M - 2] * sd.D[M - 1];
   const int64_t item_begin = begin / Din;
   const int64_t item_end = end > begin ? (end + Din - 1) / Din : item_begin;
   const int64_t n_items = item_end - item_begin;
