@@ -302,11 +302,14 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
   size_heaps(rc, inst, min_need, max_q);
   void* d_qrec;
   if ((rcode = ensure(c, S_WREC, (size_t)(h_off[T] > 0 ? h_off[T] : 1) * hs::kQRecBytes, &d_qrec))) return rcode;
-  size_t free_b = 0, tot_b = 0;
-  HS_CUDA(cudaMemGetInfo(&free_b, &tot_b));
   const size_t per_trace = (size_t)rc.heap_stride * hs::kHEntBytes;
-  size_t budget_b = (size_t)((double)(free_b + c->cap[S_HEAP]) * 0.6);
-  int64_t chunk = per_trace ? (int64_t)(budget_b / per_trace) : T;
+  int64_t chunk = T;
+  if ((size_t)T * per_trace > c->cap[S_HEAP]) {  // query free memory only when the heap buffer must grow
+    size_t free_b = 0, tot_b = 0;
+    HS_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+    const size_t budget_b = (size_t)((double)(free_b + c->cap[S_HEAP]) * 0.6);
+    chunk = per_trace ? (int64_t)(budget_b / per_trace) : T;
+  }
   if (chunk < 1) chunk = 1;
   if (chunk > T) chunk = T;
   if (chunk > 16384) chunk = 16384;
@@ -887,15 +890,17 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
     hs::ReplayConst rs = base;
     size_heaps(rs, inst, c->pinned_min[0], sq);
     const size_t heap_bytes = (size_t)T * rs.heap_stride * hs::kHEntBytes;
-    size_t free_b = 0, total_b = 0;
-    HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (heap_bytes > free_b / 10 * 8) {  // all heaps at once do not fit: the chunked path below
+    HS_CUDA(cudaStreamWaitEvent(ks, c->ev_copy[0], 0));
+    void* heap = nullptr;
+    // (cudaMemGetInfo costs milliseconds per call: try the allocation instead)
+    const cudaError_t ae = cudaMallocAsync(&heap, heap_bytes, ks);
+    if (ae == cudaErrorMemoryAllocation) {  // all heaps at once do not fit: the chunked path below
+      (void)cudaGetLastError();
+      HS_CUDA(cudaStreamSynchronize(ks));
       HS_CUDA(cudaStreamSynchronize(c->stream));
       goto chunked;
     }
-    HS_CUDA(cudaStreamWaitEvent(ks, c->ev_copy[0], 0));
-    void* heap = nullptr;
-    HS_CUDA(cudaMallocAsync(&heap, heap_bytes, ks));
+    HS_CUDA(ae);
     HS_CUDA(hs::launch_replay(rs, T, dOff, dI, dO, dP, dT, dA, dDep, dM, dR, dQ, static_cast<uint64_t*>(heap), ks,
                               nullptr, nullptr, nullptr, 0, 0, dProg, (int)L));
     c->launches += 1;
