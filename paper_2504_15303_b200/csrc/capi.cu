@@ -836,7 +836,7 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
   for (int64_t t = 1; equal && t <= T; ++t) equal = off[t] == t * sq;
   const WriteValue32Fn wv = equal ? write_value32() : nullptr;
   if (wv) {
-    constexpr int64_t kPhases = 8;
+    constexpr int64_t kPhases = 16;
     const int64_t L = ((sq + kPhases - 1) / kPhases + 31) / 32 * 32;
     const int64_t nphase = (sq + L - 1) / L;
     uint32_t* dProg;
