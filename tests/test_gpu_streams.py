@@ -228,3 +228,37 @@ def test_streamed_replay_equals_chunked(eng, seeded, monkeypatch):
     assert np.array_equal(got.depart.view(np.uint64), want.depart.view(np.uint64))
     assert got.metrics.tobytes() == want.metrics.tobytes()
     assert got.result.tobytes() == want.result.tobytes()
+
+
+def test_streamed_replay_redoes_when_phase0_sizing_is_too_small(eng, monkeypatch):
+    """Phase 0 of every trace holds only huge requests, so min(I + O) over
+    phase 0 (which sizes the streamed heaps) is far above the rest; at rate
+    inf the later tiny requests pile up beyond that capacity, the kernel
+    reports CAPACITY and the call is redone on the exactly sized chunked path.
+    The result must equal the chunked path's."""
+    prof = wl.config1()
+    cluster = hs.ClusterSpec(hs.ModelSpec(**prof.model), hs.EngineOverheads(**prof.engine),
+                             tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+                             hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {"v100": 1, "a800": 1})
+    nT, q = 4, 512
+    I = np.ones((nT, q), np.int32)
+    O = np.ones((nT, q), np.int32)
+    I[:, :32], O[:, :32] = 2000, 2000
+    I, O = I.reshape(-1), O.reshape(-1)
+    off = np.arange(nT + 1, dtype=np.int64) * q
+    pol = hs.PolicyConfig()
+    n0 = eng.launch_count
+    got = hs.replay_traces(cluster, config, params, pol, off, I, O, O, want_assign=True, want_depart=True,
+                           engine=eng)
+    n1 = eng.launch_count
+    monkeypatch.setenv("HS_NO_STREAM", "1")
+    want = hs.replay_traces(cluster, config, params, pol, off, I, O, O, want_assign=True, want_depart=True,
+                            engine=eng)
+    # streamed attempt (phase-0 sizing + replay) then the chunked redo's launches
+    assert n1 - n0 == 2 + (eng.launch_count - n1)
+    assert (want.result["error"] == 0).all() and (got.result["error"] == 0).all()
+    assert np.array_equal(got.assign, want.assign)
+    assert np.array_equal(got.depart.view(np.uint64), want.depart.view(np.uint64))
+    assert got.metrics.tobytes() == want.metrics.tobytes()
