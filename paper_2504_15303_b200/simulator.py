@@ -34,7 +34,7 @@ from .domain import (
     kv_budget,
     kv_bytes_per_token,
 )
-from .scheduling import InstanceHandle, OutputLengthPredictor, PolicyConfig, PredictorConfig
+from .scheduling import InstanceHandle, OutputLengthPredictor, PolicyConfig
 
 
 @dataclass(frozen=True)

@@ -9,9 +9,7 @@ import time
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-sys.path.insert(0, str(ROOT / "tests"))
 
-import helpers as H  # noqa: E402
 import paper_2504_15303_b200 as hs  # noqa: E402
 from paper_2504_15303_b200 import simulator  # noqa: E402
 from paper_2504_15303_b200 import workloads as wl  # noqa: E402

@@ -6,7 +6,6 @@ import pathlib
 import sys
 import time
 
-import numpy as np
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
