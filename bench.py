@@ -442,7 +442,10 @@ def engine_arm(args, rank, world, local_rank):
                          "note": "replay is latency-bound (dependent event chains); see DESIGN.md"},
             "roofline_k2": {"bound": "fp64", "achieved": k2_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
                             "frac": k2_fp64 / fp64_peak, "kernel": "k_search_best",
-                            "peak_source": "hs_probe_fp64 DADD throughput measured in this run"},
+                            "peak_source": "hs_probe_fp64 DADD throughput measured in this run",
+                            "note": "algorithmic count: 2 ops per candidate (the left-to-right add and the "
+                                    "compare, SURVEY.md 8d); in non-negative spaces the kernel runs the "
+                                    "compare as an integer test on the total's high word (ALU pipe)"},
             "roofline_k3_fp64": {"bound": "fp64", "achieved": k3_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
                                  "frac": k3_fp64 / fp64_peak, "kernel": "k_replay",
                                  "ops_per_dispatch": k3_ops_per_dispatch,

@@ -21,6 +21,8 @@
 //
 // k_search_score: per-candidate total + first failing machine, for the full
 //   ranking of small spaces (sorted afterwards with CUB).
+#include <cmath>
+
 #include <cub/cub.cuh>
 
 #include "hs_device.cuh"
@@ -242,6 +244,25 @@ __device__ __forceinline__ void gt_or(double v, double b, unsigned& h) {
       : "d"(v), "d"(b));
 }
 
+// Non-negative spaces (every OK contribution has a clear sign bit and is not
+// NaN, checked on the host): every feasible total is >= +0.0, and for such
+// doubles the high 32-bit word is monotone in the value, so
+// h |= hi(v) >= thr with thr = max(hi(best), 0) never misses a v > best; it
+// may report equal-high-word candidates (and NaN totals), which only send the
+// item to the exact in-order re-scan.  One ISETP on the integer pipe instead
+// of a DSETP on the half-rate FP64 pipe; infeasible totals (-inf) have a
+// negative high word and never hit.
+__device__ __forceinline__ void ge_or_hi(double v, int32_t thr, unsigned& h) {
+  asm("{\n\t.reg .pred p, q;\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tsetp.ne.u32 q, %0, 0;\n\t"
+      "setp.ge.or.s32 p, hi, %2, q;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "+r"(h)
+      : "d"(v), "r"(thr));
+}
+__device__ __forceinline__ int32_t hi_threshold(double best) {
+  const int32_t hb = (int32_t)(__double_as_longlong(best) >> 32);
+  return hb > 0 ? hb : 0;
+}
+
 template <int D1, int DL>
 struct Radix {
   static constexpr bool kStatic = D1 > 0 && DL > 0;
@@ -279,8 +300,8 @@ __device__ __noinline__ void item_scan(const double* sC, int M, double s, bool p
   }
 }
 
-template <int D1, int DL>
-__global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t item_end, int64_t begin,
+template <int D1, int DL, bool NN>
+__global__ void __launch_bounds__(256, 3) k_search_best(int64_t item_begin, int64_t item_end, int64_t begin,
                                                      int64_t end, int64_t chunk, double* blk_best,
                                                      int64_t* blk_idx, int64_t* blk_cnt) {
   __shared__ double sC[kMaxM * HS_MAX_DEGREES];
@@ -303,6 +324,7 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
   for (int d = 0; d < RL; ++d) CL[d] = sC[(M - 1) * HS_MAX_DEGREES + d];
 
   double best = -INFINITY;
+  int32_t thr = 0;  // NN: hi_threshold(best)
   int64_t bidx = -1, cnt = 0;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t it = item_begin + tid * chunk;
@@ -328,8 +350,11 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
       const int64_t base = it * Din;
       if (base < begin || base + Din > end) {
         item_scan(sC, M, s, prefix_ok, base, begin - base, end - base, best, bidx, cnt, true);
+        if (NN) thr = hi_threshold(best);
       } else {
-        unsigned hit = 0;
+        // four independent hit accumulators: one predicate chain would
+        // serialise every compare on the previous one's result
+        unsigned hit = 0, h4[4] = {0u, 0u, 0u, 0u};
         if (Radix<D1, DL>::kStatic) {
           for (int d3 = 0; d3 < D3; ++d3) {
             const double s3 = __dadd_rn(s, C3[d3]);
@@ -339,7 +364,10 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
               for (int d1 = 0; d1 < R1; ++d1) {
                 const double v1 = __dadd_rn(s2, C1[d1]);
 #pragma unroll
-                for (int dl = 0; dl < RL; ++dl) gt_or(__dadd_rn(v1, CL[dl]), best, hit);
+                for (int dl = 0; dl < RL; ++dl) {
+                  if (NN) ge_or_hi(__dadd_rn(v1, CL[dl]), thr, h4[(d1 * RL + dl) & 3]);
+                  else gt_or(__dadd_rn(v1, CL[dl]), best, h4[(d1 * RL + dl) & 3]);
+                }
               }
             }
           }
@@ -353,12 +381,19 @@ __global__ void __launch_bounds__(256) k_search_best(int64_t item_begin, int64_t
               const double s2 = __dadd_rn(s3, C2[d2]);
               for (int d1 = 0; d1 < rD1; ++d1) {
                 const double v1 = __dadd_rn(s2, g1[d1]);
-                for (int dl = 0; dl < rDL; ++dl) gt_or(__dadd_rn(v1, gl[dl]), best, hit);
+                for (int dl = 0; dl < rDL; ++dl) {
+                  if (NN) ge_or_hi(__dadd_rn(v1, gl[dl]), thr, hit);
+                  else gt_or(__dadd_rn(v1, gl[dl]), best, hit);
+                }
               }
             }
           }
         }
-        if (hit) item_scan(sC, M, s, prefix_ok, base, 0, Din, best, bidx, cnt, false);
+        hit |= (h4[0] | h4[1]) | (h4[2] | h4[3]);
+        if (hit) {
+          item_scan(sC, M, s, prefix_ok, base, 0, Din, best, bidx, cnt, false);
+          if (NN) thr = hi_threshold(best);
+        }
         if (prefix_ok) cnt += inner_ok;
       }
       // odometer over the outer digits, recomputing the changed prefix sums
@@ -462,8 +497,9 @@ constexpr int kMaxStaticRadix = 6;
 
 template <int D1, int DL>
 struct BestTable {
-  static void fill(BestKernel (&t)[kMaxStaticRadix + 1][kMaxStaticRadix + 1]) {
-    t[D1][DL] = k_search_best<D1, DL>;
+  static void fill(BestKernel (&t)[2][kMaxStaticRadix + 1][kMaxStaticRadix + 1]) {
+    t[0][D1][DL] = k_search_best<D1, DL, false>;
+    t[1][D1][DL] = k_search_best<D1, DL, true>;
     if constexpr (DL < kMaxStaticRadix) {
       BestTable<D1, DL + 1>::fill(t);
     } else if constexpr (D1 < kMaxStaticRadix) {
@@ -475,7 +511,7 @@ struct BestTable {
 cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, int blocks, double* d_blk_best,
                                int64_t* d_blk_idx, int64_t* d_blk_cnt, hs_cand* d_out, int64_t* d_cnt_out,
                                cudaStream_t st) {
-  static BestKernel table[kMaxStaticRadix + 1][kMaxStaticRadix + 1] = {};
+  static BestKernel table[2][kMaxStaticRadix + 1][kMaxStaticRadix + 1] = {};
   static bool filled = false;
   if (!filled) {
     BestTable<1, 1>::fill(table);
@@ -493,8 +529,18 @@ cudaError_t launch_search_best(const SpaceDesc& sd, int64_t begin, int64_t end, 
   int64_t chunk = (n_items + nthreads - 1) / nthreads;
   if (chunk < 1) chunk = 1;
   const int D1 = sd.D[M - 2], DL = sd.D[M - 1];
-  BestKernel k = k_search_best<0, 0>;
-  if (D1 <= kMaxStaticRadix && DL <= kMaxStaticRadix) k = table[D1][DL];
+  // non-negative space: every OK contribution has a clear sign bit and is not NaN
+  bool nn = true;
+  for (int i = 0; i < M && nn; ++i)
+    for (int d = 0; d < sd.D[i]; ++d) {
+      const double c = sd.C[i * HS_MAX_DEGREES + d];
+      if (c != -INFINITY && (std::signbit(c) || std::isnan(c))) {
+        nn = false;
+        break;
+      }
+    }
+  BestKernel k = nn ? k_search_best<0, 0, true> : k_search_best<0, 0, false>;
+  if (D1 <= kMaxStaticRadix && DL <= kMaxStaticRadix) k = table[nn ? 1 : 0][D1][DL];
   k<<<blocks, threads, 0, st>>>(item_begin, item_end, begin, end, chunk, d_blk_best, d_blk_idx, d_blk_cnt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
