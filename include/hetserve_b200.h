@@ -287,9 +287,10 @@ int hs_search_topk(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees,
 
 /* ---- batched scheduler replay ------------------------------------------ */
 /* Replay every trace of the batch on the same instance set.  assign
- * ([total requests], may be NULL) receives the chosen instance per request;
- * depart ([total requests], may be NULL) the departure time; metrics is
- * [n_traces][n_instances]; result is [n_traces]. */
+ * ([total requests], may be NULL) receives the chosen instance per request
+ * (page-locked, device-mapped memory -- e.g. hs_host_alloc -- is written by the
+ * kernel in place while it runs); depart ([total requests], may be NULL) the
+ * departure time; metrics is [n_traces][n_instances]; result is [n_traces]. */
 int hs_replay(hs_ctx* ctx, const hs_instance* instances, const hs_policy* policy,
               const hs_trace_batch* batch, uint8_t* assign, double* depart,
               hs_inst_metrics* metrics, hs_trace_result* result);

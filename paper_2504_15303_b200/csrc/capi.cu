@@ -767,6 +767,20 @@ WriteValue32Fn write_value32() {
   return fn;
 }
 
+// The device address of a page-locked, device-mapped host buffer (nullptr for
+// pageable memory): the replay then writes the assignments straight into the
+// caller's buffer while it runs -- one 32-byte store per warp per 32 requests
+// -- instead of a device buffer copied back after the kernel.
+uint8_t* mapped_host(uint8_t* host) {
+  if (!host) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer ? static_cast<uint8_t*>(a.devicePointer) : nullptr;
+}
+
 int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const hs_trace_batch* b,
                 const hs_replay_seeds* seeds, uint8_t* assign, double* depart, hs_inst_metrics* metrics,
                 hs_trace_result* result) {
@@ -820,7 +834,12 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
     return rc;
   }
   if ((b->arrival || gen_arr) && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
-  if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
+  uint8_t* const zA = mapped_host(assign);
+  if (zA) {
+    dA = zA;
+  } else if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) {
+    return rc;
+  }
   if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
   HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
   // Streamed replay (equal-length traces, the batched-replay shape): every
@@ -912,7 +931,7 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
     if ((rc = end_timing(c))) return rc;
     HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * N, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
-    if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
+    if (assign && !zA && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
     if (depart && total > 0)
       HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaStreamSynchronize(c->stream));
@@ -1013,7 +1032,7 @@ chunked:
     HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * N, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
   }
-  if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
+  if (assign && !zA && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
   if (depart && total > 0)
     HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));

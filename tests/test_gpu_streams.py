@@ -262,3 +262,27 @@ def test_streamed_replay_redoes_when_phase0_sizing_is_too_small(eng, monkeypatch
     assert np.array_equal(got.assign, want.assign)
     assert np.array_equal(got.depart.view(np.uint64), want.depart.view(np.uint64))
     assert got.metrics.tobytes() == want.metrics.tobytes()
+
+
+@pytest.mark.parametrize("ragged", [False, True])
+def test_pinned_assign_written_in_place(eng, ragged):
+    """A page-locked `assign_out` is written by the replay kernel itself while
+    it runs (zero-copy, no copy back after the kernel); the assignments equal
+    those of the pageable-buffer replay on the streamed (equal lengths) and the
+    chunked (ragged) host paths."""
+    cluster, params, config = _config4()
+    lens = [1500 + (53 * t if ragged else 0) for t in range(24)]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    I = np.concatenate([wl.trace_lengths(q, seed=300 + t)[0] for t, q in enumerate(lens)])
+    O = np.concatenate([wl.trace_lengths(q, seed=300 + t)[1] for t, q in enumerate(lens)])
+    aseeds = [42 + t for t in range(len(lens))]
+    pol = hs.PolicyConfig()
+    want = hs.replay_traces(cluster, config, params, pol, off, I, O, O, want_assign=True, engine=eng, rate=140.0,
+                            arrival_seeds=aseeds)
+    hA = eng.host_array((len(I),), np.uint8)
+    hA[:] = 255
+    got = hs.replay_traces(cluster, config, params, pol, off, I, O, O, want_assign=True, assign_out=hA,
+                           engine=eng, rate=140.0, arrival_seeds=aseeds)
+    assert (want.result["error"] == 0).all() and (got.result["error"] == 0).all()
+    assert np.array_equal(hA, want.assign[:len(I)])
+    assert got.metrics.tobytes() == want.metrics.tobytes()
