@@ -352,6 +352,48 @@ def test_config4_full_size_traces_vs_oracle(eng):
         assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
 
 
+@pytest.mark.parametrize("policy,pred", [("RR", "oracle"), ("WRR", "oracle"), ("SI", "oracle"), ("MB", "oracle"),
+                                         ("OS", "normal")])
+def test_config4_full_size_policies_vs_oracle(eng, policy, pred):
+    """Bench-scale parity for the baselines and the normal predictor: 8 full
+    config-4 traces (1e5 requests each, 140 req/s, 32 instances) per policy,
+    inputs drawn on the device (lengths, arrivals, normal predictions), vs the
+    literal C oracle bit for bit."""
+    from paper_2504_15303_b200 import streams
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    prof = wl.config4()
+    cluster = hs.ClusterSpec(hs.ModelSpec(**prof.model), hs.EngineOverheads(**prof.engine),
+                             tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+                             hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {a: 1 for a in wl.CONFIG4_TYPES})
+    nT, q = 8, wl.CONFIG4_Q
+    seeds = list(range(100, 100 + nT))
+    I, O = streams.gen_trace_lengths(seeds, q, "lognormal:200:0.6", "lognormal:150:0.6", 4096, 4096, engine=eng)
+    T = streams.arrival_times([42 + s for s in seeds], [q] * nT, wl.CONFIG4_RATE, engine=eng)
+    if pred == "normal":
+        P = streams.predict_lengths([7 + s for s in seeds], [q] * nT, 150.0, 60.0, 4096, engine=eng)
+        pc = hs.PredictorConfig(mode="normal", mean=150.0, stddev=60.0, seed=7)
+    else:
+        P = O
+        pc = hs.PredictorConfig()
+    off = np.arange(nT + 1, dtype=np.int64) * q
+    # WRR weights: proportional to the instance's capacity class (b200 > h100 = a800 > v100)
+    wrr = tuple(float(w) for w in np.repeat([4.0, 2.0, 2.0, 1.0], 8)) if policy == "WRR" else None
+    pol = hs.PolicyConfig(policy=policy, theta=2.0, predictor=pc, wrr_weights=wrr)
+    res = hs.replay_traces(cluster, config, params, pol, off, I, O, P, arrival=T, want_assign=True,
+                           want_depart=True, engine=eng)
+    handles = build_instances(cluster, config, params)
+    a, d, m, r = orc.replay(engine_instances(handles, pol), _policy_struct(pol, 32, hs.kv_bytes_per_token(cluster.model)),
+                            off, I, O, P, T, nthreads=16)
+    assert (res.result["error"] == 0).all() and (r["error"] == 0).all()
+    assert np.array_equal(res.result["n_steps"], r["n_steps"])
+    assert np.array_equal(res.assign, a)
+    assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64))
+    for f in ("completion_time", "peak_kv_usage", "residual_load"):
+        assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
+
+
 def test_config5_full_size_rescore_vs_oracle(eng):
     """BASELINE config 5 at full size for a slice: the top-1024 deployments of
     the config-3 space, the first 16 of them each replayed on the 1e5-request
