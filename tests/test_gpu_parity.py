@@ -219,6 +219,35 @@ def test_batched_static_replay_vs_oracle(eng, policy):
         assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
 
 
+def test_config4_full_size_static_vs_oracle(eng):
+    """run_static at bench scale: 4 full config-4 traces (1e5 requests each,
+    OS) vs the oracle -- every assignment, batch completion time and metric."""
+    from paper_2504_15303_b200 import streams
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    prof = wl.config4()
+    cluster = hs.ClusterSpec(hs.ModelSpec(**prof.model), hs.EngineOverheads(**prof.engine),
+                             tuple(hs.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+                             hs.WorkloadLimits(**prof.limits))
+    params = {k: hs.LatencyParams(*v) for k, v in prof.params.items()}
+    config = hs.deployment_for(cluster.machines, {a: 1 for a in wl.CONFIG4_TYPES})
+    nT, q = 4, wl.CONFIG4_Q
+    I, O = streams.gen_trace_lengths(list(range(200, 200 + nT)), q, "lognormal:200:0.6", "lognormal:150:0.6",
+                                     4096, 4096, engine=eng)
+    off = np.arange(nT + 1, dtype=np.int64) * q
+    pol = hs.PolicyConfig()
+    res = hs.replay_traces(cluster, config, params, pol, off, I, O, O, want_assign=True, want_depart=True,
+                           engine=eng, static=True)
+    handles = build_instances(cluster, config, params)
+    a, d, m, r = orc.replay(engine_instances(handles, pol),
+                            _policy_struct(pol, 32, hs.kv_bytes_per_token(cluster.model), 1), off, I, O, O, None,
+                            nthreads=8)
+    assert (res.result["error"] == 0).all() and (r["error"] == 0).all()
+    assert np.array_equal(res.assign, a)
+    assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64))
+    for f in ("completion_time", "peak_kv_usage", "residual_load"):
+        assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), f
+
+
 def test_config3_top1024_vs_oracle(eng):
     """BASELINE config 5's first stage: top-1024 of the 5^16 space."""
     _case, _req, t = _config3_tables(eng)
