@@ -401,11 +401,13 @@ def engine_arm(args, rank, world, local_rank):
     k1 = statistics.median(kms["k1"])
     achieved = BYTES_PER_DISPATCH * nreq / (k3 / 1e3) / 1e9
     traffic = None
+    inst_per_dispatch = None
     prof = ROOT / "profiles" / "k3_replay_ncu.json"
     if prof.exists():
         pj = json.loads(prof.read_text())
         if pj.get("dram_bytes_per_dispatch"):
             traffic = pj["dram_bytes_per_dispatch"] * nreq
+        inst_per_dispatch = pj.get("warp_inst_per_dispatch")
     fp64_peak = eng.probe_fp64()
     cand_local = hi - lo
     k2_fp64 = 2.0 * cand_local / (k2 / 1e3)
@@ -415,6 +417,19 @@ def engine_arm(args, rank, world, local_rank):
     steps_per_req = n_steps_ev / max(nreq, 1)
     k3_ops_per_dispatch = N * 67 + 15 * steps_per_req
     k3_fp64 = k3_ops_per_dispatch * nreq / (k3 / 1e3)
+    # K3 against the instruction-issue roofline (what bounds it): the live
+    # dispatch rate times the warp instructions per dispatch ncu measured at
+    # this workload, vs one warp instruction per scheduler per SM cycle
+    clocks = clk.summary()
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    issue_peak = 4.0 * n_sm * (clocks.get("sm_mhz") or 1965.0) * 1e6
+    roof_issue = None
+    if inst_per_dispatch:
+        ach = inst_per_dispatch * nreq / (k3 / 1e3)
+        roof_issue = {"bound": "issue", "achieved": ach, "peak": issue_peak, "unit": "warp-instructions/s",
+                      "frac": ach / issue_peak, "kernel": "k_replay", "inst_per_dispatch": inst_per_dispatch,
+                      "note": "instructions per dispatch from ncu at this workload (profiles/k3_replay_ncu.json, "
+                              "smsp__inst_executed.sum / dispatches); peak = 4 schedulers x SMs x SM clock"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -452,7 +467,8 @@ def engine_arm(args, rank, world, local_rank):
                                  "note": "reference-literal FP64 op count (SURVEY.md 8d: N*67 per dispatch + 15 per "
                                          "step event); the kernel executes fewer (per-class pricing, O(N) min-max)"},
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "roofline_k3_issue": roof_issue,
+            "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
