@@ -234,7 +234,9 @@ __constant__ SpaceDesc c_space;
 //   inner2 machine  M-1        compile-time radix DL (registers)
 // An item = one outer prefix = D3*D2*D1*DL candidates.  Per candidate the fast
 // path issues one DADD (prefix + last contribution, the reference's own
-// left-to-right order) and one DSETP.GT.OR into the `hit` predicate.
+// left-to-right order) and one compare OR-ed into a `hit` predicate: a
+// DSETP.GT.OR, or in non-negative spaces an ISETP on the total's high word
+// (ge_or_hi below).
 // h |= (v > b) as one DSETP.GT.OR per candidate (left to nvcc, a run of
 // `hit |= v > best` is rewritten into a max-reduction costing ~8 ALU ops
 // per candidate; ptxas folds the selp/setp pairs of consecutive calls).
