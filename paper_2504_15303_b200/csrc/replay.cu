@@ -56,8 +56,16 @@ __device__ unsigned long long g_timers[16];
 #endif
 
 constexpr int kWarps = 4;
+// Resident blocks per SM that __launch_bounds__ asks for.  One-warp traces
+// (N <= 32) are issue-bound and gain from occupancy: 4 blocks (128 registers)
+// beats 3 (168) by 17 % on config 4.  Multi-warp traces (W > 1) spill at 128
+// registers (60-150 B) and lose more to the spills than they gain from the
+// extra block: 3 blocks is 11 % faster on config 5 (K3).
 #ifndef HS_REPLAY_MIN_BLOCKS
 #define HS_REPLAY_MIN_BLOCKS 4
+#endif
+#ifndef HS_REPLAY_MIN_BLOCKS_MULTI
+#define HS_REPLAY_MIN_BLOCKS_MULTI 3
 #endif
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -210,7 +218,7 @@ __device__ __forceinline__ void group_bar(int g, int nthreads) {
 }
 
 template <int W, bool MULTI>
-__global__ void __launch_bounds__(kWarps * 32, HS_REPLAY_MIN_BLOCKS)
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : HS_REPLAY_MIN_BLOCKS_MULTI)
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
