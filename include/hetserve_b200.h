@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define HS_ABI_VERSION 3
+#define HS_ABI_VERSION 4
 #define HS_MAX_DEGREES 32   /* power-of-two divisors of an accelerator count  */
 #define HS_MAX_MACHINES 64
 #define HS_MAX_INSTANCES 128 /* one lane per instance, up to 4 warps per trace */
@@ -151,8 +151,17 @@ typedef struct {
   int64_t per_token;     /* capacity.py:67-69 kv_bytes_per_token */
   int32_t mode;          /* 0 continuous batching (simulator.py:272-363),
                             1 static batching (simulator.py:206-250; rate=inf) */
-  int32_t _pad;
+  int32_t flags;         /* HS_REPLAY_* bits */
 } hs_policy;
+
+/* hs_policy.flags: `depart` receives three doubles per request instead of
+ * one -- (departure time, heap key, per-instance sequence).  The reference's
+ * event heap (simulator.py:285-355) pops a retiring step once every earlier
+ * step of the instance's busy period has popped, so request_times order =
+ * sort by (heap key, instance, sequence); the heap key is the running max of
+ * the instance's step times since it last went idle (== the departure time
+ * whenever step costs are non-negative). */
+#define HS_REPLAY_ORDER_KEYS 1
 
 /* simulator.py:82-88 InstanceMetrics + scheduler.loads() residual. */
 typedef struct {
@@ -380,6 +389,17 @@ int hs_sched_complete(hs_scheduler* s, const char* request_id, int32_t id_len, h
 /* Scheduler.snapshot / loads / running_totals (any pointer may be NULL). */
 int hs_sched_snapshot(hs_scheduler* s, double* loads, int64_t* running_totals, double* kv_usage, int64_t* oversized,
                       int64_t* in_flight);
+/* Scheduler._states[j] (scheduling.py:157-164 InstanceState): read or
+ * overwrite one instance's load, running token sums (RunningTokens
+ * input_sum / predicted_output_sum) and oversized count, or replace its
+ * handle (params, budget, wrr_weight) -- what the reference's tests and a
+ * gateway reach into directly (tests/test_scheduling.py:142-143, 275;
+ * tests/test_gateway.py:140-149).  Any out pointer may be NULL. */
+int hs_sched_get_state(hs_scheduler* s, int32_t j, double* load, int64_t* input_sum, int64_t* pred_sum,
+                       int64_t* oversized);
+int hs_sched_set_state(hs_scheduler* s, int32_t j, double load, int64_t input_sum, int64_t pred_sum,
+                       int64_t oversized);
+int hs_sched_set_instance(hs_scheduler* s, int32_t j, const hs_instance* instance);
 
 /* Device buffers for hs_replay_device. */
 int hs_device_alloc(hs_ctx* ctx, int64_t bytes, void** out);

@@ -76,7 +76,10 @@ class hs_instance(C.Structure):
 
 class hs_policy(C.Structure):
     _fields_ = [("policy", C.c_int32), ("n_instances", C.c_int32), ("theta", C.c_double), ("per_token", C.c_int64),
-                ("mode", C.c_int32), ("_pad", C.c_int32)]
+                ("mode", C.c_int32), ("flags", C.c_int32)]
+
+
+REPLAY_ORDER_KEYS = 1  # hs_policy.flags: depart = (time, heap key, per-instance sequence) per request
 
 
 class hs_inst_metrics(C.Structure):
@@ -142,7 +145,7 @@ EXPORTS = (
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
     "hs_replay_seeded", "hs_pcg64_seed", "hs_pcg64_seed_u64", "hs_rng_generate",
     "hs_sched_create", "hs_sched_destroy", "hs_sched_evaluate", "hs_sched_choose", "hs_sched_complete",
-    "hs_sched_snapshot", "hs_plan_instance",
+    "hs_sched_snapshot", "hs_plan_instance", "hs_sched_get_state", "hs_sched_set_state", "hs_sched_set_instance",
 )
 
 _lib = None
@@ -192,6 +195,9 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_sched_choose": ([vp, C.c_char_p, i32, i64, i64, vp, vp, vp], C.c_int),
             "hs_sched_complete": ([vp, C.c_char_p, i32, vp], C.c_int),
             "hs_sched_snapshot": ([vp, vp, vp, vp, vp, vp], C.c_int),
+            "hs_sched_get_state": ([vp, i32, vp, vp, vp, vp], C.c_int),
+            "hs_sched_set_state": ([vp, i32, dbl, i64, i64, i64], C.c_int),
+            "hs_sched_set_instance": ([vp, i32, vp], C.c_int),
             "hs_plan_instance": ([vp, dbl, i64, vp, vp, vp, i64, vp, vp, vp, vp], C.c_int),
             "hs_rng_generate": ([vp, vp, i32, vp, vp, i32, vp, vp], C.c_int),
         }
@@ -417,7 +423,8 @@ class Engine:
         batch = hs_trace_batch(T, offsets.ctypes.data, I.ctypes.data, O.ctypes.data,
                                None if P is None else P.ctypes.data, None if arrival is None else arrival.ctypes.data)
         assign = _out_buf(assign_out, total, np.uint8) if want_assign else None
-        depart = _out_buf(depart_out, total, np.float64) if want_depart else None
+        dw = 3 if policy.flags & REPLAY_ORDER_KEYS else 1
+        depart = _out_buf(depart_out, total * dw, np.float64) if want_depart else None
         metrics = np.zeros(max(T * N, 1), METRICS_DTYPE)
         result = np.zeros(max(T, 1), RESULT_DTYPE)
         if seeds is None:
@@ -429,7 +436,8 @@ class Engine:
                                            C.byref(batch), C.byref(seeds), _ptr(assign), _ptr(depart),
                                            _ptr(metrics), _ptr(result))
             self.check(rc, "hs_replay_seeded")
-        return (None if assign is None else assign[:total], None if depart is None else depart[:total],
+        return (None if assign is None else assign[:total],
+                None if depart is None else (depart[:total] if dw == 1 else depart[: 3 * total].reshape(total, 3)),
                 metrics[: T * N].reshape(T, N), result[:T])
 
 

@@ -15,6 +15,7 @@ import pathlib
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
@@ -36,12 +37,22 @@ def build(verbose: bool = False, force: bool = False, timers: bool = False) -> p
     deps.append(PKG.parent / "include" / "hetserve_b200.h")
     if not force and lib.exists() and all(lib.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return lib
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off",
-           "-Xptxas", "-v" if verbose else "-O3", "-cudart", "static", *(["-DHS_TIMERS"] if timers else []), "-o", str(lib) + ".tmp",
-           *[str(CSRC / s) for s in SOURCES]]
+    flags = [*ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+             "-Xptxas", "-v" if verbose else "-O3", *(["-DHS_TIMERS"] if timers else [])]
+    objdir = PKG / "build" / ("timers" if timers else "release")
+    objdir.mkdir(parents=True, exist_ok=True)
+    # one nvcc per translation unit, in parallel, then one link
+    cmds = [[nvcc(), *flags, "-c", str(CSRC / s), "-o", str(objdir / (s + ".o"))] for s in SOURCES]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True, cwd=CSRC)
+        for c in cmds:
+            print(" ".join(c))
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        for r in ex.map(lambda c: subprocess.run(c, cwd=CSRC, capture_output=not verbose, text=True), cmds):
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed:\n{r.stderr}")
+    link = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(lib) + ".tmp",
+            *[str(objdir / (s + ".o")) for s in SOURCES]]
+    subprocess.run(link, check=True, cwd=CSRC)
     os.replace(str(lib) + ".tmp", lib)
     return lib
 

@@ -228,6 +228,11 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
   rc.per_token = pol->per_token;
   rc.has_arrival = has_arrival;
   rc.mode = pol->mode;
+  if (pol->flags & ~HS_REPLAY_ORDER_KEYS) return fail(HS_ERR_ARG, "unknown hs_policy.flags bits");
+  bool negative = false;  // a negative coefficient can make a step cost negative
+  for (int j = 0; j < N; ++j)
+    for (int k = 0; k < 8; ++k) negative |= inst[j].p[k] < 0.0;
+  rc.flags = (pol->flags & HS_REPLAY_ORDER_KEYS) ? (1 | (negative ? 2 : 0)) : 0;
   int nt = 0;
   std::vector<double> wts(N);
   for (int j = 0; j < N; ++j) {
@@ -236,6 +241,11 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
     if (ty >= hs::kMaxTypes) return fail(HS_ERR_UNSUPPORTED, "more than 32 distinct instance classes");
     if (!(inst[j].budget > 0)) return fail(HS_ERR_ARG, "instance budget must be positive");
     rc.inst_type[j] = (int8_t)ty;
+    bool seen = false;  // every instance of a class must carry the class's exact params and budget
+    for (int i = 0; i < j && !seen; ++i) seen = inst[i].type == ty;
+    if (seen && (std::memcmp(rc.type_p[ty], inst[j].p, sizeof(double) * 8) != 0 ||
+                 std::memcmp(&rc.type_budget[ty], &inst[j].budget, sizeof(double)) != 0))
+      return fail(HS_ERR_ARG, "instances sharing a type id differ in params or budget");
     if (ty >= nt) nt = ty + 1;
     std::memcpy(rc.type_p[ty], inst[j].p, sizeof(double) * 8);
     rc.type_budget[ty] = inst[j].budget;
@@ -840,7 +850,10 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
   } else if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) {
     return rc;
   }
-  if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
+  const size_t dep_w = (pol->flags & HS_REPLAY_ORDER_KEYS) ? 3 : 1;  // doubles per request in `depart`
+  if (depart && (rc = ensure_t(c, S_DEPART, tq * dep_w, &dDep))) return rc;
+  // requests that never retire (a failed trace) read back as NaN
+  if (dDep) HS_CUDA(cudaMemsetAsync(dDep, 0xff, sizeof(double) * dep_w * tq, c->stream));
   HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
   // Streamed replay (equal-length traces, the batched-replay shape): every
   // trace is launched once the first of kPhases phases of every trace is
@@ -933,7 +946,7 @@ int replay_host(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, const 
     HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
     if (assign && !zA && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
     if (depart && total > 0)
-      HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
+      HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * dep_w * total, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaStreamSynchronize(c->stream));
     bool redo = false;
     for (int64_t t = 0; t < T; ++t) redo |= result[t].error == HS_TRACE_CAPACITY;
@@ -1034,7 +1047,7 @@ chunked:
   }
   if (assign && !zA && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
   if (depart && total > 0)
-    HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * dep_w * total, cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   return HS_OK;
 }
@@ -1199,7 +1212,10 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
     return rc;
   if (b->arrival && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
   if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
-  if (depart && (rc = ensure_t(c, S_DEPART, tq, &dDep))) return rc;
+  const size_t dep_w = (pol->flags & HS_REPLAY_ORDER_KEYS) ? 3 : 1;  // doubles per request in `depart`
+  if (depart && (rc = ensure_t(c, S_DEPART, tq * dep_w, &dDep))) return rc;
+  // requests that never retire (a failed trace) read back as NaN
+  if (dDep) HS_CUDA(cudaMemsetAsync(dDep, 0xff, sizeof(double) * dep_w * tq, c->stream));
   HS_CUDA(cudaMemcpyAsync(dOff, off, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, c->stream));
   if (total > 0) {
     HS_CUDA(cudaMemcpyAsync(dI, b->input_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
@@ -1238,7 +1254,7 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
   }
   if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
   if (depart && total > 0)
-    HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * total, cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * dep_w * total, cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   return HS_OK;
 }

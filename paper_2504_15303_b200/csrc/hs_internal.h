@@ -56,7 +56,7 @@ struct ReplayConst {
   int32_t n_types;
   int32_t has_arrival;
   int32_t mode;  // 0 continuous (simulator.py:272), 1 static (simulator.py:206)
-  int32_t _pad0;
+  int32_t flags;  // replay.cu kOrderKeys | kTrackMax
   double theta;
   int64_t per_token;
   double wrr_total;

@@ -192,10 +192,16 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t k) {
 // Rarely touched per-lane state lives in shared memory.
 struct Cold {
   double completion, wcur, err_t;
+  double segmax;  // HS_REPLAY_ORDER_KEYS: running max of step times since the lane last went idle
   int64_t tok_count;
   int32_t req_count, cnt_max, err, err_req;
-  int32_t ty, _pad;  // instance class (read from here: a per-lane constant-bank index serialises)
+  int32_t ty;    // instance class (read from here: a per-lane constant-bank index serialises)
+  int32_t nret;  // HS_REPLAY_ORDER_KEYS: retirements so far (per-lane processing order)
 };
+
+// ReplayConst.flags
+constexpr int32_t kOrderKeys = 1;  // depart = (time, heap key, per-lane sequence) triples
+constexpr int32_t kTrackMax = 2;   // step costs may be negative: every step is an event step
 
 // One instance class of the deployment, staged in shared memory once per
 // trace group: lanes read their class by index from shared memory instead of
@@ -224,8 +230,8 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
              hs_trace_result* __restrict__ result, QRec* __restrict__ qrec_all, uint64_t* __restrict__ heap_all,
              const ReplayConst* __restrict__ deps, const int32_t* __restrict__ trace_dep,
-             const int64_t* __restrict__ trace_heap, int n_max, const uint32_t* progress, int32_t phase_len,
-             const __grid_constant__ ReplayConst c_one) {
+             const int64_t* __restrict__ trace_heap, int n_max, int max_types, const uint32_t* progress,
+             int32_t phase_len, const __grid_constant__ ReplayConst c_one) {
   constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);  // trace groups per block
   __shared__ uint64_t s_tab[256];
   __shared__ Cold s_cold[kWarps * 32];
@@ -250,8 +256,11 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
   const int policy = c_rep.policy;
   const int64_t pt = c_rep.per_token;
   const double theta = c_rep.theta;
-  double* cost = s_cost + (size_t)wib * 32 * NT;
-  TypeRec* types = reinterpret_cast<TypeRec*>(s_cost + (size_t)(W * G) * 32 * NT) + (size_t)g * NT;
+  // shared-memory strides: the launch-wide class count (traces of one block
+  // may run deployments with different class counts)
+  const int NTS = MULTI ? max_types : NT;
+  double* cost = s_cost + (size_t)wib * 32 * NTS;
+  TypeRec* types = reinterpret_cast<TypeRec*>(s_cost + (size_t)(W * G) * 32 * NTS) + (size_t)g * NTS;
   for (int k = wsub * 32 + lane; k < NT * 10; k += W * 32) {
     const int t = k / 10, f = k - t * 10;
     double* dst = reinterpret_cast<double*>(types + t) + f;
@@ -283,7 +292,8 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
   const int32_t* P = gP + o;
   const double* T = gT ? gT + o : nullptr;
   QRec* R = qrec_all + o;
-  double* DEP = depart ? depart + o : nullptr;
+  // with kOrderKeys every request owns three doubles of `depart`
+  double* DEP = depart ? depart + ((c_rep.flags & kOrderKeys) ? 3 * o : o) : nullptr;
 
   const int jj = wsub * 32 + lane;  // instance index of this lane
   const bool valid = jj < N;
@@ -313,6 +323,8 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
   double topW = 0.0;
   bool sched = false, dirty = true, ex_over = false, max_dirty = false, blocked = false, lerr = false;
   cold.completion = 0.0;
+  cold.segmax = -INFINITY;
+  cold.nret = 0;
   cold.wcur = 0.0;
   cold.err_t = 0.0;
   cold.tok_count = 0;
@@ -348,6 +360,10 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
   auto event_step = [&]() {
     const double t = t_next;
     sched = false;
+    // the reference's heap pops a step once every earlier step of its busy
+    // period has popped: its order key is the running max of their times
+    // (== t whenever step costs are non-negative)
+    if (c_rep.flags & kTrackMax) cold.segmax = t > cold.segmax ? t : cold.segmax;
 #ifdef HS_TIMERS
     tacc[14] += nact > kHS ? 1 : 0;
     tacc[15] += nact;
@@ -373,7 +389,15 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
       }
       reserved -= Ir + Or;
       cold.completion = t;
-      if (DEP) DEP[r] = t;
+      if (DEP) {
+        if (c_rep.flags & kOrderKeys) {
+          DEP[3 * (int64_t)r] = t;
+          DEP[3 * (int64_t)r + 1] = (c_rep.flags & kTrackMax) ? cold.segmax : t;
+          DEP[3 * (int64_t)r + 2] = (double)cold.nret++;
+        } else {
+          DEP[r] = t;
+        }
+      }
       load = __dsub_rn(load, wr);  // Scheduler.complete: the recorded values
       run_i -= Ir;
       run_p -= Pr;
@@ -508,7 +532,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
       // phase 1: lanes whose next step is an event (retirement due, or an
       // admission may succeed)
 
-      if (want && !(blocked && k < kr)) event_step();
+      if (want && ((c_rep.flags & kTrackMax) || !(blocked && k < kr))) event_step();
 #ifdef HS_TIMERS
       __syncwarp();
       HS_T0(tpu);
@@ -518,7 +542,8 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
       // their prices depend only on the cached length, so both are computed
       // side by side and only the clock additions stay serial (the
       // reference's rounding order).
-      const bool pure = valid && sched && !lerr && blocked && k < kr && (drain || t_next < t_limit);
+      const bool pure = valid && sched && !lerr && blocked && k < kr && (drain || t_next < t_limit) &&
+                        !(c_rep.flags & kTrackMax);
       if (pure) {
         const uint32_t k0 = k;
         // decode price of a step with cached length x (latency.py:95-97)
@@ -593,7 +618,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
     t_err = all[best].c;
     t_err_req = all[best].d;
     t_err_inst = (int32_t)all[best].b;
-    t_err_val = 0.0;
+    t_err_val = from_okey(all[best].a);  // the failing step's time
     return true;
   };
 
@@ -606,7 +631,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
       // streamed inputs (host path): phase p of every trace is resident once
       // *progress > p (the copy stream publishes it after the phase's copies)
       const uint32_t need = (uint32_t)((base + n_in - 1) / phase_len);
-      bool stalled = false;
+      int stalled = 0;
       if (lane == 0) {
         const long long t0 = clock64();
         uint32_t have;
@@ -614,13 +639,20 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
         while (have <= need) {
           __nanosleep(256);
           if (clock64() - t0 > 20000000000ll) {  // ~10 s: report instead of hanging the device
-            stalled = true;
+            stalled = 1;
             break;
           }
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(have) : "l"(progress) : "memory");
         }
       }
-      if (__shfl_sync(FULL, stalled, 0)) {
+      stalled = __shfl_sync(FULL, stalled, 0);
+      if (W > 1) {  // every warp of the trace group takes the same decision
+        Xch all[W];
+        xchg(Xch{0, 0, stalled, 0}, all);
+#pragma unroll
+        for (int w = 0; w < W; ++w) stalled |= all[w].c;
+      }
+      if (stalled) {
         t_err = HS_TRACE_STALLED;
         t_err_req = base;
         t_err_inst = -1;
@@ -839,6 +871,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
           sched = true;
           t_next = ta;
           blocked = false;
+          cold.segmax = -INFINITY;  // a new busy period
         }
       }
       if (lane == al) my_assign = (uint8_t)chosen;
@@ -883,7 +916,15 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
         for (int32_t m = r; m != stop;) {
           const QRec rec = R[m];
           load = __dsub_rn(load, rec.W);
-          if (DEP) DEP[m] = clock;
+          if (DEP) {
+            if (c_rep.flags & kOrderKeys) {
+              DEP[3 * (int64_t)m] = clock;
+              DEP[3 * (int64_t)m + 1] = clock;
+              DEP[3 * (int64_t)m + 2] = (double)cold.nret++;
+            } else {
+              DEP[m] = clock;
+            }
+          }
           m = (m == qtail) ? -1 : rec.next;
         }
         r = stop;
@@ -963,7 +1004,7 @@ cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
   const unsigned blocks = (unsigned)((n_traces + G - 1) / G);
   k_replay<W, MULTI><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
                                                 d_result, static_cast<QRec*>(d_qrec), d_heap, d_deps, d_trace_dep,
-                                                d_trace_heap, n_max, d_progress, phase_len, rc);
+                                                d_trace_heap, n_max, max_types, d_progress, phase_len, rc);
   return cudaGetLastError();
 }
 

@@ -325,3 +325,48 @@ int hs_sched_snapshot(hs_scheduler* s, double* loads, int64_t* running, double* 
 }
 
 }  // extern "C"
+
+// Scheduler._states view (scheduling.py:157-164 InstanceState): tests and
+// gateways that read or poke one instance's bookkeeping directly
+// (load, running tokens, oversized count, handle).
+extern "C" {
+
+int hs_sched_get_state(hs_scheduler* s, int32_t j, double* load, int64_t* input_sum, int64_t* pred_sum,
+                       int64_t* oversized) {
+  if (!s) return hs::set_error(HS_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> g(s->mu);
+  if (j < 0 || (size_t)j >= s->inst.size()) return hs::set_error(HS_ERR_ARG, "instance index out of range");
+  const Inst& t = s->inst[j];
+  if (load) *load = t.load;
+  if (input_sum) *input_sum = t.input_sum;
+  if (pred_sum) *pred_sum = t.pred_sum;
+  if (oversized) *oversized = t.oversized;
+  return HS_OK;
+}
+
+int hs_sched_set_state(hs_scheduler* s, int32_t j, double load, int64_t input_sum, int64_t pred_sum,
+                       int64_t oversized) {
+  if (!s) return hs::set_error(HS_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> g(s->mu);
+  if (j < 0 || (size_t)j >= s->inst.size()) return hs::set_error(HS_ERR_ARG, "instance index out of range");
+  Inst& t = s->inst[j];
+  t.load = load;
+  t.input_sum = input_sum;
+  t.pred_sum = pred_sum;
+  t.oversized = oversized;
+  return HS_OK;
+}
+
+int hs_sched_set_instance(hs_scheduler* s, int32_t j, const hs_instance* instance) {
+  if (!s || !instance) return hs::set_error(HS_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> g(s->mu);
+  if (j < 0 || (size_t)j >= s->inst.size()) return hs::set_error(HS_ERR_ARG, "instance index out of range");
+  if (!(instance->budget > 0)) return hs::set_error(HS_ERR_ARG, "instance budget must be positive");
+  Inst& t = s->inst[j];
+  std::memcpy(t.p, instance->p, sizeof(double) * 8);
+  t.budget = instance->budget;
+  t.wrr_weight = instance->wrr_weight;
+  return HS_OK;
+}
+
+}  // extern "C"

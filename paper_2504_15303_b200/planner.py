@@ -39,7 +39,7 @@ from .domain import (
     prefill_time,
 )
 
-MAX_MATERIALISED = 1 << 22  # candidates search_optimal_config will turn into objects
+MAX_MATERIALISED = 1 << 26  # candidates search_optimal_config ranks on the device (hs_search_rank's limit)
 
 
 @dataclass(frozen=True)
@@ -334,25 +334,37 @@ def search_optimal_config(cluster, requests, params_by_machine_tp, engine=None) 
         )
     eng = engine or nat.engine_for()
     ranked_arr, first_bad = eng.search_rank(tables.entries, tables.n_degrees)
+    # frozen per-(machine, digit) pieces are shared between candidates
+    machines = tables.cluster.machines
+    place = [[MachinePlacement(machine=m.name, tp_degree=t, instance_count=m.accelerator_count // t)
+              for t in tables.degrees[i]] for i, m in enumerate(machines)]
+    est = [[_machine_estimate(tables.names[i], t, tables.entries[i, d]) for d, t in enumerate(tables.degrees[i])]
+           for i in range(len(machines))]
+    nd = [int(x) for x in tables.n_degrees]
+
+    def digits_of(idx: int) -> list:
+        out = [0] * len(nd)
+        for i in range(len(nd) - 1, -1, -1):
+            idx, out[i] = divmod(idx, nd[i])
+        return out
+
     ranked = []
     for total, idx in zip(ranked_arr["total"].tolist(), ranked_arr["index"].tolist()):
-        digits = tables.digits(idx)
-        per_machine = tuple(
-            _machine_estimate(tables.names[i], tables.degrees[i][d], tables.entries[i, d])
-            for i, d in enumerate(digits)
-        )
-        ranked.append(ThroughputEstimate(config=_config_for(tables, digits), per_machine=per_machine,
-                                         system_tokens_per_sec=total))
+        digits = digits_of(idx)
+        ranked.append(ThroughputEstimate(
+            config=DeploymentConfig(per_machine=tuple(place[i][d] for i, d in enumerate(digits))),
+            per_machine=tuple(est[i][d] for i, d in enumerate(digits)), system_tokens_per_sec=total))
     infeasible = []
     cache = {}
     for c in np.nonzero(first_bad >= 0)[0].tolist():
-        digits = tables.digits(c)
+        digits = digits_of(c)
         i = int(first_bad[c])
         key = (i, digits[i])
         if key not in cache:
             cache[key] = str(_entry_exception(cluster, requests, tables.names[i], tables.degrees[i][digits[i]],
                                               tables.entries[i, digits[i]]))
-        infeasible.append((_config_for(tables, digits), cache[key]))
+        infeasible.append((DeploymentConfig(per_machine=tuple(place[k][d] for k, d in enumerate(digits))),
+                           cache[key]))
     return SearchOutcome(ranked=tuple(ranked), infeasible=tuple(infeasible))
 
 

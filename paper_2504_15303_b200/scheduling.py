@@ -134,6 +134,81 @@ def workload(cost: float, usage: float, theta: float) -> float:
     return cost * math.exp(theta * usage)
 
 
+class _RunningView:
+    """RunningTokens (capacity.py:33-55) of one native scheduler instance."""
+
+    def __init__(self, sched, j: int):
+        self._s, self._j = sched, j
+
+    @property
+    def input_sum(self) -> int:
+        return self._s._get_state(self._j)[1]
+
+    @input_sum.setter
+    def input_sum(self, v: int) -> None:
+        self._s._set_state(self._j, input_sum=int(v))
+
+    @property
+    def predicted_output_sum(self) -> int:
+        return self._s._get_state(self._j)[2]
+
+    @predicted_output_sum.setter
+    def predicted_output_sum(self, v: int) -> None:
+        self._s._set_state(self._j, pred_sum=int(v))
+
+    def add(self, input_len: int, predicted_output_len: int) -> None:
+        _l, i, p, _o = self._s._get_state(self._j)
+        self._s._set_state(self._j, input_sum=i + input_len, pred_sum=p + predicted_output_len)
+
+    def remove(self, input_len: int, predicted_output_len: int) -> None:
+        _l, i, p, _o = self._s._get_state(self._j)
+        i, p = i - input_len, p - predicted_output_len
+        self._s._set_state(self._j, input_sum=i, pred_sum=p)
+        if i < 0 or p < 0:
+            raise SpecError("running token sums went negative; completion applied twice?")
+
+    def total(self) -> int:
+        _l, i, p, _o = self._s._get_state(self._j)
+        return i + p
+
+
+class _StateView:
+    """scheduling.py:157-164 InstanceState of one native scheduler instance:
+    reads and writes go to the native state (hs_sched_get/set_state,
+    hs_sched_set_instance), so code that pokes Scheduler._states works."""
+
+    def __init__(self, sched, j: int):
+        self._s, self._j = sched, j
+
+    @property
+    def load(self) -> float:
+        return self._s._get_state(self._j)[0]
+
+    @load.setter
+    def load(self, v: float) -> None:
+        self._s._set_state(self._j, load=float(v))
+
+    @property
+    def running(self) -> _RunningView:
+        return _RunningView(self._s, self._j)
+
+    @property
+    def oversized_count(self) -> int:
+        return self._s._get_state(self._j)[3]
+
+    @oversized_count.setter
+    def oversized_count(self, v: int) -> None:
+        self._s._set_state(self._j, oversized=int(v))
+
+    @property
+    def handle(self):
+        return self._s._handles[self._j]
+
+    @handle.setter
+    def handle(self, h) -> None:
+        self._s._set_handle(self._j, h)
+
+
 class Scheduler:
     """scheduling.py:175-346 Scheduler over the native hs_sched_* engine:
     choose() / complete() / evaluate() / snapshot() with the reference's
@@ -182,6 +257,37 @@ class Scheduler:
     @property
     def instances(self) -> list:
         return list(self._handles)
+
+    @property
+    def _states(self) -> list:
+        """InstanceState views (scheduling.py:202), backed by the native state."""
+        return [_StateView(self, j) for j in range(self._n)]
+
+    def _get_state(self, j: int):
+        load, i, p, o = C.c_double(), C.c_int64(), C.c_int64(), C.c_int64()
+        rc = self._lib.hs_sched_get_state(self._h, j, C.byref(load), C.byref(i), C.byref(p), C.byref(o))
+        if rc != self._nat.HS_OK:
+            raise self._nat.EngineError(rc, "hs_sched_get_state: " + (self._lib.hs_last_error() or b"").decode())
+        return load.value, i.value, p.value, o.value
+
+    def _set_state(self, j: int, load=None, input_sum=None, pred_sum=None, oversized=None) -> None:
+        cur = self._get_state(j)
+        new = [cur[k] if v is None else v for k, v in enumerate((load, input_sum, pred_sum, oversized))]
+        rc = self._lib.hs_sched_set_state(self._h, j, float(new[0]), int(new[1]), int(new[2]), int(new[3]))
+        if rc != self._nat.HS_OK:
+            raise self._nat.EngineError(rc, "hs_sched_set_state: " + (self._lib.hs_last_error() or b"").decode())
+
+    def _set_handle(self, j: int, h) -> None:
+        nat = self._nat
+        rec = nat.hs_instance()
+        for k, name in enumerate(("p1", "p2", "p3", "p4", "p5", "p6", "p7", "p8")):
+            rec.p[k] = float(getattr(h.params, name))
+        rec.budget = float(h.budget.total_bytes)
+        rec.wrr_weight = float(self._policy.wrr_weights[j]) if self._policy.policy == "WRR" else 0.0
+        rc = self._lib.hs_sched_set_instance(self._h, j, C.byref(rec))
+        if rc != nat.HS_OK:
+            raise nat.EngineError(rc, "hs_sched_set_instance: " + (self._lib.hs_last_error() or b"").decode())
+        self._handles[j] = h
 
     @property
     def policy(self) -> PolicyConfig:

@@ -199,8 +199,43 @@ def _raise_trace_error(res, handles, trace, per_token, static=False) -> None:
     raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, f"replay hit an engine limit (code {err})")
 
 
-def _policy_struct(policy: PolicyConfig, n: int, per_token: int, mode: int = 0) -> nat.hs_policy:
-    return nat.hs_policy(nat.POLICY_CODE[policy.policy], n, float(policy.theta), per_token, mode, 0)
+def _policy_struct(policy: PolicyConfig, n: int, per_token: int, mode: int = 0, flags: int = 0) -> nat.hs_policy:
+    return nat.hs_policy(nat.POLICY_CODE[policy.policy], n, float(policy.theta), per_token, mode, flags)
+
+
+def _first_duplicate_in_flight(ids, arr, dep, static: bool):
+    """Index of the first arrival whose request id is still in flight
+    (Scheduler.choose raises before anything else, scheduling.py:239-240), or
+    None.  An earlier request with the same id is in flight unless its
+    retirement step popped before this arrival: departure < arrival (arrivals
+    pop first at equal times, simulator.py:285-290).  In static mode every
+    dispatch precedes every completion (simulator.py:216-220)."""
+    seen: dict = {}
+    first = None
+    for k, rid in enumerate(ids):
+        prev = seen.get(rid)
+        seen[rid] = k
+        if prev is None:
+            continue
+        if static or not (dep[prev] < arr[k]):  # NaN: never retired
+            if first is None or k < first:
+                first = k
+    return first
+
+
+def _duplicate_wins(a: int, res, arr, static: bool) -> bool:
+    """Does the in-flight error at arrival `a` happen before the kernel's
+    own failure (if any) in the reference's event order?"""
+    err = int(res["error"])
+    if err == nat.TRACE_OK:
+        return True
+    if err in (nat.TRACE_NONPOSITIVE_COST, nat.TRACE_EXP_OVERFLOW, nat.TRACE_NO_INSTANCE):
+        return a <= int(res["err_request"])  # both at arrivals: the in-flight check runs first
+    if static:
+        return True  # planning failures come after every dispatch
+    if err in (nat.TRACE_INFEASIBLE_REQUEST, nat.TRACE_NEGATIVE_RUNNING):
+        return arr[a] <= float(res["err_value"])  # a step at the arrival's own time pops after it
+    return True
 
 
 def _run(scenario, static: bool, engine=None) -> SimMetrics:
@@ -210,11 +245,9 @@ def _run(scenario, static: bool, engine=None) -> SimMetrics:
     N = len(handles)
     if N > nat.HS_MAX_INSTANCES:
         raise nat.EngineError(nat.HS_ERR_UNSUPPORTED,
-                              f"{N} instances: the round-1 replay kernel handles up to {nat.HS_MAX_INSTANCES}")
+                              f"{N} instances: the replay kernel handles up to {nat.HS_MAX_INSTANCES}")
     trace = scenario.trace
     ids = [r.id for r in trace]
-    if len(set(ids)) != len(ids):
-        raise nat.EngineError(nat.HS_ERR_UNSUPPORTED, "duplicate request ids in one trace are not supported")
     per_token = kv_bytes_per_token(scenario.cluster.model)
     I = np.fromiter((r.input_len for r in trace), np.int64, len(trace))
     O = np.fromiter((r.output_len for r in trace), np.int64, len(trace))
@@ -235,27 +268,38 @@ def _run(scenario, static: bool, engine=None) -> SimMetrics:
         raise SpecError(f"arrival rate must be positive, got {scenario.arrival_rate}")
     T = streams.arrival_times([scenario.seed], [len(trace)], scenario.arrival_rate, engine=eng)
     offsets = np.array([0, len(trace)], np.int64)
-    assign, depart, metrics, result = eng.replay(
-        engine_instances(handles, policy), _policy_struct(policy, N, per_token, 1 if static else 0), offsets,
+    # (time, heap key, per-instance sequence) per request; NaN = never retired
+    dep_out = np.full(3 * len(trace), np.nan)
+    assign, dep3, metrics, result = eng.replay(
+        engine_instances(handles, policy),
+        _policy_struct(policy, N, per_token, 1 if static else 0, nat.REPLAY_ORDER_KEYS), offsets,
         I.astype(np.int32), O.astype(np.int32), P.astype(np.int32),
-        None if math.isinf(scenario.arrival_rate) else T)
+        None if math.isinf(scenario.arrival_rate) else T, depart_out=dep_out)
+    depart = dep3[:, 0]
+    arr = T.tolist()
+    dup = _first_duplicate_in_flight(ids, arr, depart.tolist(), static)
+    if dup is not None and _duplicate_wins(dup, result[0], arr, static):
+        raise SchedulingError(f"request {ids[dup]!r} is already in flight")
     _raise_trace_error(result[0], handles, trace, per_token, static=static)
     m = metrics[0]
     completion = m["completion_time"].tolist()
     req_count = m["request_count"].tolist()
     tok_count = m["token_count"].tolist()
     peak = m["peak_kv_usage"].tolist()
-    idx = np.arange(len(trace))
     if static:
         # simulator.py:229-245: times filled instance by instance, batch by batch
-        order = np.lexsort((idx, assign.astype(np.int64)))
+        order = np.lexsort((dep3[:, 2], assign.astype(np.int64)))
     else:
-        # retirement order: (departure time, instance index, admission order) --
-        # the reference's heap order whenever step costs are non-negative
-        order = np.lexsort((idx, assign.astype(np.int64), depart))
+        # the reference's heap pop order of the retiring steps (simulator.py:285-355):
+        # (heap key, instance index, per-instance retirement sequence)
+        order = np.lexsort((dep3[:, 2], assign.astype(np.int64), dep3[:, 1]))
     dep = depart.tolist()
-    arr = T.tolist()
-    request_times = tuple((ids[k], arr[k], dep[k]) for k in order.tolist())
+    # `times` is a dict keyed by request id (simulator.py:275, 337): a repeated
+    # id keeps its first position and its last value
+    times: dict = {}
+    for k in order.tolist():
+        times[ids[k]] = (0.0 if static else arr[k], dep[k])
+    request_times = tuple((rid, a, d) for rid, (a, d) in times.items())
     makespan = max(completion) if completion else 0.0
     total_tokens = sum(tok_count)
     return SimMetrics(

@@ -153,9 +153,23 @@ def arrival_times(seeds, counts, rate: float, engine=None) -> np.ndarray:
         d.close()
 
 
+def _check_finite_normal(seed, mean: float, stddev: float) -> None:
+    """A non-finite mean / stddev makes the predictor's first draw non-finite,
+    and the reference's round() raises on it (scheduling.py:94: ValueError for
+    NaN, OverflowError for inf): raise exactly that, from the same draw."""
+    if math.isfinite(float(mean)) and math.isfinite(float(stddev)):
+        return
+    round(float(np.random.default_rng(seed).normal(float(mean), float(stddev))))
+
+
 def predict_lengths_device(seeds, counts, mean: float, stddev: float, max_output_len: int,
                            engine=None) -> DeviceStreams:
     """The normal-mode OutputLengthPredictor for each (seed, count)."""
+    seeds = list(seeds)
+    for sd, n in zip(seeds, counts):
+        if int(n) > 0:
+            _check_finite_normal(sd, mean, stddev)
+            break
     return _generate(list(seeds), counts,
                      [nat.hs_dist(nat.DIST_NORMAL_LEN, _upper(max_output_len), 0, 0, float(mean), float(stddev))],
                      engine)
@@ -183,6 +197,8 @@ def replay_seeds(arrival_seeds=None, rate: float = math.inf, predictor=None, pre
         s.arrival_state = st.ctypes.data
         s.arrival_scale = 1.0 / rate
     if predictor is not None and predictor.mode == "normal":
+        if len(predictor_seeds):
+            _check_finite_normal(list(predictor_seeds)[0], predictor.mean, predictor.stddev)
         st = nat.pcg64_states(list(predictor_seeds))
         keep.append(st)
         s.predictor_state = st.ctypes.data

@@ -474,3 +474,53 @@ def test_replay_candidates_equals_object_path(eng):
         assert np.array_equal(a.depart.view(np.uint64), b.depart.view(np.uint64))
         assert a.metrics.tobytes() == b.metrics.tobytes()
         assert a.result.tobytes() == b.result.tobytes()
+
+
+def _twin_cluster():
+    """Two machines of one accelerator type: equal degrees make one instance
+    class, different degrees two."""
+    prof = wl.config4()
+    base = prof.machines[1]  # h100
+    machines = (hs.MachineSpec("h100-0", 8, base[2], "h100"), hs.MachineSpec("h100-1", 8, base[2], "h100"),
+                hs.MachineSpec("b200-0", 4, prof.machines[0][2], "b200"))
+    cluster = hs.ClusterSpec(model=hs.ModelSpec(**prof.model), engine=hs.EngineOverheads(**prof.engine),
+                             machines=machines, limits=hs.WorkloadLimits(**prof.limits))
+    params = {}
+    for m in machines:
+        for t in wl.enumerate_degrees(m.accelerator_count):
+            params[(m.name, t)] = hs.LatencyParams(*wl.scaled_params(wl.RANK_BASE, t ** -wl.TP_ALPHA *
+                                                                     wl.TYPE_SCALE[m.accelerator_type]))
+    return cluster, params
+
+
+def test_replay_deployments_mixed_class_counts_small_deployments(eng):
+    """deployments of <= 32 instances share a block (4 traces
+    per block) while having different instance-class counts (1, 2, 3); the
+    shared-memory price / class regions must not overlap.  Finite rate, OS
+    and MB, each trace vs the oracle."""
+    cluster, params = _twin_cluster()
+    degs = [(1, 1, 1), (1, 2, 4), (2, 2, 2), (4, 8, 1), (1, 1, 4), (8, 8, 2), (2, 4, 1), (1, 8, 2)]
+    configs = [hs.deployment_for(cluster.machines, dict(zip(("h100-0", "h100-1", "b200-0"), d))) for d in degs]
+    q = 4000
+    T = 16
+    trace_dep = np.arange(T) % len(configs)
+    I = np.concatenate([wl.trace_lengths(q, seed=100 + t)[0] for t in range(T)])
+    O = np.concatenate([wl.trace_lengths(q, seed=100 + t)[1] for t in range(T)])
+    A = np.concatenate([wl.arrivals(q, 60.0, 7 + t) for t in range(T)])
+    off = np.arange(T + 1, dtype=np.int64) * q
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    per_token = hs.kv_bytes_per_token(cluster.model)
+    for pol in (hs.PolicyConfig(), hs.PolicyConfig(policy="MB")):
+        res = hs.replay_deployments(cluster, configs, params, pol, trace_dep, off, I, O, O, arrival=A,
+                                    want_depart=True, engine=eng)
+        for t in range(T):
+            handles = build_instances(cluster, configs[trace_dep[t]], params)
+            sl = slice(off[t], off[t + 1])
+            a, dep, m, r = orc.replay(engine_instances(handles, pol), _policy_struct(pol, len(handles), per_token),
+                                      np.array([0, q], np.int64), I[sl], O[sl], O[sl], A[sl])
+            assert int(res.result[t]["error"]) == 0 == int(r[0]["error"])
+            assert np.array_equal(res.assign[sl], a), (pol.policy, t)
+            assert np.array_equal(res.depart[sl].view(np.uint64), dep.view(np.uint64)), (pol.policy, t)
+            n = len(handles)
+            for f in ("completion_time", "peak_kv_usage", "residual_load"):
+                assert np.array_equal(res.metrics[t][:n][f].view(np.uint64), m[0][f].view(np.uint64)), f

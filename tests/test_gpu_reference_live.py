@@ -1,0 +1,100 @@
+"""Fuzzed drop-in parity against the live reference (baseline/_ref, the
+unmodified package, run on the host) for the edge cases the golden fixtures
+do not cover: repeated request ids (in flight -> SchedulingError at the
+repeat, scheduling.py:239-240; completed -> the request_times dict keeps the
+first position and the last value, simulator.py:275, 337), negative and zero
+step costs (the event heap's pop order, simulator.py:285-355), every policy,
+rate inf and finite, continuous and static mode.  Whole SimMetrics objects are
+compared with == (fp64 bit equality), exceptions by type name and message."""
+
+import math
+import pathlib
+import random
+import sys
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+REF = ROOT / "baseline" / "_ref"
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not (REF / "hetserve" / "__init__.py").exists(),
+                                 reason="baseline/_ref not vendored (python tools/vendor_reference.py)")]
+
+
+@pytest.fixture(scope="module")
+def ref():
+    sys.path.insert(0, str(REF))
+    import hetserve
+    import hetserve.simulator
+
+    yield hetserve
+    sys.path.remove(str(REF))
+
+
+def _scenario(ref, rng: random.Random, case: int):
+    n_mach = rng.randint(1, 3)
+    machines = tuple(ref.MachineSpec(f"m{i}", rng.choice([1, 2, 4]), rng.choice([200_000, 400_000, 900_000]),
+                                     "t") for i in range(n_mach))
+    model = ref.ModelSpec(layers=2, hidden_dim=4, param_count=100, bytes_per_param=2)  # 32 B/token
+    cluster = ref.ClusterSpec(model=model, engine=ref.EngineOverheads(1.0, 0), machines=machines,
+                              limits=ref.WorkloadLimits(max_input_len=64, max_output_len=64))
+    kind = case % 4
+    params = {}
+    for m in machines:
+        for t in ref.enumerate_tp_degrees(m):
+            p = [rng.uniform(1e-5, 1e-3), rng.uniform(1e-4, 1e-2), rng.uniform(1e-6, 1e-4), rng.uniform(1e-3, 1e-2),
+                 rng.uniform(1e-7, 1e-5), rng.uniform(1e-5, 1e-3), rng.uniform(1e-7, 1e-5), rng.uniform(1e-4, 1e-3)]
+            if kind == 1:  # negative decode terms: step costs can go negative
+                p[5] = -rng.uniform(1e-4, 3e-3)
+                p[7] = -rng.uniform(0, 1e-3)
+            elif kind == 2:  # constant-only prefill, zero decode: many steps at one time
+                p = [0.0, rng.choice([1.0, 0.5]), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0]
+            params[(m.name, t)] = ref.LatencyParams(*p)
+    degrees = {m.name: rng.choice(ref.enumerate_tp_degrees(m)) for m in machines}
+    config = ref.deployment_for(machines, degrees)
+    q = rng.randint(20, 250)
+    ids = [f"r{k}" for k in range(q)]
+    if kind == 3 or rng.random() < 0.5:  # repeated ids
+        for _ in range(rng.randint(1, 4)):
+            a, b = sorted(rng.sample(range(q), 2))
+            ids[b] = ids[a]
+    trace = tuple(ref.Request(ids[k], rng.randint(1, 64), o, o) for k, o in
+                  ((k, rng.randint(1, 64)) for k in range(q)))
+    policy_name = rng.choice(["OS", "OS", "RR", "WRR", "SI", "MB"])
+    n_inst = sum(p.instance_count for p in config.per_machine)
+    wrr = tuple(float(rng.randint(1, 4)) for _ in range(n_inst)) if policy_name == "WRR" else None
+    policy = ref.PolicyConfig(policy=policy_name, theta=rng.choice([0.5, 2.0]), wrr_weights=wrr)
+    mode = "static" if rng.random() < 0.2 else "continuous"
+    rate = math.inf if (mode == "static" or rng.random() < 0.3) else rng.choice([5.0, 40.0, 400.0])
+    return ref.simulator.Scenario(cluster=cluster, config=config, trace=trace, arrival_rate=rate, policy=policy,
+                                  mode=mode, seed=rng.randint(0, 99), params=params)
+
+
+def _outcome(fn, scenario):
+    try:
+        return "ok", fn(scenario)
+    except Exception as exc:  # noqa: BLE001 -- compared by type name and message
+        return "err", (type(exc).__name__, str(exc))
+
+
+def test_fuzzed_scenarios_match_live_reference(ref):
+    from paper_2504_15303_b200 import refbind
+
+    binding = refbind.bindings(ref)
+    S = sys.modules["hetserve.simulator"]
+    ours = {name: fn for (mod, name), fn in binding.items() if mod is S}
+    n_dup = n_err = n_neg = 0
+    for case in range(240):
+        rng = random.Random(case)
+        sc = _scenario(ref, rng, case)
+        run_ref = S.run_static if sc.mode == "static" else S.run_continuous
+        run_gpu = ours["run_static"] if sc.mode == "static" else ours["run_continuous"]
+        want = _outcome(run_ref, sc)
+        got = _outcome(run_gpu, sc)
+        assert got == want, (case, sc.mode, sc.policy.policy, sc.arrival_rate, want[1] if want[0] == "err" else "",
+                             got[1] if got[0] == "err" else "")
+        n_dup += len({r.id for r in sc.trace}) < len(sc.trace)
+        n_err += want[0] == "err"
+        n_neg += case % 4 == 1 and want[0] == "ok"
+    assert n_dup > 50 and n_err > 10 and n_neg > 10, (n_dup, n_err, n_neg)

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(nat.EXPORTS) == declared
-    assert lib.hs_abi_version() == 3
+    assert lib.hs_abi_version() == 4
 
 
 def test_no_cuda_means_engine_unavailable_not_fallback():
