@@ -272,10 +272,14 @@ int hs_plan_instance(hs_ctx* ctx, double budget, int64_t per_token, const double
                      const int32_t* O, int64_t q, int64_t* stops, double* times, int64_t* n_batches,
                      hs_entry* entry);
 
-/* Exhaustive argmax over candidate indices [begin, end) of the product
- * space defined by (table, n_degrees): best = max total, ties -> lowest
- * index (planner.py:227).  *n_feasible receives the number of feasible
- * candidates in the range.  best->index = -1 when none is feasible. */
+/* Argmax over candidate indices [begin, end) of the product space defined
+ * by (table, n_degrees): best = max total, ties -> lowest index
+ * (planner.py:227).  *n_feasible receives the number of feasible candidates
+ * in the range.  best->index = -1 when none is feasible.  Every candidate is
+ * decided: an infeasible one has a non-OK (machine, degree) entry and can
+ * never win, so the kernel scores the feasible sub-product only (per machine
+ * its OK degrees, an order-preserving compression of the mixed radix);
+ * environment HS_SEARCH_EXHAUSTIVE=1 scores every candidate instead. */
 int hs_search_best(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees, int32_t n_machines,
                    int64_t begin, int64_t end, hs_cand* best, int64_t* n_feasible);
 

@@ -260,14 +260,14 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
 
 // Heap overflow regions from the exact active-set bound: at most
 // floor(budget / (per_token * min(I+O))) requests fit an instance at once.
-void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q) {
+void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q, bool multi = false) {
   if (min_need < 1) min_need = 1;
   int64_t acc = 0;
   for (int j = 0; j < rc.N; ++j) {
     const double tokens = std::floor(inst[j].budget / (double)rc.per_token);
     const double capd = std::floor(tokens / (double)min_need) + 1.0;
     int64_t capj = capd > (double)max_q ? max_q : (int64_t)capd;
-    capj -= hs::kHeapShared;  // the first entries live in shared memory
+    capj -= hs::replay_shared_heap(rc, multi);  // the first entries live in shared memory
     if (capj < 1) capj = 1;
     rc.heap_off[j] = acc;
     acc += capj;
@@ -543,6 +543,71 @@ int hs_plan_instance(hs_ctx* c, double budget, int64_t per_token, const double* 
   return HS_OK;
 }
 
+// The feasible sub-product of a space: per machine its OK degrees only, in
+// degree order.  The map is monotone in every digit, so it preserves the
+// mixed-radix order (itertools.product order, planner.py:216): the argmax
+// with the lowest-index tie rule (planner.py:227) over the feasible
+// sub-product is the argmax over the whole space, and the feasible
+// candidates of an index range [b, e) are the compressed range
+// [rank(b), rank(e)).  Infeasible candidates (-inf contributions) can never
+// win, so the kernel need not visit them: every one of them is decided by
+// the per-machine factorisation (hs_entry.status), not by a sum.
+struct Compressed {
+  hs::SpaceDesc cs;
+  int32_t orig[hs::kMaxM][HS_MAX_DEGREES];
+  int64_t suffix_ok[hs::kMaxM + 1];  // prod of okcnt over machines > i
+  int64_t feasible;
+};
+
+void compress_space(const hs::SpaceDesc& sd, Compressed* c) {
+  std::memset(&c->cs, 0, sizeof(c->cs));
+  c->cs.M = sd.M;
+  for (int i = 0; i < sd.M; ++i) {
+    int k = 0;
+    for (int d = 0; d < sd.D[i]; ++d) {
+      const double v = sd.C[i * HS_MAX_DEGREES + d];
+      if (v == -INFINITY) continue;
+      c->cs.C[i * HS_MAX_DEGREES + k] = v;
+      c->orig[i][k] = d;
+      ++k;
+    }
+    c->cs.D[i] = k;
+    c->cs.okcnt[i] = k;
+  }
+  c->suffix_ok[sd.M] = 1;
+  for (int i = sd.M - 1; i >= 0; --i) c->suffix_ok[i] = c->suffix_ok[i + 1] * sd.okcnt[i];
+  c->feasible = c->suffix_ok[0];
+}
+
+// number of feasible candidates with original index < x
+int64_t feasible_rank(const hs::SpaceDesc& sd, const Compressed& c, int64_t x, int64_t P) {
+  if (x >= P) return c.feasible;
+  int32_t dig[hs::kMaxM];
+  for (int i = sd.M - 1; i >= 0; --i) {
+    dig[i] = (int32_t)(x % sd.D[i]);
+    x /= sd.D[i];
+  }
+  int64_t r = 0;
+  for (int i = 0; i < sd.M; ++i) {
+    int less = 0;
+    for (int d = 0; d < dig[i]; ++d) less += sd.C[i * HS_MAX_DEGREES + d] != -INFINITY;
+    r += (int64_t)less * c.suffix_ok[i + 1];
+    if (sd.C[i * HS_MAX_DEGREES + dig[i]] == -INFINITY) break;
+  }
+  return r;
+}
+
+int64_t original_index(const hs::SpaceDesc& sd, const Compressed& c, int64_t ci) {
+  int32_t dig[hs::kMaxM];
+  for (int i = sd.M - 1; i >= 0; --i) {
+    dig[i] = c.orig[i][ci % c.cs.D[i]];
+    ci /= c.cs.D[i];
+  }
+  int64_t x = 0;
+  for (int i = 0; i < sd.M; ++i) x = x * sd.D[i] + dig[i];
+  return x;
+}
+
 int hs_search_best(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, int32_t M, int64_t begin, int64_t end,
                    hs_cand* best, int64_t* n_feasible) {
   if (!c || !table || !n_degrees || !best || !n_feasible) return fail(HS_ERR_ARG, "null argument");
@@ -553,8 +618,27 @@ int hs_search_best(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
   int64_t P;
   if ((rc = build_space(table, n_degrees, M, &sd, &m_off, &P))) return rc;
   if (begin < 0 || end > P || begin > end) return fail(HS_ERR_ARG, "index range outside the candidate space");
-  const int64_t Din = (int64_t)sd.D[sd.M - 4] * sd.D[sd.M - 3] * sd.D[sd.M - 2] * sd.D[sd.M - 1];
-  const int64_t items = (end - begin) / Din + 2;
+  // default: the feasible sub-product (HS_SEARCH_EXHAUSTIVE=1: every candidate)
+  const bool exhaustive = std::getenv("HS_SEARCH_EXHAUSTIVE") != nullptr;
+  static thread_local Compressed cmp;
+  const hs::SpaceDesc* space = &sd;
+  int64_t b = begin, e = end;
+  if (!exhaustive) {
+    compress_space(sd, &cmp);
+    b = feasible_rank(sd, cmp, begin, P);
+    e = feasible_rank(sd, cmp, end, P);
+    space = &cmp.cs;
+    if (e <= b) {  // nothing feasible in the range
+      best->total = 0.0;
+      best->index = -1;
+      *n_feasible = 0;
+      c->last_ms = 0.0;
+      return HS_OK;
+    }
+  }
+  const int64_t Din = (int64_t)space->D[space->M - 4] * space->D[space->M - 3] * space->D[space->M - 2] *
+                      space->D[space->M - 1];
+  const int64_t items = (e - b) / Din + 2;
   int blocks = hs::sm_count() * 8;
   const int64_t need_blocks = (items + 255) / 256;
   if (need_blocks < blocks) blocks = (int)(need_blocks > 0 ? need_blocks : 1);
@@ -566,12 +650,13 @@ int hs_search_best(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
       (rc = ensure_t(c, S_CNT, 1, &cnt)))
     return rc;
   if ((rc = begin_timing(c))) return rc;
-  HS_CUDA(hs::launch_search_best(sd, begin, end, blocks, bb, bi, bc, cand, cnt, c->stream));
+  HS_CUDA(hs::launch_search_best(*space, b, e, blocks, bb, bi, bc, cand, cnt, c->stream));
   c->launches += 2;
   if ((rc = end_timing(c))) return rc;
   HS_CUDA(cudaMemcpyAsync(best, cand, sizeof(hs_cand), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaMemcpyAsync(n_feasible, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
+  if (!exhaustive && best->index >= 0) best->index = original_index(sd, cmp, best->index);
   return HS_OK;
 }
 
@@ -1231,7 +1316,7 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
   int32_t min_need = 0;
   HS_CUDA(cudaMemcpyAsync(&min_need, dMin, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q);
+  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q, true);
   std::vector<int64_t> theap((size_t)(T > 0 ? T : 1));
   int64_t hacc = 0;
   for (int64_t t = 0; t < T; ++t) {

@@ -46,8 +46,7 @@ def _scenario(ref, rng: random.Random, case: int):
             p = [rng.uniform(1e-5, 1e-3), rng.uniform(1e-4, 1e-2), rng.uniform(1e-6, 1e-4), rng.uniform(1e-3, 1e-2),
                  rng.uniform(1e-7, 1e-5), rng.uniform(1e-5, 1e-3), rng.uniform(1e-7, 1e-5), rng.uniform(1e-4, 1e-3)]
             if kind == 1:  # negative decode terms: step costs can go negative
-                p[5] = -rng.uniform(1e-4, 3e-3)
-                p[7] = -rng.uniform(0, 1e-3)
+                p[7] = -rng.uniform(1e-3, 2e-2)  # short steps of small batches cost < 0
             elif kind == 2:  # constant-only prefill, zero decode: many steps at one time
                 p = [0.0, rng.choice([1.0, 0.5]), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0]
             params[(m.name, t)] = ref.LatencyParams(*p)
@@ -55,7 +54,7 @@ def _scenario(ref, rng: random.Random, case: int):
     config = ref.deployment_for(machines, degrees)
     q = rng.randint(20, 250)
     ids = [f"r{k}" for k in range(q)]
-    if kind == 3 or rng.random() < 0.5:  # repeated ids
+    if kind == 3 or rng.random() < 0.2:  # repeated ids
         for _ in range(rng.randint(1, 4)):
             a, b = sorted(rng.sample(range(q), 2))
             ids[b] = ids[a]
@@ -97,4 +96,4 @@ def test_fuzzed_scenarios_match_live_reference(ref):
         n_dup += len({r.id for r in sc.trace}) < len(sc.trace)
         n_err += want[0] == "err"
         n_neg += case % 4 == 1 and want[0] == "ok"
-    assert n_dup > 50 and n_err > 10 and n_neg > 10, (n_dup, n_err, n_neg)
+    assert n_dup > 40 and n_err > 10 and n_neg > 20, (n_dup, n_err, n_neg)
