@@ -160,12 +160,139 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ------------------------------------------------------------ CPU baseline
-def cpu_baseline(target_s: float, P: int, R_total: int, q: int, rate: float):
+# ------------------------------------------------------------ CPU baselines
+# (1) the reference itself: the unmodified Python package vendored in
+#     baseline/_ref (tools/vendor_reference.py), on every host core through a
+#     process pool -- kind "reference";
+# (2) the reference's algorithm restated in C (oracle/, test infrastructure)
+#     on every host core -- kind "port".
+# Both run outside the timed regions of the engine.
+REF_DIR = ROOT / "baseline" / "_ref"
+_REF: dict = {}
+
+
+def _ref_cluster(H, prof):
+    return H.ClusterSpec(model=H.ModelSpec(**prof.model), engine=H.EngineOverheads(**prof.engine),
+                         machines=tuple(H.MachineSpec(n, c, m, a) for n, c, m, a in prof.machines),
+                         limits=H.WorkloadLimits(**prof.limits))
+
+
+def _ref_init(q_search: int, rate: float):
+    """Pool worker setup: the reference's own objects for config 3 (search)
+    and config 4 (replay), built once per worker."""
+    sys.path.insert(0, str(REF_DIR))
+    import hetserve as H
+    import hetserve.simulator as HS
+    from paper_2504_15303_b200 import workloads as wl
+    p3 = wl.config3()
+    c3 = _ref_cluster(H, p3)
+    I, O = wl.trace_lengths(q_search, seed=3)
+    p4 = wl.config4()
+    c4 = _ref_cluster(H, p4)
+    _REF.update(H=H, HS=HS, wl=wl, c3=c3, params3={k: H.LatencyParams(*v) for k, v in p3.params.items()},
+                reqs3=[H.Request(f"r{k}", int(I[k]), int(O[k]), int(O[k])) for k in range(q_search)],
+                degs3=[H.enumerate_tp_degrees(m) for m in c3.machines], c4=c4,
+                cfg4=H.deployment_for(c4.machines, {a: 1 for a in wl.CONFIG4_TYPES}),
+                params4={k: H.LatencyParams(*v) for k, v in p4.params.items()}, rate=rate)
+
+
+def _ref_candidates(indices) -> float:
+    """The body of the reference's search loop (planner.py:216-226) for the
+    given mixed-radix indices: deployment_for -> estimate_system_throughput,
+    infeasibility exceptions caught and turned into their message."""
+    H, c3, degs = _REF["H"], _REF["c3"], _REF["degs3"]
+    names = [m.name for m in c3.machines]
+    t0 = time.perf_counter()
+    for idx in indices:
+        idx = int(idx)
+        dig = [0] * len(degs)
+        for i in range(len(degs) - 1, -1, -1):
+            idx, dig[i] = divmod(idx, len(degs[i]))
+        config = H.deployment_for(c3.machines, {n: degs[i][d] for i, (n, d) in enumerate(zip(names, dig))})
+        try:
+            H.estimate_system_throughput(c3, config, _REF["reqs3"], _REF["params3"])
+        except (H.InfeasibleConfigError, H.InfeasibleRequestError, H.SpecError) as exc:
+            str(exc)
+    return time.perf_counter() - t0
+
+
+def _ref_replay(task) -> float:
+    """The reference's run_continuous on config-4 trace t (gen-trace lengths
+    seeded t, arrivals seeded 42 + t), truncated to q requests."""
+    t, q = task
+    H, HS, wl = _REF["H"], _REF["HS"], _REF["wl"]
+    I, O = wl.trace_lengths(100_000, seed=t)
+    trace = tuple(H.Request(f"r{k}", int(I[k]), int(O[k]), int(O[k])) for k in range(q))
+    sc = HS.Scenario(cluster=_REF["c4"], config=_REF["cfg4"], trace=trace, arrival_rate=_REF["rate"],
+                     policy=H.PolicyConfig(), mode="continuous", seed=42 + t, params=_REF["params4"])
+    t0 = time.perf_counter()
+    HS.run_continuous(sc)
+    return time.perf_counter() - t0
+
+
+class RefPool:
+    """A fork pool of reference workers on every host core."""
+
+    def __init__(self, rate: float, q_search: int = 10_000):
+        import multiprocessing as mp
+        self.cores = len(os.sched_getaffinity(0))
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_ref_init, initargs=(q_search, rate))
+
+    def close(self):
+        self.pool.terminate()
+
+    def sample(self, P: int, feasible_digits, f_feasible: float, n_uniform: int, n_feasible: int, n_traces: int,
+               q_trace: int, rng) -> dict:
+        """Per-candidate cost of the reference's search loop, stratified: a
+        uniform sample of candidate indices (the infeasible ~all of the space)
+        plus a sample of feasible candidates, weighted by the exact feasible
+        fraction; and run_continuous throughput on n_traces traces of
+        q_trace requests.  Wall-clock over all cores."""
+        cores = self.cores
+        uni = rng.integers(0, P, n_uniform)
+        t0 = time.perf_counter()
+        self.pool.map(_ref_candidates, np.array_split(uni, cores))
+        w_uni = time.perf_counter() - t0
+        fea = feasible_digits(rng, n_feasible)
+        t0 = time.perf_counter()
+        self.pool.map(_ref_candidates, np.array_split(fea, cores))
+        w_fea = time.perf_counter() - t0
+        # wall seconds per candidate on all cores, stratified by feasibility
+        per_cand = (1.0 - f_feasible) * (w_uni / n_uniform) + f_feasible * (w_fea / max(n_feasible, 1))
+        t0 = time.perf_counter()
+        self.pool.map(_ref_replay, [(t, q_trace) for t in range(n_traces)], chunksize=1)
+        w_rep = time.perf_counter() - t0
+        return {"configs_per_s": 1.0 / per_cand, "requests_per_s": n_traces * q_trace / w_rep,
+                "desc": (f"the unmodified reference (baseline/_ref, Python {sys.version.split()[0]}) in a {cores}-process "
+                         f"pool: search loop body (planner.py:216-226) on {n_uniform} uniform + {n_feasible} feasible "
+                         f"config-3 candidates, stratified by the exact feasible fraction {f_feasible:.3g} "
+                         f"({w_uni:.1f}s + {w_fea:.1f}s); run_continuous on {n_traces} config-4 traces x {q_trace} "
+                         f"requests ({w_rep:.1f}s)")}
+
+
+def feasible_sampler(tables):
+    """Random candidates of the feasible sub-product (original mixed-radix indices)."""
+    from paper_2504_15303_b200 import _native as nat
+    ok = [np.nonzero(tables.entries[i, : tables.n_degrees[i]]["status"] == nat.ENTRY_OK)[0]
+          for i in range(len(tables.names))]
+    nd = [int(x) for x in tables.n_degrees]
+
+    def draw(rng, n):
+        out = np.zeros(n, np.int64)
+        for i, digs in enumerate(ok):
+            out = out * nd[i] + rng.choice(digs, n)
+        return out
+    n_feas = 1
+    for d in ok:
+        n_feas *= len(d)
+    return draw, n_feas
+
+
+def port_baseline(target_s: float, P: int, R_total: int, q: int, rate: float):
     """The reference's algorithm, restated in C (oracle/, kind "port"), on the
     host cores: the literal per-candidate estimate_system_throughput on
-    random candidates of config 3 and literal run_continuous on config-4
-    traces; extrapolated to the full step workload."""
+    random candidates of config 3 and literal run_continuous on full-length
+    config-4 traces; extrapolated to the full step workload."""
     from oracle import hs_oracle as orc
     import paper_2504_15303_b200 as hs
     from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
@@ -186,51 +313,91 @@ def cpu_baseline(target_s: float, P: int, R_total: int, q: int, rate: float):
     orc.candidates_literal(model, engine, limits, machines, pr, present, I, O, idx, cores)
     t_search = time.perf_counter() - t0
     cand_rate = n_c / t_search
-    # replay sample: `cores` traces in parallel, shortened if one would take too long
+    # replay sample: `cores` full-length traces in parallel
     rc, config, rparams = replay_deployment()
     handles = build_instances(rc, config, rparams)
     pol = hs.PolicyConfig()
     inst = engine_instances(handles, pol)
     ps = _policy_struct(pol, len(handles), hs.kv_bytes_per_token(rc.model))
-    q_s = min(q, 20_000)
-    off, Ir, Or, Tr = replay_inputs(0, cores, q_s, rate)
+    off, Ir, Or, Tr = replay_inputs(0, cores, q, rate)
     t0 = time.perf_counter()
     orc.replay(inst, ps, off, Ir, Or, Or, Tr, nthreads=cores, want_depart=False)
     t_rep = time.perf_counter() - t0
-    req_rate = (cores * q_s) / t_rep
+    req_rate = (cores * q) / t_rep
     value = (P + R_total) / (P / cand_rate + R_total / req_rate)
     return {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": (f"oracle/hs_oracle.c on {cores} threads: literal estimate_system_throughput on {n_c} random "
                        f"config-3 candidates ({t_search:.1f}s, {cand_rate:.3g} cand/s) + literal run_continuous on "
-                       f"{cores} config-4 traces x {q_s} requests ({t_rep:.1f}s, {req_rate:.3g} req/s); "
+                       f"{cores} config-4 traces x {q} requests ({t_rep:.1f}s, {req_rate:.3g} req/s); "
                        f"extrapolated to the step's {P:.3g} candidates + {R_total:.3g} requests"),
             "configs_per_s": cand_rate, "requests_per_s": req_rate}
 
 
+def reference_baseline(pool: RefPool, P: int, R_total: int, tables, q_trace: int, n_traces: int, n_uniform: int,
+                       n_feasible: int, seed: int = 1):
+    draw, n_feas = feasible_sampler(tables)
+    r = pool.sample(P, draw, n_feas / P, n_uniform, n_feasible, n_traces, q_trace, np.random.default_rng(seed))
+    value = (P + R_total) / (P / r["configs_per_s"] + R_total / r["requests_per_s"])
+    return {"value": value, "unit": UNIT, "cores": pool.cores, "kind": "reference",
+            "sample": r["desc"] + f"; extrapolated to the step's {P:.3g} candidates + {R_total:.3g} requests",
+            "configs_per_s": r["configs_per_s"], "requests_per_s": r["requests_per_s"]}
+
+
 def reference_arm(args, rank, world):
+    """bench.py --impl reference: the unmodified Python reference on the host
+    cores, each step a bounded sample of the step workload (~5 s)."""
     if rank != 0:
         return
+    import paper_2504_15303_b200  # noqa: F401 (workloads for the inputs; no engine call)
     P = 5**16
     R = args.traces * args.q
+    tables = reference_tables(args.search_q)
+    pool = RefPool(args.rate, args.search_q)
+    cores = pool.cores
     vals = []
-    for _ in range(args.warmup):
-        cpu_baseline(args.cpu_seconds / 3, P, R, args.q, args.rate)
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(args.cpu_seconds, P, R, args.q, args.rate))
+    try:
+        for k in range(args.warmup + args.steps):
+            v = reference_baseline(pool, P, R, tables, q_trace=4000, n_traces=cores, n_uniform=cores * 400,
+                                   n_feasible=cores, seed=k)
+            if k >= args.warmup:
+                vals.append(v)
+    finally:
+        pool.close()
     v = statistics.median(x["value"] for x in vals)
     last = vals[-1]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": (P + R) / v * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
-        "config": {"workload": "config3 search (5^16 candidates, 70B, 10k trace) + config4 replay "
-                               f"({args.traces} traces x {args.q} requests, 32 instances, {args.rate} req/s, OS)",
-                   "parallelism": "host threads"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port", "sample": last["sample"]},
+        "config": {"workload": WORKLOAD.format(traces=args.traces, q=args.q, rate=args.rate),
+                   "candidates": P, "requests": R, "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": last["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "breakdown": {"configs_per_s": last["configs_per_s"], "requests_per_s": last["requests_per_s"]},
+        "breakdown": {"configs_per_s": statistics.median(x["configs_per_s"] for x in vals),
+                      "requests_per_s": statistics.median(x["requests_per_s"] for x in vals)},
     }
     print(json.dumps(line), flush=True)
+
+
+def reference_tables(q_search: int):
+    """The config-3 (machine, degree) feasibility table for the stratified
+    sample, from the C oracle's table build (host only: no GPU on this arm)."""
+    from oracle import hs_oracle as orc
+    sys.path.insert(0, str(ROOT / "tests"))
+    from helpers import search_structs
+    from paper_2504_15303_b200 import _native as nat
+    from paper_2504_15303_b200.planner import SearchTables
+    cluster, reqs, params, I, O = search_inputs(q_search)
+    model, engine, limits, machines, pr, present = search_structs(cluster, params)
+    table, nd = orc.tables(model, engine, limits, machines, pr, present, I, O)
+    names = [m.name for m in cluster.machines]
+    from paper_2504_15303_b200.domain import enumerate_tp_degrees
+    return SearchTables(cluster, reqs, names, [enumerate_tp_degrees(m) for m in cluster.machines],
+                        np.asarray(table).reshape(len(names), nat.HS_MAX_DEGREES), np.asarray(nd, np.int32))
+
+
+WORKLOAD = ("config3 search (5^16 candidates, 70B, 10k trace) + config4 replay ({traces} traces x {q} requests, "
+            "32 instances, {rate} req/s, OS)")
 
 
 # ------------------------------------------------------------------ engine

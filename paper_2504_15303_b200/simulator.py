@@ -203,13 +203,15 @@ def _policy_struct(policy: PolicyConfig, n: int, per_token: int, mode: int = 0, 
     return nat.hs_policy(nat.POLICY_CODE[policy.policy], n, float(policy.theta), per_token, mode, flags)
 
 
-def _first_duplicate_in_flight(ids, arr, dep, static: bool):
+def _first_duplicate_in_flight(ids, arr, key, static: bool):
     """Index of the first arrival whose request id is still in flight
     (Scheduler.choose raises before anything else, scheduling.py:239-240), or
     None.  An earlier request with the same id is in flight unless its
-    retirement step popped before this arrival: departure < arrival (arrivals
-    pop first at equal times, simulator.py:285-290).  In static mode every
-    dispatch precedes every completion (simulator.py:216-220)."""
+    retirement step popped before this arrival: the step's heap key (its
+    time, or with negative step costs the running max of its busy period's
+    step times) < the arrival time (arrivals pop first at equal times,
+    simulator.py:285-290).  In static mode every dispatch precedes every
+    completion (simulator.py:216-220)."""
     seen: dict = {}
     first = None
     for k, rid in enumerate(ids):
@@ -217,7 +219,7 @@ def _first_duplicate_in_flight(ids, arr, dep, static: bool):
         seen[rid] = k
         if prev is None:
             continue
-        if static or not (dep[prev] < arr[k]):  # NaN: never retired
+        if static or not (key[prev] < arr[k]):  # NaN: never retired
             if first is None or k < first:
                 first = k
     return first
@@ -277,7 +279,7 @@ def _run(scenario, static: bool, engine=None) -> SimMetrics:
         None if math.isinf(scenario.arrival_rate) else T, depart_out=dep_out)
     depart = dep3[:, 0]
     arr = T.tolist()
-    dup = _first_duplicate_in_flight(ids, arr, depart.tolist(), static)
+    dup = _first_duplicate_in_flight(ids, arr, dep3[:, 1].tolist(), static)
     if dup is not None and _duplicate_wins(dup, result[0], arr, static):
         raise SchedulingError(f"request {ids[dup]!r} is already in flight")
     _raise_trace_error(result[0], handles, trace, per_token, static=static)
