@@ -53,10 +53,8 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", choices=["config34", "config5"], default="config34",
-                    help="config34 (default line): config-3 search + config-4 replay; config5: top-k search "
-                         "+ every top-k deployment replayed on its own copy of one trace")
     ap.add_argument("--topk", type=int, default=1024)
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 sub-record of the default line")
     return ap.parse_args()
 
 
@@ -525,18 +523,20 @@ def engine_arm(args, rank, world, local_rank):
         rc_, config_, rparams_ = rc, config, rparams
         aseeds = [42 + t for t in tseeds]
         hA = eng.host_array((max(nreq, 1),), np.uint8)  # page-locked result buffer, reused every step
-        e2e_parts = {"replay_call_ms": [], "replay_pipeline_ms": []}
+        e2e_parts = {"search_call_ms": [], "replay_call_ms": [], "replay_pipeline_ms": []}
 
         def e2e_step():
+            w0 = time.perf_counter()
             t = planner.build_tables(cluster, reqs, params, engine=eng)
             total, idx, nfeas, _ = planner.search_best(t, lo, hi, engine=eng)
+            w1 = time.perf_counter()
+            e2e_parts["search_call_ms"].append((w1 - w0) * 1e3)
             # arrivals drawn on the device from the seeds, inside the call, as
             # run_continuous draws them (simulator.py:112-124)
-            w0 = time.perf_counter()
             r = hs.replay_traces(rc_, config_, rparams_, pol, off, hI, hO, hO, rate=args.rate,
                                  arrival_seeds=aseeds, want_assign=True, assign_out=hA,
                                  want_depart=False, engine=eng)
-            e2e_parts["replay_call_ms"].append((time.perf_counter() - w0) * 1e3)
+            e2e_parts["replay_call_ms"].append((time.perf_counter() - w1) * 1e3)
             e2e_parts["replay_pipeline_ms"].append(eng.last_kernel_ms)
             assert (r.result["error"] == 0).all()
             return combine(total, idx, nfeas)
@@ -550,11 +550,14 @@ def engine_arm(args, rank, world, local_rank):
         d2h = nreq + nT * N * nat.METRICS_DTYPE.itemsize + nT * nat.RESULT_DTYPE.itemsize + \
             M * nat.HS_MAX_DEGREES * nat.ENTRY_DTYPE.itemsize + 16
         if dist:
-            h2d += 0
             d2h += world * 24
+        sc_ms = statistics.median(e2e_parts["search_call_ms"][-args.steps:])
+        rc_ms = statistics.median(e2e_parts["replay_call_ms"][-args.steps:])
         e2e = {"value": units / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
                "d2h_bytes_per_step": int(d2h * world), "ms_per_step": e2e_ms,
-               "replay_call_ms": statistics.median(e2e_parts["replay_call_ms"][-args.steps:]),
+               # the two halves of the metric, each through its own public call (rank 0's wall clock)
+               "configs_per_s": P / (sc_ms / 1e3), "requests_per_s": R_total / (rc_ms / 1e3),
+               "search_call_ms": sc_ms, "replay_call_ms": rc_ms,
                "replay_pipeline_ms": statistics.median(e2e_parts["replay_pipeline_ms"][-args.steps:])}
 
     # ---- roofline of the dominant kernel (K3 replay)
@@ -573,20 +576,20 @@ def engine_arm(args, rank, world, local_rank):
     if prof.exists():
         pj = json.loads(prof.read_text())
         if pj.get("dram_bytes_per_dispatch"):
-            traffic = pj["dram_bytes_per_dispatch"] * nreq
+            traffic = pj["dram_bytes_per_dispatch"] * BYTES_PER_DISPATCH / BYTES_PER_DISPATCH * nreq
         inst_per_dispatch = pj.get("warp_inst_per_dispatch")
     fp64_peak = eng.probe_fp64()
-    cand_local = hi - lo
-    k2_fp64 = 2.0 * cand_local / (k2 / 1e3)
+    # K2 scores the feasible sub-product only (every infeasible candidate is
+    # decided by its non-OK (machine, degree) entry): 1 DADD + 1 compare per
+    # feasible candidate of this rank's range
+    _t, _i, nfeas_local, _ms = planner.search_best(tables, lo, hi, engine=eng)
+    k2_fp64 = 2.0 * nfeas_local / (k2 / 1e3)
     # K3 against the FP64 pipe with the reference-literal op count of SURVEY
     # section 8(d): OS scoring ~67 FP64 ops per instance per dispatch
     # (divides, floordiv, prefill, decode, exp, min-max) + ~15 per step event
     steps_per_req = n_steps_ev / max(nreq, 1)
     k3_ops_per_dispatch = N * 67 + 15 * steps_per_req
     k3_fp64 = k3_ops_per_dispatch * nreq / (k3 / 1e3)
-    # K3 against the instruction-issue roofline (what bounds it): the live
-    # dispatch rate times the warp instructions per dispatch ncu measured at
-    # this workload, vs one warp instruction per scheduler per SM cycle
     clocks = clk.summary()
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     issue_peak = 4.0 * n_sm * (clocks.get("sm_mhz") or 1965.0) * 1e6
@@ -598,22 +601,40 @@ def engine_arm(args, rank, world, local_rank):
                       "note": "instructions per dispatch from ncu at this workload (profiles/k3_replay_ncu.json, "
                               "smsp__inst_executed.sum / dispatches); peak = 4 schedulers x SMs x SM clock"}
 
+    c5 = None
+    if not args.no_config5:
+        c5 = config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, params)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.cpu_seconds, P, R_total, args.q, args.rate)
+        pool = RefPool(args.rate, args.search_q)
+        try:
+            cpu = reference_baseline(pool, P, R_total, tables, q_trace=args.q, n_traces=8,
+                                     n_uniform=pool.cores * 200, n_feasible=pool.cores * 2)
+            if c5 is not None:
+                c5["cpu_baseline"] = config5_reference_baseline(pool, args, cpu["configs_per_s"], c5)
+        finally:
+            pool.close()
+        cpu["port"] = port_baseline(args.cpu_seconds, P, R_total, args.q, args.rate)
 
+    if c5 is not None:
+        for key in ("_units", "_P", "_nreq", "top_indices"):
+            c5.pop(key, None)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (gen-trace lognormal lengths + Poisson arrivals, numpy PCG64 streams drawn on the GPU)",
-            "config": {"workload": "config3 search (5^16 candidates, 70B, 10k trace) + config4 replay "
-                                   f"({args.traces} traces x {args.q} requests, 32 instances, {args.rate} req/s, OS)",
+            "config": {"workload": WORKLOAD.format(traces=args.traces, q=args.q, rate=args.rate),
                        "candidates": P, "requests": R_total, "parallelism": f"shard{world}",
                        "l2": "inputs larger than L2 (replay inputs %.1f GB)" % (I.nbytes * 5 * world / 1e9),
                        "e2e_inputs": "host I/O lengths copied in; arrivals drawn on the device from per-trace seeds"},
+            "search": {"candidates_visited": P, "feasible_scored": best[2],
+                       "note": "every candidate is decided; K2 sums and compares only the feasible sub-product "
+                               "(an infeasible candidate holds a non-OK (machine, degree) entry and cannot win)"},
             "breakdown": {"k1_table_ms": k1, "k2_search_ms": k2, "k3_replay_ms": k3,
-                          "configs_per_s": P / (k2 / 1e3) if world == 1 else cand_local / (k2 / 1e3) * world,
+                          "configs_per_s": P / (k2 / 1e3) if world == 1 else (hi - lo) / (k2 / 1e3) * world,
+                          "feasible_scored_per_s": nfeas_local / (k2 / 1e3) * world,
                           "requests_per_s_kernel": nreq / (k3 / 1e3) * world,
                           "step_events_per_request": n_steps_ev / max(nreq, 1),
                           "best_total": best[0], "best_index": best[1], "n_feasible": best[2],
@@ -621,13 +642,13 @@ def engine_arm(args, rank, world, local_rank):
                           "gen_arrivals_kernel_ms": gen_arr_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "k_replay",
-                         "note": "replay is latency-bound (dependent event chains); see DESIGN.md"},
+                         "note": "replay is bound by dependent FP64 event chains, not bytes: see roofline_k3_fp64 "
+                                 "and DESIGN.md"},
             "roofline_k2": {"bound": "fp64", "achieved": k2_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
                             "frac": k2_fp64 / fp64_peak, "kernel": "k_search_best",
                             "peak_source": "hs_probe_fp64 DADD throughput measured in this run",
-                            "note": "algorithmic count: 2 ops per candidate (the left-to-right add and the "
-                                    "compare, SURVEY.md 8d); in non-negative spaces the kernel runs the "
-                                    "compare as an integer test on the total's high word (ALU pipe)"},
+                            "note": "2 FP64 ops (the left-to-right add and the compare, SURVEY.md 8d) per FEASIBLE "
+                                    "candidate scored; a launch of a few microseconds is bound by launch latency"},
             "roofline_k3_fp64": {"bound": "fp64", "achieved": k3_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
                                  "frac": k3_fp64 / fp64_peak, "kernel": "k_replay",
                                  "ops_per_dispatch": k3_ops_per_dispatch,
@@ -638,32 +659,33 @@ def engine_arm(args, rank, world, local_rank):
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "config5": c5,
         }
         print(json.dumps(line), flush=True)
     if dist:
         tdist.barrier(device_ids=[local_rank])
 
 
-def config5_arm(args, rank, world, local_rank):
-    """BASELINE config 5: top-k deployments of the config-3 space, each
-    re-scored by a full continuous-batching simulation of one trace
-    (rate = inf, OS).  Units = feasible candidates ranked + requests."""
+def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, params) -> dict | None:
+    """BASELINE config 5: the top-k deployments of the config-3
+    space (planner.py:227 order), each re-scored by a full continuous-batching
+    simulation of one 1e5-request trace (rate = inf, OS; simulator.py:60-80 +
+    run_continuous).  Units = feasible candidates ranked + requests replayed.
+    value: device time of the top-k and replay kernels; e2e: the same step
+    through the public calls with host buffers (search_topk, replay_candidates)."""
     import torch
     import paper_2504_15303_b200 as hs
     from paper_2504_15303_b200 import _native as nat
     from paper_2504_15303_b200 import planner
     from paper_2504_15303_b200.distributed import shard_range
+    from paper_2504_15303_b200 import workloads as wl
     dist = world > 1
     if dist:
         import torch.distributed as tdist
     dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    eng = nat.engine_for(local_rank)
-    ext = torch.cuda.ExternalStream(eng.stream, device=dev)
-    cluster, reqs, params, sI, sO = search_inputs(args.search_q)
-    from paper_2504_15303_b200 import workloads as wl
     I1, O1 = wl.trace_lengths(args.q, seed=0)
     tiles = {}
+    kk = args.topk
 
     def tiled(n):
         # every deployment replays the same trace: tiled once into page-locked buffers
@@ -677,10 +699,11 @@ def config5_arm(args, rank, world, local_rank):
 
     def step():
         t = planner.build_tables(cluster, reqs, params, engine=eng)
-        cands, nf, ms_topk = planner.search_topk(t, args.topk, rank, world, engine=eng)
+        k1 = eng.last_kernel_ms
+        cands, nf, ms_topk = planner.search_topk(t, kk, rank, world, engine=eng)
         if dist:  # one all-gather of the per-rank top-k lists
-            buf = torch.zeros(args.topk, 2, dtype=torch.int64, device=dev)
-            loc = np.zeros((args.topk, 2), np.int64)
+            buf = torch.zeros(kk, 2, dtype=torch.int64, device=dev)
+            loc = np.zeros((kk, 2), np.int64)
             loc[:, 1] = -1
             loc[:len(cands), 0] = cands["total"].view(np.int64)
             loc[:len(cands), 1] = cands["index"]
@@ -696,7 +719,7 @@ def config5_arm(args, rank, world, local_rank):
                 p["total"] = h[:, 0].view(np.float64)
                 p["index"] = h[:, 1]
                 parts.append(p)
-            top = planner.merge_topk(parts, args.topk)
+            top = planner.merge_topk(parts, kk)
             nf_all = torch.tensor([nf], dtype=torch.int64, device=dev)
             tdist.all_reduce(nf_all)
             nf = int(nf_all.item())
@@ -707,37 +730,90 @@ def config5_arm(args, rank, world, local_rank):
         off = np.arange(n + 1, dtype=np.int64) * args.q
         I, O = tiled(n)
         res = hs.replay_candidates(t, params, top["index"][lo:hi], hs.PolicyConfig(), np.arange(n), off, I, O, O,
-                                   engine=eng, want_assign=False)
+                                   engine=eng, want_assign=True)
         assert (res.result["error"] == 0).all()
-        return nf, ms_topk, res.kernel_ms, n
+        return nf, k1, ms_topk, res.kernel_ms, n, top, res
 
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup - 1)):
         step()
     if dist:
         tdist.barrier(device_ids=[local_rank])
     torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(ext)
+    kern, walls = [], []
     for _ in range(args.steps):
-        nf, ms_topk, ms_rep, n = step()
-    e1.record(ext)
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+        w0 = time.perf_counter()
+        nf, k1, ms_topk, ms_rep, n, top, res = step()
+        walls.append((time.perf_counter() - w0) * 1e3)
+        kern.append(k1 + ms_topk + ms_rep)
+    ms_k = statistics.median(kern)
+    ms_w = statistics.median(walls)
     if dist:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms_k, ms_w], dtype=torch.float64, device=dev)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        ms = float(tt.item())
-    units = nf + args.topk * args.q
-    if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": units / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
-            "config": {"workload": f"config5: top-{args.topk} of the config-3 space (70B), each deployment "
-                                   f"replayed on {args.q} requests (rate=inf, OS)",
-                       "feasible_candidates_ranked": nf, "requests": args.topk * args.q},
-            "breakdown": {"topk_ms": ms_topk, "replay_ms_rank0": ms_rep, "deployments_rank0": n}}), flush=True)
+        ms_k, ms_w = (float(x) for x in tt.tolist())
+    units = nf + kk * args.q
+    nreq = n * args.q
+    steps_per_req = float(res.result["n_steps"].sum()) / max(nreq, 1)
+    h2d = 2 * nreq * 4 + (n + 1) * 8
+    d2h = nreq + n * res.metrics.shape[1] * nat.METRICS_DTYPE.itemsize + n * nat.RESULT_DTYPE.itemsize
+    return {
+        "metric": METRIC, "value": units / (ms_k / 1e3), "unit": UNIT, "ms_per_step": ms_k,
+        "config": {"workload": f"config5: top-{kk} of the config-3 space (70B), each deployment replayed on "
+                               f"{args.q} requests (rate=inf, OS)",
+                   "feasible_candidates_ranked": nf, "requests": kk * args.q},
+        "breakdown": {"k1_table_ms": k1, "topk_ms": ms_topk, "replay_ms": ms_rep, "deployments_rank0": n,
+                      "step_events_per_request": steps_per_req, "requests_per_s_kernel": nreq / (ms_rep / 1e3)},
+        "roofline": {"bound": "hbm", "achieved": BYTES_PER_DISPATCH * nreq / (ms_rep / 1e3) / 1e9,
+                     "peak": json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6650.0)
+                     if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0,
+                     "unit": "GB/s", "kernel": "k_replay (multi-deployment)", "traffic": None},
+        "e2e": {"value": units / (ms_w / 1e3), "unit": UNIT, "ms_per_step": ms_w, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "note": "search_topk + replay_candidates with page-locked host traces (copies inside the call)"},
+        "top_indices": [int(x) for x in top["index"][:8]],
+        "_units": units, "_P": 5**16, "_nreq": kk * args.q,
+    }
+
+
+def _ref_replay5(task) -> float:
+    """The reference's run_continuous of config-3 candidate `index` at rate =
+    inf (OS) on the first q requests of the config-5 trace (seed 0)."""
+    index, q = task
+    H, HS, wl, c3, degs = _REF["H"], _REF["HS"], _REF["wl"], _REF["c3"], _REF["degs3"]
+    idx = int(index)
+    dig = [0] * len(degs)
+    for i in range(len(degs) - 1, -1, -1):
+        idx, dig[i] = divmod(idx, len(degs[i]))
+    config = H.deployment_for(c3.machines, {m.name: degs[i][d] for i, (m, d) in enumerate(zip(c3.machines, dig))})
+    I, O = wl.trace_lengths(100_000, seed=0)
+    trace = tuple(H.Request(f"r{k}", int(I[k]), int(O[k]), int(O[k])) for k in range(q))
+    sc = HS.Scenario(cluster=c3, config=config, trace=trace, arrival_rate=float("inf"), policy=H.PolicyConfig(),
+                     mode="continuous", seed=0, params=_REF["params3"])
+    t0 = time.perf_counter()
+    HS.run_continuous(sc)
+    return time.perf_counter() - t0
+
+
+def config5_reference_baseline(pool: RefPool, args, cand_per_s: float, c5: dict, q_s: int = 1500) -> dict:
+    """The unmodified reference on config 5's work: its search visits all 5^16
+    candidates (per-candidate cost from the main line's sample) before it can
+    rank; each top-k deployment is then a run_continuous at rate = inf,
+    sampled on the first q_s requests of the trace for `cores` of the top
+    deployments and extrapolated per request."""
+    idx = c5["top_indices"]
+    tasks = [(idx[k % len(idx)], q_s) for k in range(pool.cores)]
+    t0 = time.perf_counter()
+    pool.pool.map(_ref_replay5, tasks, chunksize=1)
+    w = time.perf_counter() - t0
+    req_rate = len(tasks) * q_s / w
+    P, nreq, units = c5["_P"], c5["_nreq"], c5["_units"]
+    value = units / (P / cand_per_s + nreq / req_rate)
+    return {"value": value, "unit": UNIT, "cores": pool.cores, "kind": "reference",
+            "sample": (f"the unmodified reference (baseline/_ref) in a {pool.cores}-process pool: run_continuous "
+                       f"(rate=inf, OS) of {len(tasks)} of the top deployments on the first {q_s} requests "
+                       f"({w:.1f}s, {req_rate:.3g} req/s) + the search loop at the main line's "
+                       f"{cand_per_s:.3g} candidates/s over all {P:.3g} candidates; extrapolated"),
+            "configs_per_s": cand_per_s, "requests_per_s": req_rate}
 
 
 def main():
@@ -753,10 +829,7 @@ def main():
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.workload == "config5":
-        config5_arm(args, rank, world, local_rank)
-    else:
-        engine_arm(args, rank, world, local_rank)
+    engine_arm(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as tdist
         tdist.destroy_process_group()

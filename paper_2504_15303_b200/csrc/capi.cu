@@ -273,6 +273,7 @@ void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, 
     acc += capj;
   }
   rc.heap_off[rc.N] = acc;
+  acc += hs::replay_extra_heap_entries(rc, multi);  // per-instance segment rings after the heaps
   rc.heap_stride = (acc + 15) / 16 * 16;
 }
 

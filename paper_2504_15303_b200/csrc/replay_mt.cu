@@ -1,26 +1,43 @@
-// replay_mt.cu -- K3, trace-group layout: four traces per warp, eight lanes
-// per trace, each lane owning up to four instances (j = lane + 8k).
+// replay_mt.cu -- K3 without per-arrival stepping: event order from rigorous
+// fp64 interval bounds, exact clocks recomputed in bulk from a segment log.
 //
-// Same semantics, bit for bit, as replay.cu (simulator.py:272-363
+// Same results, bit for bit, as replay.cu (simulator.py:272-363
 // run_continuous with scheduling.py:216-346 Scheduler.evaluate / choose /
 // complete and the RR / WRR / SI / MB baselines); see replay.cu's header for
 // why every instance may advance independently between arrivals.
 //
-// Why this layout: with one warp per trace and one lane per instance, each
-// arrival costs as many SIMT passes as its busiest instance needs steps
-// (~35 for the fastest class at config 4), while ~9 of 32 lanes do work, and
-// every event step (retirement / admission, 1-2 lanes) costs a whole warp
-// pass.  Here a lane steps its instances one after another, and the instances
-// are dealt so that every lane owns one instance of each class when the
-// deployment lists classes in blocks of eight (config 4: b200/h100/a800/v100
-// x 8): every lane then carries the same step load, and four traces share
-// every warp instruction.  The price is lockstep across the warp's four
-// traces: an arrival costs the warp the steps of the trace with the longest
-// inter-arrival gap.  Dispatch reductions are 3-level shuffles inside the
-// eight-lane group.
+// What an arrival at t_a needs from an instance is only which of its EVENT
+// steps (a retirement, or an admission after a dispatch) happen before t_a:
+// load and running tokens change at events only, and between two events the
+// instance runs "pure" steps whose clock is t += price(cached length), with
+// the batch fixed.  A retirement's step INDEX is known at admission
+// (admission step + O, simulator.py:334), so the next event's index is known;
+// only its TIME needs the serial fp64 sum of the pure steps' prices.  Instead
+// of running that sum per arrival (per-instance step counts per arrival vary
+// with the exponential arrival gaps and the instance speeds, so SIMT lanes
+// idle), the kernel bounds it in O(1): with non-negative coefficients every
+// price lies in [P(x)(1-u)^4, P(x)(1+u)^4] for the affine
+// P(x) = (A + p7) x + (B + p8), and a chain of n additions of non-negative
+// terms lies in [S(1-u)^n, S(1+u)^n] around the exact sum S (u = 2^-53);
+// directed-rounding arithmetic evaluates both ends.  An event is due before
+// t_a when the upper bound is below t_a and not due when the lower bound is at
+// or above it; otherwise (a relative width of ~1e-13: practically never) the
+// exact chain decides.  Every event appends a segment record (event step, its
+// cost, the batch size, the cached length) to a per-instance ring in global
+// memory, and the exact clock chains -- which the outputs need (departure and
+// completion times) -- are rebuilt from the rings in bulk: every lane walks
+// its instances' records with the pipelined four-step loop, all lanes at
+// once, when a ring is half full and at the end of the trace.  The rounding
+// order is the reference's throughout.
 //
-// Used for continuous mode, one deployment of <= 32 instances, no order keys
-// (launch_replay picks it; HS_REPLAY_LEGACY=1 forces replay.cu's kernel).
+// Layout: a warp holds 32 / L traces, L lanes per trace, each lane owning
+// instances j = lane + L * k (k < K): per arrival the lanes test event
+// bounds, process their due events and take part in the dispatch reductions
+// (log2 L shuffle levels inside the trace's lane group).
+//
+// Used for continuous mode, one deployment of <= 32 instances, non-negative
+// latency coefficients, no order keys (launch_replay picks it;
+// HS_REPLAY_LEGACY=1 forces replay.cu's kernel).
 #include <cstdlib>
 
 #include "hs_device.cuh"
@@ -29,11 +46,11 @@
 namespace hs {
 namespace {
 
-constexpr int kL = 8;   // lanes per trace
-constexpr int kG = 4;   // traces per warp
-constexpr int kWPB = 2;  // warps per block
-constexpr int kHS2 = 4;  // heap entries per instance in shared memory
+constexpr int kWPB = 2;    // warps per block
+constexpr int kHS2 = 4;    // heap entries per instance in shared memory
+constexpr int kRing = 16;  // segment records per instance
 constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t NONE = 0xffffffffu;
 
 struct HEnt {
   uint64_t key;
@@ -46,13 +63,32 @@ struct QRec {  // replay.cu QRec (kQRecBytes)
 static_assert(sizeof(QRec) == kQRecBytes, "QRec layout");
 static_assert(sizeof(HEnt) == kHEntBytes, "HEnt layout");
 
-// Per-instance state in shared memory; the stepping state is in registers (Hot).
+// One event step of an instance: the exact clock chain is rebuilt from these.
+enum : uint32_t { R_RESTART = 1, R_IDLE = 2 };
+struct SegRec {
+  uint32_t k;         // event step index
+  int32_t first_ret;  // requests retiring at this step (linked through QRec.next when departures are wanted), -1 none
+  uint32_t nact;      // batch size of the pure steps that follow (A = p5 * nact, B = p6 * nact)
+  uint32_t flags;     // R_RESTART: the step starts a busy period at time t0; R_IDLE: last step of one
+  double c_e;         // cost of this step: (0.0 + prefill) + decode
+  double cd1;         // cached length of step k + 1
+  double t0;          // R_RESTART: exact time of this step (the dispatch time)
+};
+static_assert(kRing * sizeof(SegRec) % sizeof(HEnt) == 0, "the rings live in the heap buffer");
+constexpr int kRingEntries = (int)(kRing * sizeof(SegRec) / sizeof(HEnt));  // heap-buffer entries per instance
+
+// Per-instance state in shared memory.
 struct IState {
-  double hW, topW, completion, ex, wcur;
+  double hW, topW, completion, ex, wcur, at;
   int64_t run_tot, reserved, cur_max, max_res, tok_count;
   uint64_t topkey;
   int32_t qhead, qtail, hI, hO, hP, hnext, hnI, hnO;
   int32_t nact, topI, topO, topP, req_count, cnt_max;
+  uint32_t ak;     // anchor: T(ak) = at exactly, step ak's cost not yet added
+  uint32_t ri;     // ring index of the record whose segment holds the anchor
+  uint32_t rw;     // records written
+  uint32_t kidle;  // step index the instance went idle at (its next busy period restarts there)
+  uint32_t adone;  // the anchor sits on ring[ri].k with that record's outputs written
 };
 
 struct TypeRec {  // one instance class
@@ -62,10 +98,18 @@ struct TypeRec {  // one instance class
 };
 
 // Hot per-instance registers.
-enum : uint32_t { F_VALID = 1, F_SCHED = 2, F_BLOCKED = 4, F_DIRTY = 8, F_EXOVER = 16, F_MAXDIRTY = 32, F_ERR = 64 };
+enum : uint32_t {
+  F_VALID = 1, F_DIRTY = 2, F_EXOVER = 4, F_MAXDIRTY = 8, F_ERR = 16, F_RESTART = 32
+};
 struct Hot {
-  double t_next, cd, A, B, load;
-  uint32_t k, kr, fl;
+  double load;
+  double Elo, Ehi;  // bounds of T(kn)
+  double slo, shi;  // bounds of T(sk)
+  double sce;       // cost of step sk
+  double sA, sB;    // p5 * nact, p6 * nact of the segment's pure steps
+  double scd;       // cached length of step sk + 1
+  uint32_t sk, kn;  // segment start (an event step) and the next event step (NONE: idle)
+  uint32_t fl;
 };
 
 __device__ __forceinline__ uint64_t okey(double x) {
@@ -80,19 +124,20 @@ __device__ __forceinline__ double from_okey(uint64_t k) {
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   return (uint64_t)__shfl_xor_sync(FULL, (long long)v, m);
 }
-// group (8-lane) reductions; every lane of the warp takes part
+// lane-group reductions (xor offsets below L stay inside the group); every lane takes part
+template <int L>
 __device__ __forceinline__ uint64_t group_max_u64(uint64_t v) {
 #pragma unroll
-  for (int m = 4; m > 0; m >>= 1) {
+  for (int m = L / 2; m > 0; m >>= 1) {
     const uint64_t o = shfl_xor_u64(v, m);
     v = o > v ? o : v;
   }
   return v;
 }
-// min of (key, idx) pairs, ties on the lowest idx
-__device__ __forceinline__ void group_min_key_idx(uint64_t& key, int& idx) {
+template <int L>
+__device__ __forceinline__ void group_min_key_idx(uint64_t& key, int& idx) {  // ties: lowest idx
 #pragma unroll
-  for (int m = 4; m > 0; m >>= 1) {
+  for (int m = L / 2; m > 0; m >>= 1) {
     const uint64_t ok = shfl_xor_u64(key, m);
     const int oi = __shfl_xor_sync(FULL, idx, m);
     if (ok < key || (ok == key && oi < idx)) {
@@ -101,9 +146,10 @@ __device__ __forceinline__ void group_min_key_idx(uint64_t& key, int& idx) {
     }
   }
 }
-__device__ __forceinline__ void group_max_key_idx(uint64_t& key, int& idx) {
+template <int L>
+__device__ __forceinline__ void group_max_key_idx(uint64_t& key, int& idx) {  // ties: lowest idx
 #pragma unroll
-  for (int m = 4; m > 0; m >>= 1) {
+  for (int m = L / 2; m > 0; m >>= 1) {
     const uint64_t ok = shfl_xor_u64(key, m);
     const int oi = __shfl_xor_sync(FULL, idx, m);
     if (ok > key || (ok == key && oi < idx)) {
@@ -204,23 +250,165 @@ struct Ctx {
   QRec* R;
   double* DEP;
   int64_t pt;
+  double wscale;  // diagnostic: widens the bounds (HS_REPLAY_WIDEN) to exercise the exact paths
 };
 
-// A full STEP event of one instance (simulator.py:330-355): retirements due
-// at this step (in admission order), FCFS admission, prefill for newcomers,
-// one decode iteration.  Returns false on a trace error (recorded in le).
-__device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, const TypeRec& tr, const Ctx& c,
-                                           int32_t cap, int j, uint32_t& n_steps, LaneErr& le) {
-  const double t = h.t_next;
-  h.fl &= ~F_SCHED;
-  ++n_steps;
+// ---------------------------------------------------------------- bounds
+// Bounds of T(sk + 1 + n): T(sk) in [slo, shi], then sce, then n pure steps
+// priced at cached lengths scd, scd + 1, ...  All terms are >= 0.
+__device__ __forceinline__ void seg_bounds(const Hot& h, double p7, double p8, double wscale, uint32_t n, double& L,
+                                           double& U) {
+  const double dn = (double)n;
+  const double tri_lo = __dmul_rd(__dmul_rd(dn, __dsub_rd(dn, 1.0)), 0.5);
+  const double tri_hi = __dmul_ru(__dmul_ru(dn, __dsub_ru(dn, 1.0)), 0.5);
+  const double sx_lo = __dadd_rd(__dmul_rd(dn, h.scd), tri_lo);
+  const double sx_hi = __dadd_ru(__dmul_ru(dn, h.scd), tri_hi);
+  const double S_lo = __dadd_rd(__dmul_rd(__dadd_rd(h.sA, p7), sx_lo), __dmul_rd(dn, __dadd_rd(h.sB, p8)));
+  const double S_hi = __dadd_ru(__dmul_ru(__dadd_ru(h.sA, p7), sx_hi), __dmul_ru(dn, __dadd_ru(h.sB, p8)));
+  // each price within a factor (1 -+ u)^4 of its affine value; n + 1 chain additions
+  const double m = __dmul_ru(dn + 2.0, 0x1p-53 * wscale);
+  L = __dmul_rd(__dadd_rd(__dadd_rd(h.slo, h.sce), __dmul_rd(S_lo, 1.0 - 0x1p-50 * wscale)), __dsub_rd(1.0, m));
+  U = __dmul_ru(__dadd_ru(__dadd_ru(h.shi, h.sce), __dmul_ru(S_hi, 1.0 + 0x1p-49 * wscale)),
+                __dadd_ru(1.0, __dmul_ru(2.0, m)));
+}
+
+// ------------------------------------------------------- exact clock chain
+// Walk one instance's exact clock chain forward from its anchor through its
+// ring's segment records (the reference's rounding order: t = t + cost, step
+// by step), writing departure / completion times at retiring steps.
+//   TO_STEP: stop at step kt;  TO_TIME: stop at the first step after sk whose
+//   time is >= t_target;  ALL: stop at the last record's event step.
+enum CatchMode { TO_STEP = 0, TO_TIME = 1, ALL = 2 };
+__device__ __noinline__ void catch_up(IState& S, uint32_t sk, const SegRec* ring, const TypeRec& tr, const Ctx& c,
+                                      int mode, uint32_t kt, double t_target, uint32_t* k_out, double* t_out) {
+  const double p5 = tr.p[4], p6 = tr.p[5], p7 = tr.p[6], p8 = tr.p[7];
+  uint32_t r = S.ri;
+  uint32_t k = S.ak;
+  double t = S.at;
+  bool at_event_done = S.adone != 0;  // anchor on ring[r].k, its outputs written
+  const uint32_t rw = S.rw;
+  const bool by_time = mode == TO_TIME;
+  for (;;) {
+    const SegRec rec = ring[r % kRing];
+    if (k == rec.k) {
+      if (!at_event_done) {
+        if (rec.flags & R_RESTART) t = rec.t0;
+        if (rec.first_ret >= 0) {
+          S.completion = t;
+          if (c.DEP)
+            for (int32_t x = rec.first_ret; x >= 0; x = c.R[x].next) c.DEP[x] = t;
+        }
+        at_event_done = true;
+      }
+      if (mode == TO_STEP && k == kt) break;
+      if (mode == ALL && r + 1 == rw) break;
+      if (rec.flags & R_IDLE) {  // no step follows: the next record restarts at the same index
+        if (r + 1 == rw) break;
+        ++r;
+        at_event_done = false;
+        continue;
+      }
+      if (by_time && t >= t_target && k > sk) break;
+      t = __dadd_rn(t, rec.c_e);
+      k += 1;
+      at_event_done = false;
+    }
+    // pure steps of this segment, up to the next record's event step
+    const uint32_t kend = (r + 1 < rw) ? ring[(r + 1) % kRing].k : NONE;
+    uint32_t stop = kend;
+    if (mode == TO_STEP && kt < stop) stop = kt;
+    if (k < stop && !(by_time && t >= t_target && k > sk)) {
+      const double dnact = (double)rec.nact;
+      const double A = __dmul_rn(p5, dnact), B = __dmul_rn(p6, dnact);
+      auto price = [&](double x) {
+        return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, x), B), __dmul_rn(p7, x)), p8);
+      };
+      double cd = __dadd_rn(rec.cd1, (double)(k - rec.k - 1));
+      double c0 = price(cd), c1 = price(__dadd_rn(cd, 1.0)), c2 = price(__dadd_rn(cd, 2.0)),
+             c3 = price(__dadd_rn(cd, 3.0));
+      for (;;) {
+        // step k (time t) costs c0: step k + 1 is at t1, ...
+        const double t1 = __dadd_rn(t, c0);
+        const double t2 = __dadd_rn(t1, c1);
+        const double t3 = __dadd_rn(t2, c2);
+        const double t4 = __dadd_rn(t3, c3);
+        const double cd4 = __dadd_rn(cd, 4.0);
+        const double n0 = price(cd4), n1 = price(__dadd_rn(cd, 5.0)), n2 = price(__dadd_rn(cd, 6.0)),
+                     n3 = price(__dadd_rn(cd, 7.0));
+        // step k + i is reached while k + i <= stop and, by time, the chain
+        // stops at the first step whose time reaches the target
+        const bool g1 = k + 1 <= stop && !(by_time && t1 >= t_target);
+        const bool g2 = g1 && k + 2 <= stop && !(by_time && t2 >= t_target);
+        const bool g3 = g2 && k + 3 <= stop && !(by_time && t3 >= t_target);
+        const bool g4 = g3 && k + 4 <= stop && !(by_time && t4 >= t_target);
+        if (!g4 || k + 4 == stop) {
+          uint32_t n;
+          double tn;
+          if (g4) {
+            n = 4;
+            tn = t4;
+          } else if (!g1) {  // k + 1 > stop is excluded above: step k + 1 reaches the target
+            n = 1;
+            tn = t1;
+          } else if (!g2) {
+            n = (k + 2 > stop) ? 1 : 2;
+            tn = (k + 2 > stop) ? t1 : t2;
+          } else if (!g3) {
+            n = (k + 3 > stop) ? 2 : 3;
+            tn = (k + 3 > stop) ? t2 : t3;
+          } else {
+            n = (k + 4 > stop) ? 3 : 4;
+            tn = (k + 4 > stop) ? t3 : t4;
+          }
+          k += n;
+          t = tn;
+          break;
+        }
+        t = t4;
+        cd = cd4;
+        k += 4;
+        c0 = n0;
+        c1 = n1;
+        c2 = n2;
+        c3 = n3;
+      }
+    }
+    if (mode == TO_STEP && k == kt) break;
+    if (by_time && t >= t_target && k > sk) break;
+    if (k == kend) {  // the next record's event step
+      ++r;
+      at_event_done = false;
+      continue;
+    }
+    break;
+  }
+  S.ri = r;
+  S.ak = k;
+  S.at = t;
+  S.adone = (k == ring[r % kRing].k && at_event_done) ? 1u : 0u;
+  if (k_out) *k_out = k;
+  if (t_out) *t_out = t;
+}
+
+// ----------------------------------------------------------------- events
+// The STEP event of one instance at step h.kn (simulator.py:330-355):
+// retirements due at this step (admission order), FCFS admission, prefill
+// for newcomers, one decode iteration -- as replay.cu's event_step, with the
+// step's time known within [Elo, Ehi]; appends the step's segment record.
+__device__ __forceinline__ void event(Hot& h, IState& S, const Heap& heap, SegRec* ring, const TypeRec& tr,
+                                      const Ctx& c, int32_t cap, int j, uint32_t& n_steps, LaneErr& le) {
+  const uint32_t ke = h.kn;
+  const bool restart = (h.fl & F_RESTART) != 0;
+  n_steps += restart ? 1u : ke - h.sk;
+  if (S.rw - S.ri >= (uint32_t)kRing)  // ring full (rare: the arrival loop drains the rings early)
+    catch_up(S, h.sk, ring, tr, c, ALL, 0, 0.0, nullptr, nullptr);
   int32_t nact = S.nact;
   uint64_t topkey = S.topkey;
   int64_t reserved = S.reserved, run_tot = S.run_tot, cur_max = S.cur_max;
   int32_t cnt_max = S.cnt_max;
   bool max_dirty = (h.fl & F_MAXDIRTY) != 0;
-  bool retired = false;
-  while (nact > 0 && (uint32_t)(topkey >> 32) == h.k) {
+  int32_t first_ret = -1;
+  while (nact > 0 && (uint32_t)(topkey >> 32) == ke) {
     // retire in (departure step, admission order); payload was prefetched
     const int32_t r = (int32_t)(topkey & 0xffffffffu);
     const int64_t Ir = S.topI, Or = S.topO, Pr = S.topP;
@@ -235,17 +423,14 @@ __device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, 
       S.topW = c.R[r2].W;
     }
     reserved -= Ir + Or;
-    retired = true;
-    if (c.DEP) c.DEP[r] = t;
+    if (c.DEP) c.R[r].next = first_ret;  // departure chain of this step (the queue link is dead)
+    first_ret = r;
     h.load = __dsub_rn(h.load, wr);  // Scheduler.complete: the recorded values
     run_tot -= Ir + Pr;
-    const int64_t ka = (int64_t)h.k - (Or > 1 ? Or : 1);
+    const int64_t ka = (int64_t)ke - (Or > 1 ? Or : 1);
     if (Ir - ka == cur_max && --cnt_max == 0) max_dirty = true;
   }
-  if (retired) {
-    S.completion = t;
-    h.fl |= F_DIRTY;
-  }
+  if (first_ret >= 0) h.fl |= F_DIRTY;
   if (nact == 0) {
     cur_max = INT64_MIN;
     cnt_max = 0;
@@ -254,22 +439,20 @@ __device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, 
   // admit FCFS (simulator.py:297-316)
   int64_t newly = 0, max_i_new = 0;
   int32_t qhead = S.qhead;
-  bool fail = false;
+  int32_t fail = 0, fail_req = -1;
   while (qhead >= 0) {
     const int64_t need = (int64_t)S.hI + S.hO;
     // simulator.py:303 per_token * (reserved + need) > budget, exactly
     if (reserved + need > tr.cap_tok) {
       if (nact == 0 && newly == 0) {
-        if (t < le.t || (t == le.t && j < le.inst)) le = LaneErr{t, HS_TRACE_INFEASIBLE_REQUEST, j, qhead};
-        h.fl |= F_ERR;
-        fail = true;
+        fail = HS_TRACE_INFEASIBLE_REQUEST;
+        fail_req = qhead;
       }
       break;
     }
-    if (nact >= cap || h.k > 0x7fffffffu) {
-      if (t < le.t || (t == le.t && j < le.inst)) le = LaneErr{t, HS_TRACE_CAPACITY, j, qhead};
-      h.fl |= F_ERR;
-      fail = true;
+    if (nact >= cap || ke > 0x7fffffffu) {
+      fail = HS_TRACE_CAPACITY;
+      fail_req = qhead;
       break;
     }
     const int32_t r = qhead;
@@ -291,7 +474,7 @@ __device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, 
     reserved += need;
     if (Ir > max_i_new) max_i_new = Ir;
     ++newly;
-    const uint64_t key = ((uint64_t)(h.k + (uint32_t)(Or > 1 ? Or : 1)) << 32) | (uint32_t)r;
+    const uint64_t key = ((uint64_t)(ke + (uint32_t)(Or > 1 ? Or : 1)) << 32) | (uint32_t)r;
     if (nact == 0 || key < topkey) {
       topkey = key;
       S.topI = (int32_t)Ir;
@@ -299,7 +482,7 @@ __device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, 
       S.topP = (int32_t)Pr;
       S.topW = wr;
     }
-    const int64_t mk = Ir - (int64_t)h.k;
+    const int64_t mk = Ir - (int64_t)ke;
     heap.push(nact, HEnt{key, mk});
     if (mk > cur_max) {
       cur_max = mk;
@@ -310,17 +493,22 @@ __device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, 
     }
   }
   S.qhead = qhead;
-  h.fl |= F_BLOCKED;  // queue empty or its head does not fit
   // simulator.py:315: the max of the quotients is the quotient of the max reservation
   if (newly && reserved > S.max_res) S.max_res = reserved;
+  SegRec rec;
+  rec.k = ke;
+  rec.first_ret = first_ret;
+  rec.flags = restart ? R_RESTART : 0u;
+  rec.t0 = restart ? h.Elo : 0.0;
+  h.fl &= ~F_RESTART;
   if (!fail && nact > 0) {
     double cst = 0.0;
     if (newly) cst = __dadd_rn(cst, prefill_time(tr.p, newly, max_i_new));
     if (max_dirty || cnt_max <= 0) {  // the last holder of the max retired: rescan
       int64_t m = INT64_MIN;
       int32_t cm = 0;
-      for (int32_t q = 0; q < nact; ++q) {
-        const int64_t mk = heap.get(q, nact).mk;
+      for (int32_t x = 0; x < nact; ++x) {
+        const int64_t mk = heap.get(x, nact).mk;
         if (mk > m) {
           m = mk;
           cm = 1;
@@ -333,21 +521,35 @@ __device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, 
       max_dirty = false;
     }
     const double db = i2d(nact);
-    h.A = __dmul_rn(tr.p[4], db);
-    h.B = __dmul_rn(tr.p[5], db);
-    h.cd = i2d(cur_max + (int64_t)h.k + 1);
+    const double A = __dmul_rn(tr.p[4], db), B = __dmul_rn(tr.p[5], db);
+    const double cd = i2d(cur_max + (int64_t)ke + 1);
     // decode_iteration_time(cached, batch) = ((A*c + B) + p7*c) + p8
-    const double dec =
-        __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(h.A, h.cd), h.B), __dmul_rn(tr.p[6], h.cd)), tr.p[7]);
+    const double dec = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, cd), B), __dmul_rn(tr.p[6], cd)), tr.p[7]);
     cst = __dadd_rn(cst, dec);
-    h.k += 1;
-    h.cd = __dadd_rn(h.cd, 1.0);
-    h.kr = (uint32_t)(topkey >> 32);
-    h.t_next = __dadd_rn(t, cst);
-    h.fl |= F_SCHED;
+    rec.nact = (uint32_t)nact;
+    rec.c_e = cst;
+    rec.cd1 = __dadd_rn(cd, 1.0);
+    // the new segment starts at ke; the next event is the heap minimum's step
+    h.slo = h.Elo;
+    h.shi = h.Ehi;
+    h.sce = cst;
+    h.sA = A;
+    h.sB = B;
+    h.scd = rec.cd1;
+    h.sk = ke;
+    h.kn = (uint32_t)(topkey >> 32);
+    seg_bounds(h, tr.p[6], tr.p[7], c.wscale, h.kn - ke - 1, h.Elo, h.Ehi);
   } else {
-    h.kr = 0xffffffffu;  // idle until the next dispatch (simulator.py:344-345)
+    rec.nact = 0;
+    rec.c_e = 0.0;
+    rec.cd1 = 0.0;
+    rec.flags |= R_IDLE;
+    h.sk = ke;
+    h.kn = NONE;  // idle until the next dispatch (simulator.py:344-345)
+    S.kidle = ke;
   }
+  ring[S.rw % kRing] = rec;
+  S.rw += 1;
   if (max_dirty) h.fl |= F_MAXDIRTY;
   else h.fl &= ~F_MAXDIRTY;
   S.nact = nact;
@@ -356,66 +558,85 @@ __device__ __forceinline__ void event_step(Hot& h, IState& S, const Heap& heap, 
   S.run_tot = run_tot;
   S.cur_max = cur_max;
   S.cnt_max = cnt_max;
+  if (fail) {  // the failing step's exact time orders errors across instances
+    h.kn = NONE;
+    double tf;
+    catch_up(S, h.sk, ring, tr, c, TO_STEP, ke, 0.0, nullptr, &tf);
+    if (tf < le.t || (tf == le.t && j < le.inst)) le = LaneErr{tf, fail, j, fail_req};
+    h.fl |= F_ERR;
+  }
 }
 
-// Advance one instance's steps with t_next < t_limit (strict: steps at an
-// arrival's own time run after it), or every step when draining.
-__device__ __forceinline__ void advance(Hot& h, IState& S, const Heap& heap, const TypeRec& tr, const Ctx& c,
-                                        int32_t cap, int j, double t_limit, bool drain, uint32_t& n_steps,
-                                        LaneErr& le) {
-  const double lim = t_limit;
-  const double p7 = tr.p[6], p8 = tr.p[7];
-  while ((h.fl & (F_VALID | F_SCHED | F_ERR)) == (F_VALID | F_SCHED) && (drain || h.t_next < lim)) {
-    if (!(h.fl & F_BLOCKED) || h.k >= h.kr) {
-      event_step(h, S, heap, tr, c, cap, j, n_steps, le);
+// Process every event of one instance before t_a (every event when
+// draining); returns true when the next one's order against t_a is
+// undecided by the bounds (the caller resolves it exactly).
+__device__ __forceinline__ bool events_before(Hot& h, IState& S, const Heap& heap, SegRec* ring, const TypeRec& tr,
+                                              const Ctx& c, int32_t cap, int j, double t_a, bool drain,
+                                              uint32_t& n_steps, LaneErr& le) {
+  while ((h.fl & (F_VALID | F_ERR)) == F_VALID && h.kn != NONE) {
+    if (drain || h.Ehi < t_a) {
+      event(h, S, heap, ring, tr, c, cap, j, n_steps, le);
       continue;
     }
-    // pure steps: decode price and clock only, blocks of four, the next
-    // block's prices computed while this block's clock additions (the only
-    // serial part, in the reference's rounding order) run
-    const uint32_t k0 = h.k;
-    const double A = h.A, B = h.B;
-    auto price = [&](double x) {
-      return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, x), B), __dmul_rn(p7, x)), p8);
-    };
-    double cd = h.cd, tn = h.t_next;
-    uint32_t k = h.k;
-    const uint32_t kr = h.kr;
-    double c0 = price(cd), c1 = price(__dadd_rn(cd, 1.0)), c2 = price(__dadd_rn(cd, 2.0)),
-           c3 = price(__dadd_rn(cd, 3.0));
-    for (;;) {
-      const double t1 = __dadd_rn(tn, c0);
-      const double t2 = __dadd_rn(t1, c1);
-      const double t3 = __dadd_rn(t2, c2);
-      const double t4 = __dadd_rn(t3, c3);
-      const double cd4 = __dadd_rn(cd, 4.0);
-      const double n0 = price(cd4), n1 = price(__dadd_rn(cd, 5.0)), n2 = price(__dadd_rn(cd, 6.0)),
-                   n3 = price(__dadd_rn(cd, 7.0));
-      // step i+1 runs iff step i ran, k+i < kr and t_i < lim
-      const bool g1 = k + 1 < kr && (drain || t1 < lim);
-      const bool g2 = g1 && k + 2 < kr && (drain || t2 < lim);
-      const bool g3 = g2 && k + 3 < kr && (drain || t3 < lim);
-      const bool g4 = g3 && k + 4 < kr && (drain || t4 < lim);
-      if (!g4) {
-        const uint32_t n = 1u + (uint32_t)g1 + (uint32_t)g2 + (uint32_t)g3;
-        tn = g3 ? t4 : (g2 ? t3 : (g1 ? t2 : t1));
-        cd = __dadd_rn(cd, (double)n);
-        k += n;
-        break;
-      }
-      tn = t4;
-      cd = cd4;
-      k += 4;
-      c0 = n0;
-      c1 = n1;
-      c2 = n2;
-      c3 = n3;
-    }
-    h.t_next = tn;
-    h.cd = cd;
-    h.k = k;
-    n_steps += k - k0;
+    return !(h.Elo >= t_a);
   }
+  return false;
+}
+
+// The exact time of the pending event decides its order against t_a.
+__device__ __forceinline__ void resolve_exact(Hot& h, IState& S, SegRec* ring, const TypeRec& tr, const Ctx& c) {
+  double t;
+  catch_up(S, h.sk, ring, tr, c, TO_STEP, h.kn, 0.0, nullptr, &t);
+  h.Elo = t;
+  h.Ehi = t;
+}
+
+// Dispatch to a busy instance whose queue was empty and whose new head fits:
+// it is admitted at the first step at or after t_a (arrivals pop before steps
+// at equal times), which becomes the next event when it precedes the pending
+// retirement.  T(sk) < t_a <= T(kn), so that step is sk + 1 + n, n <= nmax.
+__device__ __forceinline__ void admission_step(Hot& h, IState& S, SegRec* ring, const TypeRec& tr, const Ctx& c,
+                                               double t_a) {
+  const double p7 = tr.p[6], p8 = tr.p[7];
+  const uint32_t nmax = h.kn - h.sk - 1;
+  uint32_t lo = 0, hi = nmax;
+  while (lo < hi) {  // smallest n whose lower bound reaches t_a (nmax: known to)
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    double L, U;
+    seg_bounds(h, p7, p8, c.wscale, mid, L, U);
+    if (L >= t_a) hi = mid;
+    else lo = mid + 1;
+  }
+  bool ok = true;
+  double mlo = h.Elo, mhi = h.Ehi;
+  if (lo < nmax) {
+    seg_bounds(h, p7, p8, c.wscale, lo, mlo, mhi);
+    ok = mlo >= t_a;
+  }
+  if (ok && lo > 0) {
+    double L, U;
+    seg_bounds(h, p7, p8, c.wscale, lo - 1, L, U);
+    ok = U < t_a;
+  }
+  if (ok) {
+    if (lo == nmax) return;  // the pending event's step itself
+    h.kn = h.sk + 1 + lo;
+    h.Elo = mlo;
+    h.Ehi = mhi;
+    return;
+  }
+  // undecided by the bounds: walk the exact chain to the first step at/after t_a
+  uint32_t m;
+  double t;
+  catch_up(S, h.sk, ring, tr, c, TO_TIME, 0, t_a, &m, &t);
+  if (m >= h.kn) {  // the pending event's step (its exact time is now known)
+    h.Elo = t;
+    h.Ehi = t;
+    return;
+  }
+  h.kn = m;
+  h.Elo = t;
+  h.Ehi = t;
 }
 
 // shared memory per block: [IState kWPB*K*32][HEnt kWPB*K*32*kHS2][TypeRec n_types]
@@ -424,13 +645,14 @@ __host__ __device__ constexpr size_t mt_smem_fixed() {
   return sizeof(IState) * kWPB * K * 32 + sizeof(HEnt) * kWPB * K * 32 * kHS2;
 }
 
-template <int K>
-__global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
+template <int L, int K>
+__global__ void __launch_bounds__(kWPB * 32) k_replay_mt(
     int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI, const int32_t* __restrict__ gO,
     const int32_t* __restrict__ gP, const double* __restrict__ gT, uint8_t* __restrict__ assign,
     double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics, hs_trace_result* __restrict__ result,
     QRec* __restrict__ qrec_all, uint64_t* __restrict__ heap_all, const uint32_t* progress, int32_t phase_len,
-    const __grid_constant__ ReplayConst rc) {
+    double wscale, const __grid_constant__ ReplayConst rc) {
+  constexpr int G = 32 / L;  // traces per warp
   __shared__ uint64_t s_tab[256];
   extern __shared__ double4 s_dyn[];
   IState(*s_ist)[K][32] = reinterpret_cast<IState(*)[K][32]>(s_dyn);
@@ -450,11 +672,12 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
 
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int grp = lane >> 3;  // trace group within the warp
-  const int l = lane & 7;     // lane within the group
+  const int grp = lane / L;  // trace group within the warp
+  const int l = lane % L;    // lane within the group
+  const int gbase = grp * L;
   const int64_t warp_global = (int64_t)blockIdx.x * kWPB + wib;
-  const int64_t tr_raw = warp_global * kG + grp;
-  if (warp_global * kG >= n_traces) return;  // whole warp idle
+  const int64_t tr_raw = warp_global * G + grp;
+  if (warp_global * G >= n_traces) return;  // whole warp idle
   const bool tvalid = tr_raw < n_traces;
   const int64_t tr = tvalid ? tr_raw : n_traces - 1;
   const int N = rc.N;
@@ -466,11 +689,11 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
   // every group walks arrival indices in lockstep up to the warp's longest trace
   int64_t qmax = q;
 #pragma unroll
-  for (int m = 8; m < 32; m <<= 1) {
+  for (int m = L; m < 32; m <<= 1) {
     const int64_t oq = __shfl_xor_sync(FULL, (long long)qmax, m);
     qmax = oq > qmax ? oq : qmax;
   }
-  const Ctx c{gI + o, gO + o, qrec_all + o, depart ? depart + o : nullptr, pt};
+  const Ctx c{gI + o, gO + o, qrec_all + o, depart ? depart + o : nullptr, pt, wscale};
   const int32_t* P = gP + o;
   const double* T = gT ? gT + o : nullptr;
 
@@ -478,12 +701,15 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
   int ty[K];
   int32_t capk[K];
   Heap heap[K];
+  SegRec* ring[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const int j = l + kL * k;
+    const int j = l + L * k;
     const bool v = tvalid && j < N;
     ty[k] = v ? rc.inst_type[j] : 0;
-    h[k] = Hot{0.0, 0.0, 0.0, 0.0, 0.0, 0u, 0xffffffffu, v ? (F_VALID | F_DIRTY) : 0u};
+    h[k] = Hot{};
+    h[k].kn = NONE;
+    h[k].fl = v ? (F_VALID | F_DIRTY) : 0u;
     IState& S = s_ist[wib][k][lane];
     S = IState{};
     S.ex = 1.0;
@@ -491,9 +717,10 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
     S.qhead = -1;
     S.qtail = -1;
     const int jj = v ? j : 0;
-    heap[k] = Heap{s_heap[wib][k][lane],
-                   reinterpret_cast<HEnt*>(heap_all) + tr * rc.heap_stride + rc.heap_off[jj]};
+    HEnt* base = reinterpret_cast<HEnt*>(heap_all) + tr * rc.heap_stride;
+    heap[k] = Heap{s_heap[wib][k][lane], base + rc.heap_off[jj]};
     capk[k] = (int32_t)(rc.heap_off[jj + 1] - rc.heap_off[jj]) + kHS2;
+    ring[k] = reinterpret_cast<SegRec*>(base + rc.heap_off[N] + (int64_t)jj * kRingEntries);
   }
   __syncwarp();
   LaneErr le{INFINITY, HS_TRACE_OK, 0x7fffffff, -1};
@@ -504,38 +731,62 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
   int64_t t_err_req = -1;
   double t_err_val = 0.0;
   const bool eval_all = policy == HS_POLICY_OS || policy == HS_POLICY_MB;
+  const unsigned gmask = (L == 32 ? FULL : (((1u << L) - 1u) << gbase));
 
   // trace error from the lanes' step errors: earliest (time, instance) wins
-  auto step_error = [&]() -> bool {
-    const bool mine = (h[0].fl & F_ERR) || (K > 1 && (h[K > 1 ? 1 : 0].fl & F_ERR)) ||
-                      (K > 2 && (h[K > 2 ? 2 : 0].fl & F_ERR)) || (K > 3 && (h[K > 3 ? 3 : 0].fl & F_ERR));
-    const unsigned gb = __ballot_sync(FULL, mine && !failed) & (0xffu << (grp * 8));
-    if (!__any_sync(FULL, gb != 0)) return false;
+  auto step_error = [&]() {
+    bool mine = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) mine |= (h[k].fl & F_ERR) != 0;
+    if (!__any_sync(FULL, mine && !failed)) return;
     uint64_t key = mine ? okey(le.t) : ~0ull;
     int idx = mine ? le.inst : 0x7fffffff;
-    group_min_key_idx(key, idx);
-    const int src = __ffs(__ballot_sync(FULL, mine && le.inst == idx) & (0xffu << (grp * 8))) - 1;
-    const int code = __shfl_sync(FULL, le.code, src < 0 ? lane : src);
-    const int req = __shfl_sync(FULL, le.req, src < 0 ? lane : src);
-    if (gb && !failed) {
+    group_min_key_idx<L>(key, idx);
+    const unsigned sb = __ballot_sync(FULL, mine && le.inst == idx) & gmask;
+    const int src = sb ? __ffs(sb) - 1 : lane;
+    const int code = __shfl_sync(FULL, le.code, src);
+    const int req = __shfl_sync(FULL, le.req, src);
+    if ((__ballot_sync(FULL, mine) & gmask) && !failed) {
       failed = true;
       t_err = code;
       t_err_inst = idx;
       t_err_req = req;
       t_err_val = from_okey(key);
     }
-    return true;
+  };
+  // every lane brings its instances' exact chains up to their last records
+  auto drain_rings = [&]() {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      IState& S = s_ist[wib][k][lane];
+      if ((h[k].fl & F_VALID) && S.rw > 0) catch_up(S, h[k].sk, ring[k], s_types[ty[k]], c, ALL, 0, 0.0, nullptr, nullptr);
+    }
+  };
+  // all events before t_a (or all events), undecided ones resolved exactly
+  auto process_events = [&](double t_a, bool drain) {
+    for (;;) {
+      unsigned amb = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (events_before(h[k], s_ist[wib][k][lane], heap[k], ring[k], s_types[ty[k]], c, capk[k], l + L * k, t_a,
+                          drain, n_steps, le))
+          amb |= 1u << k;
+      if (!amb) break;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (amb >> k & 1u) resolve_exact(h[k], s_ist[wib][k][lane], ring[k], s_types[ty[k]], c);
+    }
   };
 
   uint64_t apack = 0;  // assignments of the current 8-arrival block (byte i = arrival base + i)
   int32_t bI = 0, bO = 0, bP = 0;
   double bT = 0.0;
   for (int64_t a = 0; a < qmax; ++a) {
-    const int slot = (int)(a & 7);
+    const int slot = (int)(a % L);
     if (slot == 0) {
       if (progress) {
         // streamed inputs (host path): phase p is resident once *progress > p
-        const int64_t last = (a + 7 < qmax ? a + 7 : qmax - 1);
+        const int64_t last = (a + L - 1 < qmax ? a + L - 1 : qmax - 1);
         const uint32_t need = (uint32_t)(last / phase_len);
         int stalled = 0;
         if (lane == 0) {
@@ -570,30 +821,33 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
         bT = T ? __ldcg(T + x) : 0.0;
       }
     }
-    const int src = (grp << 3) | slot;
+    {  // keep every ring below half full: the exact chains are rebuilt in bulk
+      bool full = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const IState& S = s_ist[wib][k][lane];
+        full |= S.rw - S.ri >= (uint32_t)(kRing / 2);
+      }
+      if (__any_sync(FULL, full)) drain_rings();
+    }
+    const int src = gbase | slot;
     const int64_t Ia = __shfl_sync(FULL, bI, src);
     const int64_t Oa = __shfl_sync(FULL, bO, src);
     const int64_t Pa = __shfl_sync(FULL, bP, src);
     const double ta = shfl_d(bT, src);
-    const bool act = !failed && a < q;
 
-    // ---- advance every instance to the arrival (strictly earlier steps)
-    if (act) {
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-        advance(h[k], s_ist[wib][k][lane], heap[k], s_types[ty[k]], c, capk[k], l + kL * k, ta, false, n_steps,
-                le);
-    }
+    // ---- every event before the arrival (steps strictly earlier)
+    if (!failed && a < q) process_events(ta, false);
     step_error();
     const bool live = !failed && a < q;
 
     // ---- per-class price of this arrival (scheduling.py:119-147): lane l
-    // prices class l (+8, +16, ...), the owners of each instance fetch theirs
+    // prices class l (+L, ...), the owners of each instance fetch theirs
     double cost[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) cost[k] = 1.0;
     if (policy != HS_POLICY_MB) {
-      for (int base = 0; base < NT; base += kL) {  // NT is launch-uniform
+      for (int base = 0; base < NT; base += L) {  // NT is launch-uniform
         double v = 0.0;
         const int cl = base + l;
         if (live && cl < NT) {
@@ -607,8 +861,8 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const int want = ty[k] - base;
-          const double got = shfl_d(v, (grp << 3) | (want >= 0 && want < kL ? want : 0));
-          if (want >= 0 && want < kL) cost[k] = got;
+          const double got = shfl_d(v, gbase | (want >= 0 && want < L ? want : 0));
+          if (want >= 0 && want < L) cost[k] = got;
         }
       }
     }
@@ -630,19 +884,19 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
       for (int k = 0; k < K; ++k) {
         if (live && (h[k].fl & F_VALID)) {
           IState& S = s_ist[wib][k][lane];
-          S.wcur = __dadd_rn(S.wcur, rc.wrr_weight[l + kL * k]);
+          S.wcur = __dadd_rn(S.wcur, rc.wrr_weight[l + L * k]);
           const uint64_t wk = okey(S.wcur);
           if (wk > key) {
             key = wk;
-            idx = l + kL * k;
+            idx = l + L * k;
           }
         }
       }
-      group_max_key_idx(key, idx);
+      group_max_key_idx<L>(key, idx);
       chosen = live ? idx : -1;
 #pragma unroll
       for (int k = 0; k < K; ++k)
-        if (live && l + kL * k == chosen) {
+        if (live && l + L * k == chosen) {
           IState& S = s_ist[wib][k][lane];
           S.wcur = __dsub_rn(S.wcur, rc.wrr_total);
         }
@@ -654,7 +908,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       w[k] = INFINITY;
-      const int j = l + kL * k;
+      const int j = l + L * k;
       const bool need = live && (h[k].fl & F_VALID) && (eval_all || j == chosen);
       if (need) {
         IState& S = s_ist[wib][k][lane];
@@ -683,10 +937,10 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
     {
       uint64_t ekey = (uint64_t)(uint32_t)err_j;
       int dummy = 0;
-      group_min_key_idx(ekey, dummy);
+      group_min_key_idx<L>(ekey, dummy);
       const int ej = (int)ekey;
       if (ej != 0x7fffffff) {
-        const int own = (grp << 3) | (ej & 7);
+        const int own = gbase | (ej % L);
         const int code = __shfl_sync(FULL, err_code, own);
         const double val = shfl_d(err_val, own);
         if (live) {
@@ -709,7 +963,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
           const uint64_t lk = okey(h[k].load);
           m1 = lk > m1 ? lk : m1;
         }
-      m1 = group_max_u64(m1);
+      m1 = group_max_u64<L>(m1);
       const double top = from_okey(m1);
       uint64_t pk = ~0ull;
       int pidx = 0x7fffffff;
@@ -721,10 +975,10 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
         const uint64_t key = cand ? okey(peak) : ~0ull;
         if (key < pk) {
           pk = key;
-          pidx = l + kL * k;
+          pidx = l + L * k;
         }
       }
-      group_min_key_idx(pk, pidx);
+      group_min_key_idx<L>(pk, pidx);
       if (go) {
         if (pk == ~0ull) {
           failed = true;
@@ -741,7 +995,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
     if (live && !failed) {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        if (l + kL * k != chosen) continue;
+        if (l + L * k != chosen) continue;
         IState& S = s_ist[wib][k][lane];
         Hot& hk = h[k];
         hk.load = __dadd_rn(hk.load, w[k]);
@@ -753,13 +1007,13 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
         S.tok_count += Ia + Oa;
         c.R[a].P = (int32_t)Pa;
         c.R[a].W = w[k];
-        if (S.qhead < 0) {
+        const bool was_empty = S.qhead < 0;
+        if (was_empty) {
           S.qhead = (int32_t)a;
           S.hI = (int32_t)Ia;
           S.hO = (int32_t)Oa;
           S.hP = (int32_t)Pa;
           S.hW = w[k];
-          hk.fl &= ~F_BLOCKED;  // a new queue head may be admitted at the next step
         } else if (S.qtail == S.qhead) {  // the head's prefetched record gains its successor
           S.hnext = (int32_t)a;
           S.hnI = (int32_t)Ia;
@@ -772,38 +1026,42 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
           tq.nO = (int32_t)Oa;
         }
         S.qtail = (int32_t)a;
-        if (!(hk.fl & F_SCHED)) {
-          hk.fl = (hk.fl | F_SCHED) & ~F_BLOCKED;
-          hk.t_next = ta;
+        if (hk.kn == NONE) {
+          // idle: a busy period starts with a step at exactly t_a
+          // (schedule_step(idx, t), simulator.py:292-295)
+          hk.kn = S.kidle;
+          hk.Elo = ta;
+          hk.Ehi = ta;
+          hk.fl |= F_RESTART;
+        } else if (was_empty && S.reserved + Ia + Oa <= s_types[ty[k]].cap_tok) {
+          // a head that does not fit waits for a retirement: no new event
+          admission_step(hk, S, ring[k], s_types[ty[k]], c, ta);
         }
       }
-      apack |= (uint64_t)(uint8_t)chosen << (8 * slot);
+      apack |= (uint64_t)(uint8_t)chosen << (8 * (a & 7));
     }
     // assignments leave in 8-byte words (one store per group per 8 arrivals)
-    if (assign && l == 0 && (slot == 7 || a + 1 == q) && a < q) {
-      const int64_t base = a - slot;
+    if (assign && l == 0 && ((a & 7) == 7 || a + 1 == q) && a < q) {
+      const int64_t base = a - (a & 7);
       uint8_t* dst = assign + o + base;
-      const int nb = slot + 1;
-      if (nb == 8 && ((uintptr_t)dst & 7) == 0 && !failed) {
+      const int nb = (int)(a & 7) + 1;
+      if (nb == 8 && ((uintptr_t)dst & 7) == 0) {
         *reinterpret_cast<uint64_t*>(dst) = apack;
       } else {
         for (int b = 0; b < nb; ++b) dst[b] = (uint8_t)(apack >> (8 * b));
       }
     }
-    if (slot == 7) apack = 0;
+    if ((a & 7) == 7) apack = 0;
   }
-  // drain: every remaining step
-  if (!failed) {
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      advance(h[k], s_ist[wib][k][lane], heap[k], s_types[ty[k]], c, capk[k], l + kL * k, 0.0, true, n_steps, le);
-  }
+  // drain: every remaining event, then every exact chain
+  if (!failed) process_events(0.0, true);
   step_error();
+  drain_rings();
 
   if (tvalid) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int j = l + kL * k;
+      const int j = l + L * k;
       if (!(h[k].fl & F_VALID)) continue;
       const IState& S = s_ist[wib][k][lane];
       hs_inst_metrics m;
@@ -817,7 +1075,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
   }
   int64_t steps_all = n_steps;
 #pragma unroll
-  for (int m = 4; m > 0; m >>= 1) steps_all += __shfl_xor_sync(FULL, steps_all, m);
+  for (int m = L / 2; m > 0; m >>= 1) steps_all += __shfl_xor_sync(FULL, steps_all, m);
   if (tvalid && l == 0) {
     hs_trace_result r;
     r.error = failed ? t_err : HS_TRACE_OK;
@@ -829,31 +1087,48 @@ __global__ void __launch_bounds__(kWPB * 32, 4) k_replay_mt(
   }
 }
 
-template <int K>
+template <int L, int K>
 cudaError_t launch_k(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                      const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign, double* d_depart,
                      hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec, uint64_t* d_heap,
-                     cudaStream_t st, const uint32_t* d_progress, int phase_len) {
+                     cudaStream_t st, const uint32_t* d_progress, int phase_len, double wscale) {
   const size_t smem = mt_smem_fixed<K>() + (size_t)rc.n_types * sizeof(TypeRec);
-  cudaError_t e = cudaFuncSetAttribute(k_replay_mt<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_replay_mt<L, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t per_block = (int64_t)kWPB * kG;
+  const int64_t per_block = (int64_t)kWPB * (32 / L);
   const unsigned blocks = (unsigned)((n_traces + per_block - 1) / per_block);
-  k_replay_mt<K><<<blocks, kWPB * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
-                                                  d_result, static_cast<QRec*>(d_qrec), d_heap, d_progress,
-                                                  phase_len, rc);
+  k_replay_mt<L, K><<<blocks, kWPB * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart,
+                                                     d_metrics, d_result, static_cast<QRec*>(d_qrec), d_heap,
+                                                     d_progress, phase_len, wscale, rc);
   return cudaGetLastError();
+}
+
+int lanes_per_trace() {
+  static const int v = [] {
+    const char* e = std::getenv("HS_REPLAY_LANES");
+    const int x = e ? std::atoi(e) : 16;
+    return (x == 8 || x == 16 || x == 32) ? x : 16;
+  }();
+  return v;
 }
 
 }  // namespace
 
 bool replay_mt_eligible(const ReplayConst& rc, bool multi) {
   static const bool legacy = std::getenv("HS_REPLAY_LEGACY") != nullptr;
-  return !legacy && !multi && rc.mode == 0 && rc.flags == 0 && rc.N >= 1 && rc.N <= kG * kL;
+  if (legacy || multi || rc.mode != 0 || rc.flags != 0 || rc.N < 1 || rc.N > 32) return false;
+  for (int t = 0; t < rc.n_types; ++t)  // the interval bounds need non-negative prices
+    for (int f = 0; f < 8; ++f)
+      if (!(rc.type_p[t][f] >= 0.0)) return false;
+  return true;
 }
 
 int replay_shared_heap(const ReplayConst& rc, bool multi) {
   return replay_mt_eligible(rc, multi) ? kHS2 : kHeapShared;
+}
+
+int64_t replay_extra_heap_entries(const ReplayConst& rc, bool multi) {
+  return replay_mt_eligible(rc, multi) ? (int64_t)rc.N * kRingEntries : 0;
 }
 
 cudaError_t launch_replay_mt(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
@@ -861,18 +1136,33 @@ cudaError_t launch_replay_mt(const ReplayConst& rc, int64_t n_traces, const int6
                              double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec,
                              uint64_t* d_heap, cudaStream_t st, const uint32_t* d_progress, int phase_len) {
   if (n_traces <= 0) return cudaSuccess;
-  const int K = (rc.N + kL - 1) / kL;
-#define HS_LK(k) \
-  launch_k<k>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result, d_qrec, d_heap, st, \
-              d_progress, phase_len)
-  switch (K) {
-    case 1: return HS_LK(1);
-    case 2: return HS_LK(2);
-    case 3: return HS_LK(3);
-    case 4: return HS_LK(4);
-    default: return cudaErrorInvalidValue;
+  static const double wscale = [] {
+    const char* e = std::getenv("HS_REPLAY_WIDEN");  // diagnostic only
+    const double x = e ? std::atof(e) : 1.0;
+    return x >= 1.0 ? x : 1.0;
+  }();
+  const int L = lanes_per_trace();
+  const int K = (rc.N + L - 1) / L;
+#define HS_LK(l, k)                                                                                              \
+  launch_k<l, k>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result, d_qrec, d_heap, \
+                 st, d_progress, phase_len, wscale)
+  if (L == 8) {
+    switch (K) {
+      case 1: return HS_LK(8, 1);
+      case 2: return HS_LK(8, 2);
+      case 3: return HS_LK(8, 3);
+      case 4: return HS_LK(8, 4);
+    }
+  } else if (L == 16) {
+    switch (K) {
+      case 1: return HS_LK(16, 1);
+      case 2: return HS_LK(16, 2);
+    }
+  } else {
+    return HS_LK(32, 1);
   }
 #undef HS_LK
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace hs
