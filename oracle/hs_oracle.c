@@ -16,7 +16,7 @@
 #include <string.h>
 #include <pthread.h>
 
-#include "exp_table_oracle.h"
+#include "../include/hs_exp_table.h"
 
 typedef __int128 i128;
 
@@ -82,8 +82,8 @@ double hs_oracle_exp(double x, int* overflow) {
   r = fma(kd, ORC_NEGLN2LON, r);
   uint64_t idx = 2 * (ki % 128);
   uint64_t top = ki << 45;
-  double tail = u2d(ORC_EXP_TAB[idx]);
-  uint64_t sbits = ORC_EXP_TAB[idx + 1] + top;
+  double tail = u2d(kExpTab[idx]);
+  uint64_t sbits = kExpTab[idx + 1] + top;
   double a = fma(r, ORC_C3, ORC_C2);
   double t1 = r + tail;
   double r2 = r * r;

@@ -18,7 +18,7 @@
  * numpy pieces restated (numpy/random/src/...):
  *   pcg64/pcg64.h            XSL-RR 128/64 step + output, next32 buffering
  *   distributions.c          random_standard_normal / _exponential (256-layer
- *                            ziggurat, tables in ziggurat_tables_oracle.h),
+ *                            ziggurat, tables in include/hs_ziggurat_tables.h),
  *                            random_normal, random_lognormal, random_exponential,
  *                            random_bounded_uint64_fill (Lemire, next32 path
  *                            for ranges below 2^32)
@@ -34,7 +34,7 @@
 #include <string.h>
 
 #include "hs_oracle.h"
-#include "ziggurat_tables_oracle.h"
+#include "../include/hs_ziggurat_tables.h"
 
 typedef unsigned __int128 u128;
 

@@ -34,7 +34,7 @@ def nvcc() -> str:
 def build(verbose: bool = False, force: bool = False, timers: bool = False) -> pathlib.Path:
     lib = PKG / "libhetserve_b200_timers.so" if timers else LIB
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
-    deps.append(PKG.parent / "include" / "hetserve_b200.h")
+    deps += list((PKG.parent / "include").glob("*.h"))
     if not force and lib.exists() and all(lib.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return lib
     flags = [*ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",

@@ -9,7 +9,8 @@
 #pragma once
 #include <stdint.h>
 
-#include "exp_table.cuh"
+#define HS_TABLE __device__ const
+#include "../../include/hs_exp_table.h"
 
 namespace hs {
 

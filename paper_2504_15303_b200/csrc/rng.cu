@@ -15,7 +15,7 @@
 // fp64 chain kept in lane 0 over a per-warp shared staging row.
 #include "hs_device.cuh"
 #include "hs_internal.h"
-#include "ziggurat_tables.cuh"
+#include "../../include/hs_ziggurat_tables.h"
 
 namespace hs {
 namespace {
