@@ -89,6 +89,8 @@ struct IState {
   uint32_t rw;     // records written
   uint32_t kidle;  // step index the instance went idle at (its next busy period restarts there)
   uint32_t adone;  // the anchor sits on ring[ri].k with that record's outputs written
+  int32_t ty;      // instance class
+  int32_t _pad;
 };
 
 struct TypeRec {  // one instance class
@@ -390,6 +392,117 @@ __device__ __noinline__ void catch_up(IState& S, uint32_t sk, const SegRec* ring
   if (t_out) *t_out = t;
 }
 
+// Every lane brings its instances' exact chains up to their last records in
+// ONE flattened loop: each iteration is a block of up to four pure steps or
+// one record boundary of the lane's current instance, so the warp pays for
+// the longest lane's total, not for the longest segment of every record in
+// turn; the next record is loaded while the current segment's steps run.
+template <int L, int K>
+__device__ __forceinline__ void bulk_catch_up(IState* sl /* this lane's IState, slot stride 32 */,
+                                              const SegRec* ring0 /* instance j's ring: ring0 + j * kRing */,
+                                              const TypeRec* types, const Ctx& c, int l, unsigned valid_mask) {
+  int slot = -1;
+  IState* S = nullptr;
+  const SegRec* ring = nullptr;
+  uint32_t r = 0, rw = 0, k = 0, stop = 0;
+  double t = 0.0, cd = 0.0, A = 0.0, B = 0.0, p7 = 0.0, p8 = 0.0;
+  int phase = 0;  // 0: at ring[r].k, outputs pending; 1: at ring[r].k, outputs written; 2: pure steps
+  SegRec rec, nrec;
+  auto load_seg = [&]() {  // pure steps of record r, up to nrec.k
+    const TypeRec& tr = types[S->ty];
+    const double dn = (double)rec.nact;
+    A = __dmul_rn(tr.p[4], dn);
+    B = __dmul_rn(tr.p[5], dn);
+    p7 = tr.p[6];
+    p8 = tr.p[7];
+    cd = __dadd_rn(rec.cd1, (double)(k - rec.k - 1));
+    nrec = ring[(r + 1) % kRing];
+    stop = nrec.k;
+  };
+  auto next_instance = [&]() -> bool {
+    for (++slot; slot < K; ++slot) {
+      if (!((valid_mask >> slot) & 1u)) continue;
+      S = sl + slot * 32;
+      rw = S->rw;
+      if (rw == 0) continue;
+      r = S->ri;
+      k = S->ak;
+      t = S->at;
+      ring = ring0 + (int64_t)(l + L * slot) * kRing;
+      rec = ring[r % kRing];
+      if (k == rec.k) {
+        phase = S->adone ? 1 : 0;
+        if (phase == 1 && r + 1 == rw) continue;  // already at the last record
+      } else {
+        if (r + 1 == rw) continue;  // past the last record's event step
+        phase = 2;
+        load_seg();
+      }
+      return true;
+    }
+    return false;
+  };
+  bool active = next_instance();
+  while (__any_sync(FULL, active)) {
+    if (!active) continue;
+    if (phase == 2) {
+      // a block of up to four pure steps (the reference's order: t = t + price)
+      const uint32_t n = (stop - k) < 4u ? (stop - k) : 4u;
+      const auto price = [&](double x) {
+        return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(A, x), B), __dmul_rn(p7, x)), p8);
+      };
+      const double c0 = price(cd), c1 = price(__dadd_rn(cd, 1.0)), c2 = price(__dadd_rn(cd, 2.0)),
+                   c3 = price(__dadd_rn(cd, 3.0));
+      const double t1 = __dadd_rn(t, c0);
+      const double t2 = __dadd_rn(t1, c1);
+      const double t3 = __dadd_rn(t2, c2);
+      const double t4 = __dadd_rn(t3, c3);
+      t = n == 4 ? t4 : (n == 3 ? t3 : (n == 2 ? t2 : t1));
+      cd = __dadd_rn(cd, (double)n);
+      k += n;
+      if (k == stop) {  // the next record's event step
+        ++r;
+        rec = nrec;
+        phase = 0;
+      }
+      continue;
+    }
+    if (phase == 0) {  // event step: outputs at its exact time
+      if (rec.flags & R_RESTART) t = rec.t0;
+      if (rec.first_ret >= 0) {
+        S->completion = t;
+        if (c.DEP)
+          for (int32_t x = rec.first_ret; x >= 0; x = c.R[x].next) c.DEP[x] = t;
+      }
+      phase = 1;
+    }
+    // phase 1: leave the event step
+    if (r + 1 == rw) {  // the last record: anchor here, next instance
+      S->ri = r;
+      S->ak = k;
+      S->at = t;
+      S->adone = 1u;
+      active = next_instance();
+      continue;
+    }
+    if (rec.flags & R_IDLE) {  // the next record restarts at the same step index
+      ++r;
+      rec = ring[r % kRing];
+      phase = 0;
+      continue;
+    }
+    t = __dadd_rn(t, rec.c_e);
+    k += 1;
+    load_seg();
+    phase = 2;
+    if (k == stop) {
+      ++r;
+      rec = nrec;
+      phase = 0;
+    }
+  }
+}
+
 // ----------------------------------------------------------------- events
 // The STEP event of one instance at step h.kn (simulator.py:330-355):
 // retirements due at this step (admission order), FCFS admission, prefill
@@ -639,14 +752,15 @@ __device__ __forceinline__ void admission_step(Hot& h, IState& S, SegRec* ring, 
   h.Ehi = t;
 }
 
-// shared memory per block: [IState kWPB*K*32][HEnt kWPB*K*32*kHS2][TypeRec n_types]
+// shared memory per block: [IState kWPB*K*32][HEnt kWPB*K*32*kHS2][TypeRec n_types][prices kWPB*32*n_types]
 template <int K>
 __host__ __device__ constexpr size_t mt_smem_fixed() {
   return sizeof(IState) * kWPB * K * 32 + sizeof(HEnt) * kWPB * K * 32 * kHS2;
 }
+__host__ __device__ inline size_t mt_smem_types(int n_types) { return sizeof(TypeRec) * (size_t)n_types; }
 
 template <int L, int K>
-__global__ void __launch_bounds__(kWPB * 32) k_replay_mt(
+__global__ void __launch_bounds__(kWPB * 32, 1) k_replay_mt(
     int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI, const int32_t* __restrict__ gO,
     const int32_t* __restrict__ gP, const double* __restrict__ gT, uint8_t* __restrict__ assign,
     double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics, hs_trace_result* __restrict__ result,
@@ -659,8 +773,10 @@ __global__ void __launch_bounds__(kWPB * 32) k_replay_mt(
   HEnt(*s_heap)[K][32][kHS2] =
       reinterpret_cast<HEnt(*)[K][32][kHS2]>(reinterpret_cast<char*>(s_dyn) + sizeof(IState) * kWPB * K * 32);
   TypeRec* s_types = reinterpret_cast<TypeRec*>(reinterpret_cast<char*>(s_dyn) + mt_smem_fixed<K>());
-  for (int x = threadIdx.x; x < 256; x += blockDim.x) s_tab[x] = kExpTab[x];
   const int NT = rc.n_types;
+  // per-(arrival, class) prices of the current block of L arrivals: [warp][lane = arrival slot][class]
+  double* s_price = reinterpret_cast<double*>(reinterpret_cast<char*>(s_types) + mt_smem_types(NT));
+  for (int x = threadIdx.x; x < 256; x += blockDim.x) s_tab[x] = kExpTab[x];
   for (int x = threadIdx.x; x < NT * 10; x += blockDim.x) {
     const int t = x / 10, f = x - t * 10;
     double* dst = reinterpret_cast<double*>(s_types + t) + f;
@@ -716,6 +832,7 @@ __global__ void __launch_bounds__(kWPB * 32) k_replay_mt(
     S.cur_max = INT64_MIN;
     S.qhead = -1;
     S.qtail = -1;
+    S.ty = ty[k];
     const int jj = v ? j : 0;
     HEnt* base = reinterpret_cast<HEnt*>(heap_all) + tr * rc.heap_stride;
     heap[k] = Heap{s_heap[wib][k][lane], base + rc.heap_off[jj]};
@@ -755,13 +872,12 @@ __global__ void __launch_bounds__(kWPB * 32) k_replay_mt(
     }
   };
   // every lane brings its instances' exact chains up to their last records
-  auto drain_rings = [&]() {
+  unsigned valid_mask = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      IState& S = s_ist[wib][k][lane];
-      if ((h[k].fl & F_VALID) && S.rw > 0) catch_up(S, h[k].sk, ring[k], s_types[ty[k]], c, ALL, 0, 0.0, nullptr, nullptr);
-    }
-  };
+  for (int k = 0; k < K; ++k) valid_mask |= (h[k].fl & F_VALID) ? (1u << k) : 0u;
+  const SegRec* ring0 = reinterpret_cast<const SegRec*>(reinterpret_cast<HEnt*>(heap_all) + tr * rc.heap_stride +
+                                                        rc.heap_off[N]);
+  auto drain_rings = [&]() { bulk_catch_up<L, K>(&s_ist[wib][0][lane], ring0, s_types, c, l, valid_mask); };
   // all events before t_a (or all events), undecided ones resolved exactly
   auto process_events = [&](double t_a, bool drain) {
     for (;;) {
@@ -820,13 +936,27 @@ __global__ void __launch_bounds__(kWPB * 32) k_replay_mt(
         bP = __ldcg(P + x);
         bT = T ? __ldcg(T + x) : 0.0;
       }
+      // price (arrival, class) pairs of the block (scheduling.py:119-147): the
+      // state-independent part of the workload, one arrival per lane
+      if (policy != HS_POLICY_MB && !failed && x < q) {
+        double* pr = s_price + (size_t)(wib * 32 + lane) * NT;
+        for (int cl = 0; cl < NT; ++cl) {
+          const TypeRec& ct = s_types[cl];
+          const double fl = py_floordiv(ct.budget, i2d(pt * ((int64_t)bI + bP)));
+          int64_t b = (int64_t)fl;
+          if (b < 1) b = 1;
+          const double tot = __dadd_rn(prefill_time(ct.p, b, bI), decode_time(ct.p, b, bI, bP));
+          pr[cl] = (tot <= 0.0) ? -1.0 : __ddiv_rn(tot, i2d(b));
+        }
+      }
+      __syncwarp();
     }
-    {  // keep every ring below half full: the exact chains are rebuilt in bulk
+    {  // keep room in every ring: the exact chains are rebuilt in bulk
       bool full = false;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const IState& S = s_ist[wib][k][lane];
-        full |= S.rw - S.ri >= (uint32_t)(kRing / 2);
+        full |= S.rw - S.ri >= (uint32_t)(kRing - 4);
       }
       if (__any_sync(FULL, full)) drain_rings();
     }
@@ -841,31 +971,11 @@ __global__ void __launch_bounds__(kWPB * 32) k_replay_mt(
     step_error();
     const bool live = !failed && a < q;
 
-    // ---- per-class price of this arrival (scheduling.py:119-147): lane l
-    // prices class l (+L, ...), the owners of each instance fetch theirs
+    // ---- this arrival's price for each instance's class (computed per block)
     double cost[K];
+    const double* prow = s_price + (size_t)(wib * 32 + src) * NT;
 #pragma unroll
-    for (int k = 0; k < K; ++k) cost[k] = 1.0;
-    if (policy != HS_POLICY_MB) {
-      for (int base = 0; base < NT; base += L) {  // NT is launch-uniform
-        double v = 0.0;
-        const int cl = base + l;
-        if (live && cl < NT) {
-          const TypeRec& ct = s_types[cl];
-          const double fl = py_floordiv(ct.budget, i2d(pt * (Ia + Pa)));
-          int64_t b = (int64_t)fl;
-          if (b < 1) b = 1;
-          const double tot = __dadd_rn(prefill_time(ct.p, b, Ia), decode_time(ct.p, b, Ia, Pa));
-          v = (tot <= 0.0) ? -1.0 : __ddiv_rn(tot, i2d(b));
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int want = ty[k] - base;
-          const double got = shfl_d(v, gbase | (want >= 0 && want < L ? want : 0));
-          if (want >= 0 && want < L) cost[k] = got;
-        }
-      }
-    }
+    for (int k = 0; k < K; ++k) cost[k] = (policy != HS_POLICY_MB && live) ? prow[ty[k]] : 1.0;
 
     // ---- choose (scheduling.py:235-254)
     int chosen = -1;
@@ -1092,7 +1202,7 @@ cudaError_t launch_k(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
                      const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign, double* d_depart,
                      hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec, uint64_t* d_heap,
                      cudaStream_t st, const uint32_t* d_progress, int phase_len, double wscale) {
-  const size_t smem = mt_smem_fixed<K>() + (size_t)rc.n_types * sizeof(TypeRec);
+  const size_t smem = mt_smem_fixed<K>() + mt_smem_types(rc.n_types) + sizeof(double) * kWPB * 32 * rc.n_types;
   cudaError_t e = cudaFuncSetAttribute(k_replay_mt<L, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t per_block = (int64_t)kWPB * (32 / L);
