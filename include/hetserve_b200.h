@@ -250,6 +250,10 @@ double hs_ctx_last_kernel_ms(const hs_ctx* ctx);
 void* hs_ctx_stream(const hs_ctx* ctx);
 /* Diagnostic: measured FP64 add throughput of this device (DADD/s). */
 int hs_probe_fp64(hs_ctx* ctx, double* dadd_per_s);
+/* CPython's math.exp (glibc 2.39, FMA ifunc body) as the replay kernels
+ * evaluate it for workload() (scheduling.py:154): y[i] = exp(x[i]) and
+ * overflow[i] = 1 where math.exp raises OverflowError.  Host arrays. */
+int hs_exp_batch(hs_ctx* ctx, const double* x, int64_t n, double* y, uint8_t* overflow);
 
 /* ---- deployment search ------------------------------------------------ */
 /* Fill table[i * HS_MAX_DEGREES + d] for d < n_degrees[i] (degree list =

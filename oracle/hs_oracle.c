@@ -854,3 +854,16 @@ int hs_oracle_replay(const hs_instance* inst, const hs_policy* pol, const hs_tra
   for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
   return HS_OK;
 }
+
+/* Batch forms for the exp tests: the port above, and libm's exp itself (the
+ * function CPython's math.exp calls), over an array. */
+void hs_oracle_exp_batch(const double* x, int64_t n, double* y, uint8_t* of) {
+  for (int64_t i = 0; i < n; ++i) {
+    int o;
+    y[i] = hs_oracle_exp(x[i], &o);
+    of[i] = (uint8_t)o;
+  }
+}
+void hs_libm_exp_batch(const double* x, int64_t n, double* y) {
+  for (int64_t i = 0; i < n; ++i) y[i] = exp(x[i]);
+}

@@ -87,6 +87,23 @@ def exp(x: float):
     return y, bool(of.value)
 
 
+def exp_batch(x):
+    """The C port over an array: (values, overflow flags)."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    of = np.empty(len(x), np.uint8)
+    lib().hs_oracle_exp_batch(_p(x), C.c_int64(len(x)), _p(y), _p(of))
+    return y, of.astype(bool)
+
+
+def libm_exp_batch(x):
+    """glibc's exp itself (what CPython's math.exp calls) over an array."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    lib().hs_libm_exp_batch(_p(x), C.c_int64(len(x)), _p(y))
+    return y
+
+
 def floordiv(a: float, b: float) -> float:
     return lib().hs_oracle_floordiv(float(a), float(b))
 

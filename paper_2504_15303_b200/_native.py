@@ -145,7 +145,7 @@ EXPORTS = (
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
     "hs_replay_seeded", "hs_pcg64_seed", "hs_pcg64_seed_u64", "hs_rng_generate",
     "hs_sched_create", "hs_sched_destroy", "hs_sched_evaluate", "hs_sched_choose", "hs_sched_complete",
-    "hs_sched_snapshot", "hs_plan_instance", "hs_sched_get_state", "hs_sched_set_state", "hs_sched_set_instance",
+    "hs_sched_snapshot", "hs_plan_instance", "hs_sched_get_state", "hs_sched_set_state", "hs_sched_set_instance", "hs_exp_batch",
 )
 
 _lib = None
@@ -198,6 +198,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_sched_get_state": ([vp, i32, vp, vp, vp, vp], C.c_int),
             "hs_sched_set_state": ([vp, i32, dbl, i64, i64, i64], C.c_int),
             "hs_sched_set_instance": ([vp, i32, vp], C.c_int),
+            "hs_exp_batch": ([vp, vp, i64, vp, vp], C.c_int),
             "hs_plan_instance": ([vp, dbl, i64, vp, vp, vp, i64, vp, vp, vp, vp], C.c_int),
             "hs_rng_generate": ([vp, vp, i32, vp, vp, i32, vp, vp], C.c_int),
         }
@@ -333,6 +334,14 @@ class Engine:
                                        None if d_assign is None else C.c_void_p(d_assign), None,
                                        C.c_void_p(d_metrics), C.c_void_p(d_result))
         self.check(rc, "hs_replay_device")
+
+    def exp_batch(self, x: np.ndarray):
+        """hs_exp_batch: (math.exp(x) as the replay kernels compute it, overflow flags)."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        of = np.empty(len(x), np.uint8)
+        self.check(self.lib.hs_exp_batch(self.handle, _ptr(x), len(x), _ptr(y), _ptr(of)), "hs_exp_batch")
+        return y, of.astype(bool)
 
     # --------------------------------------------------------------- streams
     def rng_generate(self, states: np.ndarray, offsets: np.ndarray, dists, outs) -> np.ndarray:

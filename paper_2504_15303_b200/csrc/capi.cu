@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include "hs_device.cuh"
 #include "hs_internal.h"
 
 namespace {
@@ -437,6 +438,45 @@ int hs_probe_fp64(hs_ctx* c, double* out) {
   return HS_OK;
 }
 double hs_ctx_last_kernel_ms(const hs_ctx* c) { return c ? c->last_ms : 0.0; }
+// CPython math.exp (glibc 2.39, FMA variant) as the replay evaluates it
+// (scheduling.py:154 via hs_device.cuh py_exp), over an array.
+__global__ void k_exp_batch(const double* __restrict__ x, int64_t n, double* __restrict__ y,
+                            uint8_t* __restrict__ of) {
+  __shared__ uint64_t tab[256];
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) tab[k] = kExpTab[k];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool o;
+    y[i] = hs::py_exp(x[i], tab, &o);
+    of[i] = o ? 1 : 0;
+  }
+}
+
+int hs_exp_batch(hs_ctx* c, const double* x, int64_t n, double* y, uint8_t* overflow) {
+  if (!c || n < 0 || (n > 0 && (!x || !y || !overflow))) return fail(HS_ERR_ARG, "null argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  if (n == 0) return HS_OK;
+  double *dx, *dy;
+  uint8_t* dof;
+  if ((rc = ensure_t(c, S_TOTAL, (size_t)n, &dx)) || (rc = ensure_t(c, S_KEYS, (size_t)n, &dy)) ||
+      (rc = ensure_t(c, S_FLAG, (size_t)n, &dof)))
+    return rc;
+  HS_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = begin_timing(c))) return rc;
+  const int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  if (blocks > hs::sm_count() * 16) blocks = hs::sm_count() * 16;
+  k_exp_batch<<<(unsigned)blocks, threads, 0, c->stream>>>(dx, n, dy, dof);
+  HS_CUDA(cudaGetLastError());
+  c->launches += 1;
+  if ((rc = end_timing(c))) return rc;
+  HS_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaMemcpyAsync(overflow, dof, (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+
 
 int hs_search_tables(hs_ctx* c, const hs_model* model, const hs_engine* engine, const hs_limits* limits,
                      const hs_machine* machines, int32_t M, const double* params, const uint8_t* present,

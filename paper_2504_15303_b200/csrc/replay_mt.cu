@@ -696,10 +696,18 @@ __device__ __forceinline__ bool events_before(Hot& h, IState& S, const Heap& hea
   return false;
 }
 
-// The exact time of the pending event decides its order against t_a.
+// The exact time of the pending event decides its order against t_a.  The
+// anchor is put back afterwards: a dispatch may still need the exact chain
+// from before that step (the first step at or after t_a, admission_step).
 __device__ __forceinline__ void resolve_exact(Hot& h, IState& S, SegRec* ring, const TypeRec& tr, const Ctx& c) {
+  const uint32_t ak = S.ak, ri = S.ri, adone = S.adone;
+  const double at = S.at;
   double t;
   catch_up(S, h.sk, ring, tr, c, TO_STEP, h.kn, 0.0, nullptr, &t);
+  S.ak = ak;
+  S.ri = ri;
+  S.adone = adone;
+  S.at = at;
   h.Elo = t;
   h.Ehi = t;
 }
@@ -713,6 +721,36 @@ __device__ __forceinline__ void admission_step(Hot& h, IState& S, SegRec* ring, 
   const double p7 = tr.p[6], p8 = tr.p[7];
   const uint32_t nmax = h.kn - h.sk - 1;
   uint32_t lo = 0, hi = nmax;
+  {
+    // closed-form guess from the midpoint of the affine sum:
+    // T(sk + 1 + n) ~ T(sk) + sce + a (n scd + n (n - 1) / 2) + b n
+    const double a = h.sA + p7, b = h.sB + p8;
+    const double c0 = 0.5 * (h.slo + h.shi) + h.sce - t_a;  // < 0 here
+    const double B1 = a * (h.scd - 0.5) + b;
+    double g = nmax;
+    if (a > 0.0) g = (-B1 + sqrt(B1 * B1 - 2.0 * a * c0)) / a;
+    else if (B1 > 0.0) g = -c0 / B1;
+    if (!(g >= 0.0)) g = 0.0;
+    uint32_t n = g >= (double)nmax ? nmax : (uint32_t)ceil(g);
+    // narrow [lo, hi] around the guess with the rigorous bounds
+    for (int it = 0; it < 3 && lo < hi; ++it) {
+      double L, U;
+      seg_bounds(h, p7, p8, c.wscale, n, L, U);
+      if (L >= t_a) {
+        hi = n;
+        if (n == 0) break;
+        seg_bounds(h, p7, p8, c.wscale, n - 1, L, U);
+        if (U < t_a) {
+          lo = n;
+          break;
+        }
+        n = n - 1;
+      } else {
+        lo = n + 1;
+        n = lo < nmax ? lo : nmax;
+      }
+    }
+  }
   while (lo < hi) {  // smallest n whose lower bound reaches t_a (nmax: known to)
     const uint32_t mid = lo + ((hi - lo) >> 1);
     double L, U;
