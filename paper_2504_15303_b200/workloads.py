@@ -19,8 +19,13 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass, field
+from types import SimpleNamespace
 
 import numpy as np
+
+from .domain import enumerate_tp_degrees
+from .scheduling import OutputLengthPredictor, PredictorConfig
+from .simulator import arrival_times
 
 RANK_BASE = (2e-5, 4e-4, 1e-5, 3e-3, 1.5e-6, 2e-4, 5e-7, 1e-4)
 TP_ALPHA = 0.6
@@ -55,13 +60,9 @@ LIMITS = dict(max_input_len=4096, max_output_len=4096)
 
 
 def enumerate_degrees(count: int) -> list[int]:
-    """Power-of-two divisors in ascending order (core.py:363-371)."""
-    out, t = [], 1
-    while t <= count:
-        if count % t == 0:
-            out.append(t)
-        t *= 2
-    return out
+    """core.py:363-371 enumerate_tp_degrees for an accelerator count
+    (domain.enumerate_tp_degrees on a bare count)."""
+    return enumerate_tp_degrees(SimpleNamespace(accelerator_count=count))
 
 
 def scaled_params(base: tuple, alpha: float) -> tuple:
@@ -165,27 +166,16 @@ def trace_lengths(q: int, seed: int, in_mean: float = 200.0, out_mean: float = 1
 
 
 def arrivals(q: int, rate: float, seed: int) -> np.ndarray:
-    """simulator.py:112-124 generate_arrivals as an fp64 array."""
-    if math.isinf(rate):
-        return np.zeros(q, dtype=np.float64)
-    rng = np.random.default_rng(seed)
-    return np.cumsum(rng.exponential(1.0 / rate, size=q))
+    """simulator.py:112-124 generate_arrivals as an fp64 array (simulator.arrival_times)."""
+    return arrival_times(q, rate, seed)
 
 
 def predictions(O: np.ndarray, mode: str = "oracle", mean=None, stddev=None, seed=None,
                 max_output_len: int = 4096) -> np.ndarray:
     """scheduling.py:65-95 OutputLengthPredictor, one draw per request in
-    trace order (the dispatch order), vectorised."""
-    if mode == "oracle":
-        return np.asarray(O, dtype=np.int32).copy()
-    if mode == "mean":
-        v = np.full(len(O), float(round(mean)))
-    elif mode == "normal":
-        rng = np.random.default_rng(seed)
-        v = np.rint(rng.normal(mean, stddev, size=len(O)))
-    else:
-        raise ValueError(mode)
-    return np.clip(v, 1, max_output_len).astype(np.int32)
+    trace order (the dispatch order): OutputLengthPredictor.predict_lengths."""
+    cfg = PredictorConfig(mode=mode, mean=mean, stddev=stddev, seed=seed)
+    return OutputLengthPredictor(cfg, max_output_len).predict_lengths(O).astype(np.int32)
 
 
 def deployment_instances(profile: ClusterProfile, degrees: dict) -> list:

@@ -8,6 +8,7 @@ rate inf and finite, continuous and static mode.  Whole SimMetrics objects are
 compared with == (fp64 bit equality), exceptions by type name and message."""
 
 import math
+from dataclasses import replace
 import pathlib
 import random
 import sys
@@ -97,3 +98,38 @@ def test_fuzzed_scenarios_match_live_reference(ref):
         n_err += want[0] == "err"
         n_neg += case % 4 == 1 and want[0] == "ok"
     assert n_dup > 40 and n_err > 10 and n_neg > 20, (n_dup, n_err, n_neg)
+
+
+def test_run_policy_comparison_matches_live_reference(ref):
+    """run_policy_comparison (simulator.py:372-380): every policy on the
+    identical arrival / prediction realisation, the reference's own function
+    routed through the engine vs the unmodified one, normal predictor
+    included (scheduling.py:87-95)."""
+    from paper_2504_15303_b200 import refbind
+
+    S = sys.modules["hetserve.simulator"]
+    ours = {name: fn for (mod, name), fn in refbind.bindings(ref).items() if mod is S}
+    n = 0
+    for case in range(400, 430):
+        rng = random.Random(case)
+        sc = _scenario(ref, rng, 4 * case)  # kind 0: plain coefficients
+        ids = [f"r{k}" for k in range(len(sc.trace))]  # unique ids: compare metrics, not errors
+        trace = tuple(ref.Request(i, r.input_len, r.output_len, r.predicted_output_len) for i, r in zip(ids, sc.trace))
+        n_inst = sum(p.instance_count for p in sc.config.per_machine)
+        pred = ref.PredictorConfig(mode="normal", mean=30.0, stddev=12.0, seed=case) if case % 2 else \
+            ref.PredictorConfig()
+        pol = ref.PolicyConfig(policy="OS", theta=2.0, wrr_weights=tuple(float(1 + k % 3) for k in range(n_inst)),
+                               predictor=pred)
+        sc = replace(sc, trace=trace, policy=pol)
+        names = ["OS", "RR", "WRR", "SI", "MB"]
+        want = _outcome(lambda s: S.run_policy_comparison(s, names), sc)
+        # the reference's own run_policy_comparison, with run_continuous / run_static routed to the engine
+        saved = (S.run_continuous, S.run_static)
+        S.run_continuous, S.run_static = ours["run_continuous"], ours["run_static"]
+        try:
+            got = _outcome(lambda s: S.run_policy_comparison(s, names), sc)
+        finally:
+            S.run_continuous, S.run_static = saved
+        assert got == want, case
+        n += want[0] == "ok"
+    assert n >= 20

@@ -35,9 +35,11 @@ def _run(files, scheduler: bool):
 
 @pytest.mark.gpu
 def test_reference_planner_simulator_acceptance_through_engine():
-    """test_planner.py, test_simulator.py and test_acceptance.py (criteria 1-8)
-    with the search and both simulator modes on the GPU."""
-    rc, out = _run(["test_planner.py", "test_simulator.py", "test_acceptance.py"], scheduler=False)
+    """test_planner.py, test_simulator.py, test_acceptance.py (criteria 1-8)
+    and test_cli.py (hetserve plan / simulate / compare, incl. the plan
+    report's byte stability) with the search and both simulator modes on the
+    GPU."""
+    rc, out = _run(["test_planner.py", "test_simulator.py", "test_acceptance.py", "test_cli.py"], scheduler=False)
     assert rc == 0, out[-6000:]
     assert " failed" not in out and "[criterion 8] PASS" in out, out[-3000:]
 
