@@ -355,7 +355,7 @@ def reference_arm(args, rank, world):
     vals = []
     try:
         for k in range(args.warmup + args.steps):
-            v = reference_baseline(pool, P, R, tables, q_trace=4000, n_traces=cores, n_uniform=cores * 400,
+            v = reference_baseline(pool, P, R, tables, q_trace=4000, n_traces=cores, n_uniform=cores * 100,
                                    n_feasible=cores, seed=k)
             if k >= args.warmup:
                 vals.append(v)

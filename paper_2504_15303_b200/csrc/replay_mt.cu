@@ -35,9 +35,12 @@
 // bounds, process their due events and take part in the dispatch reductions
 // (log2 L shuffle levels inside the trace's lane group).
 //
-// Used for continuous mode, one deployment of <= 32 instances, non-negative
-// latency coefficients, no order keys (launch_replay picks it;
-// HS_REPLAY_LEGACY=1 forces replay.cu's kernel).
+// Used, when HS_REPLAY_MT=1, for continuous mode, one deployment of <= 32
+// instances, non-negative latency coefficients, no order keys.  Measured
+// slower than replay.cu's kernel on config 4 (K3): the per-arrival
+// event and dispatch work and the bulk catch-ups (whose lanes carry unequal
+// pending steps) cost more than the per-arrival stepping they replace.  Kept
+// opt-in and parity-tested (tests/test_gpu_replay_layouts.py).
 #include <cstdlib>
 
 #include "hs_device.cuh"
@@ -1263,8 +1266,9 @@ int lanes_per_trace() {
 }  // namespace
 
 bool replay_mt_eligible(const ReplayConst& rc, bool multi) {
-  static const bool legacy = std::getenv("HS_REPLAY_LEGACY") != nullptr;
-  if (legacy || multi || rc.mode != 0 || rc.flags != 0 || rc.N < 1 || rc.N > 32) return false;
+  // opt-in (HS_REPLAY_MT=1): measured slower than replay.cu's kernel (K3)
+  static const bool on = std::getenv("HS_REPLAY_MT") != nullptr && std::getenv("HS_REPLAY_LEGACY") == nullptr;
+  if (!on || multi || rc.mode != 0 || rc.flags != 0 || rc.N < 1 || rc.N > 32) return false;
   for (int t = 0; t < rc.n_types; ++t)  // the interval bounds need non-negative prices
     for (int f = 0; f < 8; ++f)
       if (!(rc.type_p[t][f] >= 0.0)) return false;

@@ -1,8 +1,9 @@
-"""K3 kernel configurations vs the oracle, bit for bit: the trace-group
-kernel (replay_mt.cu) at 8 / 16 / 32 lanes per trace, with its interval
-bounds as built and artificially widened (HS_REPLAY_WIDEN: nearly every
-event order and admission step is then settled by the exact clock chain
-instead of the bounds), and the one-warp-per-trace kernel (replay.cu).
+"""K3 kernel configurations vs the oracle, bit for bit: the default
+one-warp-per-trace kernel (replay.cu) and the opt-in interval-bound kernel
+(replay_mt.cu, HS_REPLAY_MT=1) at 8 / 16 / 32 lanes per trace, with its
+bounds as built and artificially widened (HS_REPLAY_WIDEN: many event orders
+and admission steps are then settled by the exact clock chain instead of
+the bounds).
 Each configuration runs in its own process (the library reads the
 environment once)."""
 
@@ -16,16 +17,16 @@ import pytest
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 pytestmark = pytest.mark.gpu
 
+MT = {"HS_REPLAY_MT": "1"}
 CONFIGS = [
-    ({"HS_REPLAY_LANES": "8"}, 32),
-    ({"HS_REPLAY_LANES": "16"}, 32),
-    ({"HS_REPLAY_LANES": "32"}, 32),
-    ({"HS_REPLAY_LANES": "8"}, 9),
-    ({"HS_REPLAY_LANES": "16"}, 17),
-    ({"HS_REPLAY_LANES": "8", "HS_REPLAY_WIDEN": "1e9"}, 32),
-    ({"HS_REPLAY_LANES": "16", "HS_REPLAY_WIDEN": "1e15"}, 32),
-    ({"HS_REPLAY_LANES": "32", "HS_REPLAY_WIDEN": "1e15"}, 24),
-    ({"HS_REPLAY_LEGACY": "1"}, 32),
+    ({**MT, "HS_REPLAY_LANES": "8"}, 32),
+    ({**MT, "HS_REPLAY_LANES": "16"}, 32),
+    ({**MT, "HS_REPLAY_LANES": "32"}, 32),
+    ({**MT, "HS_REPLAY_LANES": "8"}, 9),
+    ({**MT, "HS_REPLAY_LANES": "16"}, 17),
+    ({**MT, "HS_REPLAY_LANES": "8", "HS_REPLAY_WIDEN": "1e6"}, 32),
+    ({**MT, "HS_REPLAY_LANES": "32", "HS_REPLAY_WIDEN": "1e7"}, 24),
+    ({}, 32),
 ]
 
 
