@@ -261,20 +261,19 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
 
 // Heap overflow regions from the exact active-set bound: at most
 // floor(budget / (per_token * min(I+O))) requests fit an instance at once.
-void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q, bool multi = false) {
+void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q) {
   if (min_need < 1) min_need = 1;
   int64_t acc = 0;
   for (int j = 0; j < rc.N; ++j) {
     const double tokens = std::floor(inst[j].budget / (double)rc.per_token);
     const double capd = std::floor(tokens / (double)min_need) + 1.0;
     int64_t capj = capd > (double)max_q ? max_q : (int64_t)capd;
-    capj -= hs::replay_shared_heap(rc, multi);  // the first entries live in shared memory
+    capj -= hs::kHeapShared;  // the first entries live in shared memory
     if (capj < 1) capj = 1;
     rc.heap_off[j] = acc;
     acc += capj;
   }
   rc.heap_off[rc.N] = acc;
-  acc += hs::replay_extra_heap_entries(rc, multi);  // per-instance segment rings after the heaps
   rc.heap_stride = (acc + 15) / 16 * 16;
 }
 
@@ -1357,7 +1356,7 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
   int32_t min_need = 0;
   HS_CUDA(cudaMemcpyAsync(&min_need, dMin, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q, true);
+  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q);
   std::vector<int64_t> theap((size_t)(T > 0 ? T : 1));
   int64_t hacc = 0;
   for (int64_t t = 0; t < T; ++t) {

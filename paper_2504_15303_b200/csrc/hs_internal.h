@@ -104,17 +104,6 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           const int32_t* d_trace_dep = nullptr, const int64_t* d_trace_heap = nullptr,
                           int n_max = 0, int max_types = 0, const uint32_t* d_progress = nullptr,
                           int phase_len = 0);
-// replay_mt.cu: the trace-group kernel (continuous mode, one deployment of
-// <= 32 instances, no order keys); launch_replay dispatches to it.
-bool replay_mt_eligible(const ReplayConst& rc, bool multi);
-// heap entries per instance the chosen kernel keeps in shared memory
-int replay_shared_heap(const ReplayConst& rc, bool multi);
-// extra heap-buffer entries per trace the chosen kernel needs (segment rings)
-int64_t replay_extra_heap_entries(const ReplayConst& rc, bool multi);
-cudaError_t launch_replay_mt(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
-                             const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign,
-                             double* d_depart, hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec,
-                             uint64_t* d_heap, cudaStream_t st, const uint32_t* d_progress, int phase_len);
 constexpr int kQRecBytes = 24;  // replay.cu QRec
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
 constexpr int kHeapShared = 16;  // replay.cu kHS

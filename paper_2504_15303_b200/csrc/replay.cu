@@ -1015,9 +1015,6 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           const int64_t* d_trace_heap, int n_max, int max_types, const uint32_t* d_progress,
                           int phase_len) {
   if (n_traces <= 0) return cudaSuccess;
-  if (replay_mt_eligible(rc, d_deps != nullptr))  // trace-group layout (replay_mt.cu)
-    return launch_replay_mt(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result, d_qrec,
-                            d_heap, st, d_progress, phase_len);
   if (n_max <= 0) n_max = rc.N;
   if (max_types <= 0) max_types = rc.n_types;
   const int W = (n_max + 31) / 32;

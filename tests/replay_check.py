@@ -1,7 +1,5 @@
-"""Batched replay vs the C oracle, for one kernel configuration chosen by the
-environment (HS_REPLAY_LANES, HS_REPLAY_WIDEN, HS_REPLAY_LEGACY are read once
-per process by the library).  Run by tests/test_gpu_replay_layouts.py in a
-subprocess per configuration; prints OK or raises."""
+"""Batched replay vs the C oracle (run by tests/test_gpu_replay_layouts.py);
+prints OK or raises."""
 
 import math
 import pathlib
