@@ -709,8 +709,7 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
             loc[:len(cands), 1] = cands["index"]
             buf.copy_(torch.from_numpy(loc))
             outs = [torch.zeros_like(buf) for _ in range(world)]
-            with torch.cuda.stream(ext):
-                tdist.all_gather(outs, buf)
+            tdist.all_gather(outs, buf)  # on the stream that wrote buf
             parts = []
             for o in outs:
                 h = o.cpu().numpy()

@@ -53,6 +53,7 @@ def combine_best(total: float, index: int, n_feasible: int, group=None, device=N
     if device is not None:
         slot = slot.to(device)
     if stream is not None:
+        stream.wait_stream(torch.cuda.current_stream(slot.device))  # the slot's copy lands first
         with torch.cuda.stream(stream):
             dist.all_reduce(slot, group=group)
             host = slot.cpu().numpy()

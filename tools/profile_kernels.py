@@ -2,6 +2,7 @@
 
     python tools/profile_kernels.py replay [traces] [q]
     python tools/profile_kernels.py search
+    python tools/profile_kernels.py config5 [deployments] [q]
 
 Runs one warm-up call and one measured call; prints the kernel time.
 """
@@ -78,6 +79,23 @@ def main():
                   "lane pure blocks %.2f, rescans %.4f (mean len %.1f), event steps with nact>16: %.3f, mean nact %.1f"
                   % (buf[8] / n, buf[12] / max(buf[8], 1), buf[9] / n, buf[13] / n, buf[10] / n,
                      buf[11] / max(buf[10], 1), buf[14] / calls, buf[15] / calls))
+    elif what == "config5":
+        import numpy as np
+        from paper_2504_15303_b200 import workloads as wl
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+        q = int(sys.argv[3]) if len(sys.argv) > 3 else 100_000
+        cluster, reqs, params, _I, _O = bench.search_inputs(10_000)
+        t = planner.build_tables(cluster, reqs, params, engine=eng)
+        top, _nf, _ = planner.search_topk(t, n, engine=eng)
+        I1, O1 = wl.trace_lengths(q, seed=0)
+        off = np.arange(n + 1, dtype=np.int64) * q
+        I, O = np.tile(I1, n), np.tile(O1, n)
+        for _ in range(2):
+            res = hs.replay_candidates(t, params, top["index"], hs.PolicyConfig(), np.arange(n), off, I, O, O,
+                                       engine=eng, want_assign=False)
+        assert (res.result["error"] == 0).all()
+        print(f"config5 replay {n} deployments x {q}: {res.kernel_ms:.2f} ms, "
+              f"{res.result['n_steps'].sum() / (n * q):.2f} steps/request")
     else:
         cluster, reqs, params, _I, _O = bench.search_inputs(10_000)
         t = planner.build_tables(cluster, reqs, params, engine=eng)
