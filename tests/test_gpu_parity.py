@@ -425,31 +425,44 @@ def test_config4_full_size_policies_vs_oracle(eng, policy, pred):
 
 def test_config5_full_size_rescore_vs_oracle(eng):
     """BASELINE config 5 at full size for a slice: the top-1024 deployments of
-    the config-3 space, the first 16 of them each replayed on the 1e5-request
-    trace (rate = inf, OS) in one launch, vs the oracle."""
+    the config-3 space, the first 128 of them each replayed on the 1e5-request
+    trace (rate = inf, OS; up to 72 instances = 3 warps per trace, the
+    warp-0 dispatch phase) in one launch, vs the oracle."""
+    from concurrent.futures import ThreadPoolExecutor
     _case, _req, t = _config3_tables(eng)
     top, _nf, _ = planner.search_topk(t, 1024, engine=eng)
     assert len(top) == 1024
-    configs = [planner.deployment_of(t, int(i)) for i in top["index"][:16]]
+    n = 128
+    configs = [planner.deployment_of(t, int(i)) for i in top["index"][:n]]
     p3 = wl.config3()
     params = {k: hs.LatencyParams(*v) for k, v in p3.params.items()}
     q = wl.CONFIG4_Q
     I1, O1 = wl.trace_lengths(q, seed=0)
-    n = len(configs)
     off = np.arange(n + 1, dtype=np.int64) * q
     res = hs.replay_deployments(t.cluster, configs, params, hs.PolicyConfig(), np.arange(n), off, np.tile(I1, n),
                                 np.tile(O1, n), np.tile(O1, n), want_depart=True, engine=eng)
     from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
     per_token = hs.kv_bytes_per_token(t.cluster.model)
-    for d in range(n):
+
+    def oracle(d):
         handles = build_instances(t.cluster, configs[d], params)
-        sl = slice(off[d], off[d + 1])
-        a, dep, m, r = orc.replay(engine_instances(handles, hs.PolicyConfig()),
-                                  _policy_struct(hs.PolicyConfig(), len(handles), per_token),
-                                  np.array([0, q], np.int64), I1, O1, O1, None)
-        assert int(res.result[d]["error"]) == 0 == int(r[0]["error"])
-        assert np.array_equal(res.assign[sl], a)
-        assert np.array_equal(res.depart[sl].view(np.uint64), dep.view(np.uint64))
+        return orc.replay(engine_instances(handles, hs.PolicyConfig()),
+                          _policy_struct(hs.PolicyConfig(), len(handles), per_token),
+                          np.array([0, q], np.int64), I1, O1, O1, None)
+
+    widths = set()
+    with ThreadPoolExecutor(max_workers=16) as ex:
+        for d, (a, dep, m, r) in enumerate(ex.map(oracle, range(n))):
+            sl = slice(off[d], off[d + 1])
+            assert int(res.result[d]["error"]) == 0 == int(r[0]["error"])
+            assert res.result[d]["n_steps"] == r[0]["n_steps"]
+            assert np.array_equal(res.assign[sl], a)
+            assert np.array_equal(res.depart[sl].view(np.uint64), dep.view(np.uint64))
+            nd = m.shape[1]
+            for f in ("completion_time", "peak_kv_usage", "residual_load"):
+                assert np.array_equal(res.metrics[d][:nd][f].view(np.uint64), m[0][f].view(np.uint64)), (d, f)
+            widths.add((nd + 31) // 32)
+    assert 3 in widths
 
 
 def test_replay_candidates_equals_object_path(eng):
@@ -524,3 +537,42 @@ def test_replay_deployments_mixed_class_counts_small_deployments(eng):
             n = len(handles)
             for f in ("completion_time", "peak_kv_usage", "residual_load"):
                 assert np.array_equal(res.metrics[t][:n][f].view(np.uint64), m[0][f].view(np.uint64)), f
+
+
+@pytest.mark.parametrize("policy", ["OS", "RR", "WRR", "SI", "MB"])
+def test_multiwarp_rate_inf_dispatch_phase_vs_oracle(eng, policy):
+    """W = 2-3 warps per trace at rate = inf: warp 0 makes the whole dispatch
+    sequence, then every warp steps its own instances (replay.cu inf_multi);
+    each policy, continuous and static mode, vs the oracle."""
+    _case, _req, t = _config3_tables(eng)
+    top, _nf, _ = planner.search_topk(t, 64, engine=eng)
+    p3 = wl.config3()
+    params = {k: hs.LatencyParams(*v) for k, v in p3.params.items()}
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    per_token = hs.kv_bytes_per_token(t.cluster.model)
+    seen = set()
+    for idx in top["index"][::16]:
+        config = planner.deployment_of(t, int(idx))
+        handles = build_instances(t.cluster, config, params)
+        N = len(handles)
+        seen.add((N + 31) // 32)
+        wrr = tuple(float(1 + k % 4) for k in range(N)) if policy == "WRR" else None
+        pol = hs.PolicyConfig(policy=policy, wrr_weights=wrr)
+        q, T = 6000, 3
+        Is, Os = zip(*[wl.trace_lengths(q, seed=300 + k) for k in range(T)])
+        I, O = np.concatenate(Is), np.concatenate(Os)
+        off = np.arange(T + 1, dtype=np.int64) * q
+        for static in (False, True):
+            res = hs.replay_traces(t.cluster, config, params, pol, off, I, O, O, want_depart=True, engine=eng,
+                                   static=static)
+            a, d, m, r = orc.replay(engine_instances(handles, pol),
+                                    _policy_struct(pol, N, per_token, 1 if static else 0), off, I, O, O, None,
+                                    nthreads=4)
+            assert (res.result["error"] == 0).all() and (r["error"] == 0).all()
+            assert np.array_equal(res.assign, a), (policy, N, static)
+            assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64)), (policy, N, static)
+            for f in ("completion_time", "peak_kv_usage", "residual_load"):
+                assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), (policy, N, f)
+            for f in ("request_count", "token_count"):
+                assert np.array_equal(res.metrics[f], m[f]), (policy, N, f)
+    assert seen & {2, 3}
