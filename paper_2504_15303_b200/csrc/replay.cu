@@ -197,10 +197,6 @@ struct Cold {
   int32_t req_count, cnt_max, err, err_req;
   int32_t ty;    // instance class (read from here: a per-lane constant-bank index serialises)
   int32_t nret;  // HS_REPLAY_ORDER_KEYS: retirements so far (per-lane processing order)
-  // rate = inf, W > 1: the dispatch phase's bookkeeping handed to the instance's own lane
-  double h_load;
-  int64_t h_runi, h_runp;
-  int32_t h_qhead, h_qtail;
 };
 
 // ReplayConst.flags
@@ -629,265 +625,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
   const bool is_static = c_rep.mode == 1;
   bool failed = false;
   uint8_t my_assign = 0;
-  // Rate = inf (simulator.py:117-118) with W > 1 warps per trace: every
-  // arrival pops before any step, so the whole dispatch sequence involves no
-  // stepping (advance() would find nothing due).  Warp 0 of the trace group
-  // then makes every decision alone -- lane l owns instances l + 32k -- with
-  // warp reductions instead of W-warp exchanges behind named barriers, and
-  // hands each instance's bookkeeping to its own lane for the steps.  Same
-  // evaluation and tie order as the per-arrival loop below.
-  const bool inf_multi = W > 1 && T == nullptr;
-  if (inf_multi) {
-    if (wsub == 0) {
-      double ld[W], exk[W];
-      int64_t rik[W], rpk[W], tck[W];
-      int32_t qh[W], qt[W], rck[W], tyk[W];
-      uint32_t flk[W];  // 1 valid, 2 dirty, 4 exp overflow
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        const int j = lane + 32 * k;
-        ld[k] = 0.0;
-        exk[k] = 1.0;
-        rik[k] = rpk[k] = tck[k] = 0;
-        qh[k] = qt[k] = -1;
-        rck[k] = 0;
-        tyk[k] = j < N ? c_rep.inst_type[j] : 0;
-        flk[k] = j < N ? 3u : 0u;
-      }
-      const bool eval_all = policy == HS_POLICY_OS || policy == HS_POLICY_MB;
-      int64_t rrn = 0;
-      for (int64_t base = 0; base < q && !failed; base += 32) {
-        const int n_in = (int)((q - base) < 32 ? (q - base) : 32);
-        if (progress) {  // streamed inputs: warp 0 alone consumes them
-          const uint32_t need = (uint32_t)((base + n_in - 1) / phase_len);
-          int stalled = 0;
-          if (lane == 0) {
-            const long long t0 = clock64();
-            uint32_t have;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(have) : "l"(progress) : "memory");
-            while (have <= need) {
-              __nanosleep(256);
-              if (clock64() - t0 > 20000000000ll) {
-                stalled = 1;
-                break;
-              }
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(have) : "l"(progress) : "memory");
-            }
-          }
-          if (__shfl_sync(FULL, stalled, 0)) {
-            t_err = HS_TRACE_STALLED;
-            t_err_req = base;
-            t_err_inst = -1;
-            failed = true;
-            break;
-          }
-        }
-        int32_t cI = 0, cO = 0, cP = 0;
-        if (lane < n_in) {
-          cI = __ldcg(I + base + lane);
-          cO = __ldcg(O + base + lane);
-          cP = __ldcg(P + base + lane);
-        }
-        __syncwarp();
-        if (policy != HS_POLICY_MB) {  // price (arrival, class) pairs: scheduling.py:119-147
-          for (int pair0 = 0; pair0 < n_in * NT; pair0 += 32) {
-            const int pair = pair0 + lane;
-            const int al = pair / NT, tyc = pair - al * NT;
-            const int srcl = al < 32 ? al : 0;
-            const int64_t Ia = __shfl_sync(FULL, cI, srcl);
-            const int64_t Pa = __shfl_sync(FULL, cP, srcl);
-            if (pair < n_in * NT) {
-              const double fl = py_floordiv(types[tyc].budget, i2d(pt * (Ia + Pa)));
-              int64_t b = (int64_t)fl;
-              if (b < 1) b = 1;
-              const double* ctp = types[tyc].p;
-              const double tot = __dadd_rn(prefill_time(ctp, b, Ia), decode_time(ctp, b, Ia, Pa));
-              cost[pair] = (tot <= 0.0) ? -1.0 : __ddiv_rn(tot, i2d(b));
-            }
-          }
-          __syncwarp();
-        }
-        for (int al = 0; al < n_in; ++al) {
-          const int64_t a = base + al;
-          const int64_t Ia = __shfl_sync(FULL, cI, al);
-          const int64_t Oa = __shfl_sync(FULL, cO, al);
-          const int64_t Pa = __shfl_sync(FULL, cP, al);
-          // ---- choose (scheduling.py:235-254)
-          int chosen = -1;
-          if (policy == HS_POLICY_SI) {
-            chosen = 0;
-          } else if (policy == HS_POLICY_RR) {
-            chosen = (int)(rrn % N);
-            rrn += 1;
-          } else if (policy == HS_POLICY_WRR) {  // first strict maximum after adding the weights
-            uint64_t lk = 0;
-            int lj = 0x7fffffff;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-              const int j = lane + 32 * k;
-              if (!(flk[k] & 1u)) continue;
-              Cold& cc = s_cold[g * W * 32 + j];
-              cc.wcur = __dadd_rn(cc.wcur, c_rep.wrr_weight[j]);
-              const uint64_t wk = okey(cc.wcur);
-              if (wk > lk || lj == 0x7fffffff) {
-                lk = wk;
-                lj = j;
-              }
-            }
-            const uint64_t mk = warp_max_u64(lk);
-            chosen = (int)__reduce_min_sync(FULL, (lk == mk && lj != 0x7fffffff) ? (unsigned)lj : 0x7fffffffu);
-            if ((chosen & 31) == lane) {
-              Cold& cc = s_cold[g * W * 32 + chosen];
-              cc.wcur = __dsub_rn(cc.wcur, c_rep.wrr_total);
-            }
-          }
-          // ---- evaluate (scheduling.py:216-233)
-          double w[W];
-          int ej = 0x7fffffff, ecode = 0;
-          double eval = 0.0;
-#pragma unroll
-          for (int k = 0; k < W; ++k) {
-            w[k] = INFINITY;
-            const int j = lane + 32 * k;
-            if (!(flk[k] & 1u) || !(eval_all || j == chosen)) continue;
-            double cst = 1.0;
-            if (policy != HS_POLICY_MB) cst = cost[al * NT + tyk[k]];
-            if (flk[k] & 2u) {  // capacity.py:98-106 kv_usage, scheduling.py:154 exp
-              const double usage = __ddiv_rn(i2d(pt * (rik[k] + rpk[k])), types[tyk[k]].budget);
-              bool of;
-              exk[k] = py_exp(__dmul_rn(theta, usage), s_tab, &of);
-              flk[k] = (flk[k] & ~6u) | (of ? 4u : 0u);
-            }
-            const bool ce = cst < 0.0, ee = (flk[k] & 4u) != 0;
-            if ((ce || ee) && j < ej) {  // the first instance in evaluation order raises
-              ej = j;
-              ecode = ce ? HS_TRACE_NONPOSITIVE_COST : HS_TRACE_EXP_OVERFLOW;
-              if (ce) {
-                const TypeRec& t_ = types[tyk[k]];
-                const double fl = py_floordiv(t_.budget, i2d(pt * (Ia + Pa)));
-                int64_t b = (int64_t)fl;
-                if (b < 1) b = 1;
-                eval = __dadd_rn(prefill_time(t_.p, b, Ia), decode_time(t_.p, b, Ia, Pa));
-              }
-            }
-            w[k] = __dmul_rn(cst, exk[k]);
-          }
-          const unsigned fj = __reduce_min_sync(FULL, (unsigned)ej);
-          if (fj != 0x7fffffffu) {
-            const int own = (int)(fj & 31u);
-            t_err = __shfl_sync(FULL, ecode, own);
-            t_err_val = shfl_d(eval, own);
-            if (t_err != HS_TRACE_NONPOSITIVE_COST) t_err_val = 0.0;
-            t_err_inst = (int32_t)fj;
-            t_err_req = a;
-            failed = true;
-            break;
-          }
-          if (eval_all) {
-            // _min_max_choice (scheduling.py:299-312): argmin (lowest index) of max(L_s + w_s, max_j L_j)
-            uint64_t lm = 0;
-#pragma unroll
-            for (int k = 0; k < W; ++k)
-              if (flk[k] & 1u) {
-                const uint64_t kk = okey(ld[k]);
-                lm = kk > lm ? kk : lm;
-              }
-            const double top = from_okey(warp_max_u64(lm));
-            uint64_t pk = ~0ull;
-            int pj = 0x7fffffff;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-              const double own = __dadd_rn(ld[k], w[k]);
-              const double peak = own > top ? own : top;
-              const bool cand = (flk[k] & 1u) && !isinf(w[k]) && peak < INFINITY;
-              const uint64_t key = cand ? okey(peak) : ~0ull;
-              if (key < pk) {
-                pk = key;
-                pj = lane + 32 * k;
-              }
-            }
-            const uint64_t mp = warp_min_u64(pk);
-            if (mp == ~0ull) {
-              t_err = HS_TRACE_NO_INSTANCE;
-              t_err_req = a;
-              t_err_inst = -1;
-              failed = true;
-              break;
-            }
-            chosen = (int)__reduce_min_sync(FULL, pk == mp ? (unsigned)pj : 0x7fffffffu);
-          }
-          // ---- commit (scheduling.py:335-346) and enqueue (simulator.py:323-327)
-          if ((chosen & 31) == lane) {
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-              if (lane + 32 * k != chosen) continue;
-              ld[k] = __dadd_rn(ld[k], w[k]);
-              rik[k] += Ia;
-              rpk[k] += Pa;
-              flk[k] |= 2u;
-              rck[k] += 1;
-              tck[k] += Ia + Oa;
-              R[a].P = (int32_t)Pa;
-              R[a].W = w[k];
-              if (qh[k] < 0) {
-                qh[k] = (int32_t)a;
-              } else {  // every link is written: the lanes rebuild their queue heads from R
-                QRec& tq = R[qt[k]];
-                tq.next = (int32_t)a;
-                tq.nI = (int32_t)Ia;
-                tq.nO = (int32_t)Oa;
-              }
-              qt[k] = (int32_t)a;
-            }
-          }
-          if (lane == al) my_assign = (uint8_t)chosen;
-        }
-        if (assign && lane < n_in && !failed) assign[o + base + lane] = my_assign;
-      }
-      // hand each instance's bookkeeping to its own lane
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        const int j = lane + 32 * k;
-        if (!(flk[k] & 1u)) continue;
-        Cold& cc = s_cold[g * W * 32 + j];
-        cc.h_load = ld[k];
-        cc.h_runi = rik[k];
-        cc.h_runp = rpk[k];
-        cc.h_qhead = qh[k];
-        cc.h_qtail = qt[k];
-        cc.req_count = rck[k];
-        cc.tok_count = tck[k];
-      }
-      if (lane == 0) xg[0] = Xch{0, 0, failed ? 1 : 0, 0};
-    }
-    group_bar(g, W * 32);
-    failed = xg[0].c != 0;
-    if (valid) {
-      load = cold.h_load;
-      run_i = cold.h_runi;
-      run_p = cold.h_runp;
-      qhead = cold.h_qhead;
-      qtail = cold.h_qtail;
-      if (qhead >= 0) {
-        hI = I[qhead];
-        hO = O[qhead];
-        hP = R[qhead].P;
-        hW = R[qhead].W;
-        if (qhead != qtail) {
-          const QRec hr = R[qhead];
-          hnext = hr.next;
-          hnI = hr.nI;
-          hnO = hr.nO;
-        }
-        sched = true;  // schedule_step(idx, 0.0) at the first dispatch (simulator.py:292-295)
-        t_next = 0.0;
-        blocked = false;
-      }
-      dirty = true;
-    }
-    group_bar(g, W * 32);
-  }
-  for (int64_t base = 0; base < q && !failed && !inf_multi; base += 32) {
+  for (int64_t base = 0; base < q && !failed; base += 32) {
     const int n_in = (int)((q - base) < 32 ? (q - base) : 32);
     if (progress) {
       // streamed inputs (host path): phase p of every trace is resident once
