@@ -42,7 +42,7 @@ extern "C" {
 #define HS_ABI_VERSION 4
 #define HS_MAX_DEGREES 32   /* power-of-two divisors of an accelerator count  */
 #define HS_MAX_MACHINES 64
-#define HS_MAX_INSTANCES 128 /* one lane per instance, up to 4 warps per trace */
+#define HS_MAX_INSTANCES 255 /* one lane per instance, up to 8 warps per trace; uint8 assignments */
 #define HS_MAX_CLASSES 32    /* distinct (params, budget) instance classes      */
 
 /* call status */

@@ -15,7 +15,7 @@ import numpy as np
 
 HS_MAX_DEGREES = 32
 HS_MAX_MACHINES = 64
-HS_MAX_INSTANCES = 128
+HS_MAX_INSTANCES = 255
 HS_MAX_CLASSES = 32
 
 # enums (hetserve_b200.h)

@@ -216,7 +216,7 @@ __global__ void k_gather_ranked(const double* total, const int64_t* idx, const i
 int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, hs::ReplayConst* out) {
   const int N = pol->n_instances;
   if (N < 1) return fail(HS_ERR_ARG, "n_instances must be >= 1");
-  if (N > HS_MAX_INSTANCES) return fail(HS_ERR_UNSUPPORTED, "more than 128 instances per deployment");
+  if (N > HS_MAX_INSTANCES) return fail(HS_ERR_UNSUPPORTED, "more than 255 instances per deployment");
   if (pol->policy < HS_POLICY_OS || pol->policy > HS_POLICY_MB) return fail(HS_ERR_ARG, "unknown policy");
   if (pol->per_token <= 0) return fail(HS_ERR_ARG, "per_token must be positive");
   if (pol->mode != 0 && pol->mode != 1) return fail(HS_ERR_ARG, "mode must be 0 (continuous) or 1 (static)");
@@ -261,14 +261,17 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
 
 // Heap overflow regions from the exact active-set bound: at most
 // floor(budget / (per_token * min(I+O))) requests fit an instance at once.
-void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q) {
+// n_max: the widest deployment of the launch (it picks the kernel's warps per
+// trace, hence how many heap entries per lane live in shared memory).
+void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q, int n_max = 0) {
+  const int shared = hs::replay_heap_prefix(((n_max > 0 ? n_max : rc.N) + 31) / 32);
   if (min_need < 1) min_need = 1;
   int64_t acc = 0;
   for (int j = 0; j < rc.N; ++j) {
     const double tokens = std::floor(inst[j].budget / (double)rc.per_token);
     const double capd = std::floor(tokens / (double)min_need) + 1.0;
     int64_t capj = capd > (double)max_q ? max_q : (int64_t)capd;
-    capj -= hs::kHeapShared;  // the first entries live in shared memory
+    capj -= shared;  // the first entries live in shared memory
     if (capj < 1) capj = 1;
     rc.heap_off[j] = acc;
     acc += capj;
@@ -1356,7 +1359,7 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
   int32_t min_need = 0;
   HS_CUDA(cudaMemcpyAsync(&min_need, dMin, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q);
+  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q, n_max);
   std::vector<int64_t> theap((size_t)(T > 0 ? T : 1));
   int64_t hacc = 0;
   for (int64_t t = 0; t < T; ++t) {

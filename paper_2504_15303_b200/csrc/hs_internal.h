@@ -47,7 +47,7 @@ struct FeasSpace {
   int32_t orig[kMaxM * HS_MAX_DEGREES];  // its original digit
 };
 
-constexpr int kMaxReplayInst = 128;  // up to 4 warps per trace
+constexpr int kMaxReplayInst = 256;  // up to 8 warps per trace (<= 255 instances: uint8 assignments)
 constexpr int kMaxTypes = 32;         // distinct (params, budget) classes per deployment
 
 struct ReplayConst {
@@ -106,7 +106,8 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           int phase_len = 0);
 constexpr int kQRecBytes = 24;  // replay.cu QRec
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
-constexpr int kHeapShared = 16;  // replay.cu kHS
+// heap entries per lane kept in shared memory by a trace of w warps (replay.cu kHS)
+__host__ __device__ constexpr int replay_heap_prefix(int w) { return w > 4 ? 4 : 16; }
 
 // Seeded streams (rng.cu): up to kMaxDists distributions drawn in order from
 // each stream; out[j] is indexed by the stream offsets.

@@ -72,13 +72,14 @@ constexpr unsigned FULL = 0xffffffffu;
 // Per-lane min-heap of retirement entries: key = departure step << 32 |
 // request (orders retirements as the reference's active list does) and
 // mk = I - k_admit (the quantity whose max gives the cached length).
-// Entries [0, kHS) live in shared memory, the rest in global memory.
-constexpr int kHS = 16;
+// Entries [0, kHS) live in shared memory, the rest in global memory (kHS = 16;
+// 4 for traces of more than 4 warps, whose 256 lanes share a block).
 struct HEnt {
   uint64_t key;
   int64_t mk;
 };
-struct Heap {
+template <int kHS>
+struct HeapT {
   HEnt* s;  // shared part, kHS entries
   HEnt* g;  // global part (entry i >= kHS at g[i - kHS])
   // Generic accessors (heap larger than kHS).  Kept out of line so nvcc
@@ -224,7 +225,8 @@ __device__ __forceinline__ void group_bar(int g, int nthreads) {
 }
 
 template <int W, bool MULTI>
-__global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : HS_REPLAY_MIN_BLOCKS_MULTI)
+__global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
+                                  W == 1 ? HS_REPLAY_MIN_BLOCKS : (W > kWarps ? 1 : HS_REPLAY_MIN_BLOCKS_MULTI))
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
@@ -233,9 +235,12 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? HS_REPLAY_MIN_BLOCKS : H
              const int64_t* __restrict__ trace_heap, int n_max, int max_types, const uint32_t* progress,
              int32_t phase_len, const __grid_constant__ ReplayConst c_one) {
   constexpr int G = W == 1 ? 4 : (W == 2 ? 2 : 1);  // trace groups per block
+  constexpr int kThreads = (W > kWarps ? W : kWarps) * 32;
+  constexpr int kHS = replay_heap_prefix(W);
+  using Heap = HeapT<kHS>;
   __shared__ uint64_t s_tab[256];
-  __shared__ Cold s_cold[kWarps * 32];
-  __shared__ HEnt s_heap[kWarps * 32][kHS];
+  __shared__ Cold s_cold[kThreads];
+  __shared__ HEnt s_heap[kThreads][kHS];
   __shared__ Xch s_x[G][W];
   __shared__ uint32_t s_steps[G];
   extern __shared__ double s_cost[];  // [kWarps][32 * n_types] prices, then [G][n_types] TypeRec
@@ -1027,6 +1032,10 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
     case 2: return multi ? HS_LW(2, true) : HS_LW(2, false);
     case 3: return multi ? HS_LW(3, true) : HS_LW(3, false);
     case 4: return multi ? HS_LW(4, true) : HS_LW(4, false);
+    case 5:
+    case 6: return multi ? HS_LW(6, true) : HS_LW(6, false);  // idle lanes past N
+    case 7:
+    case 8: return multi ? HS_LW(8, true) : HS_LW(8, false);
     default: return cudaErrorInvalidValue;
   }
 #undef HS_LW

@@ -576,3 +576,45 @@ def test_multiwarp_rate_inf_dispatch_phase_vs_oracle(eng, policy):
             for f in ("request_count", "token_count"):
                 assert np.array_equal(res.metrics[f], m[f]), (policy, N, f)
     assert seen & {2, 3}
+
+
+@pytest.mark.parametrize("n_machines", [17, 31])
+def test_wide_deployments_over_128_instances_vs_oracle(eng, n_machines):
+    """Deployments of 136 and 248 instances (6 and 8 warps per trace, four
+    heap entries per lane in shared memory), every policy, finite rate and
+    rate = inf, vs the oracle (the reference has no instance limit;
+    simulator.py:127-158)."""
+    prof = wl.config4()
+    types = list(wl.CONFIG4_TYPES)
+    machines = tuple(hs.MachineSpec(f"m{k}", 8, wl.TYPE_MEM_GB[types[k % 4]] * 1_000_000_000, types[k % 4])
+                     for k in range(n_machines))
+    cluster = hs.ClusterSpec(model=hs.ModelSpec(**prof.model), engine=hs.EngineOverheads(**prof.engine),
+                             machines=machines, limits=hs.WorkloadLimits(**prof.limits))
+    params = {(m.name, t): hs.LatencyParams(*wl.scaled_params(wl.RANK_BASE, t ** -wl.TP_ALPHA *
+                                                               wl.TYPE_SCALE[m.accelerator_type]))
+              for m in machines for t in wl.enumerate_degrees(8)}
+    config = hs.deployment_for(machines, {m.name: 1 for m in machines})
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    handles = build_instances(cluster, config, params)
+    N = len(handles)
+    assert N > 128
+    q, T = 5000, 3
+    Is, Os = zip(*[wl.trace_lengths(q, seed=700 + k) for k in range(T)])
+    I, O = np.concatenate(Is), np.concatenate(Os)
+    off = np.arange(T + 1, dtype=np.int64) * q
+    per_token = hs.kv_bytes_per_token(cluster.model)
+    for policy in ("OS", "RR", "WRR", "SI", "MB"):
+        wrr = tuple(float(1 + k % 3) for k in range(N)) if policy == "WRR" else None
+        pol = hs.PolicyConfig(policy=policy, wrr_weights=wrr)
+        for rate in (600.0, math.inf):
+            A = None if math.isinf(rate) else np.concatenate([wl.arrivals(q, rate, seed=k) for k in range(T)])
+            res = hs.replay_traces(cluster, config, params, pol, off, I, O, O, arrival=A, want_depart=True,
+                                   engine=eng)
+            a, d, m, r = orc.replay(engine_instances(handles, pol), _policy_struct(pol, N, per_token), off, I, O, O,
+                                    A, nthreads=3)
+            assert (res.result["error"] == 0).all() and (r["error"] == 0).all(), (policy, rate)
+            assert np.array_equal(res.assign, a), (policy, rate)
+            assert np.array_equal(res.depart.view(np.uint64), d.view(np.uint64)), (policy, rate)
+            assert np.array_equal(res.result["n_steps"], r["n_steps"]), (policy, rate)
+            for f in ("completion_time", "peak_kv_usage", "residual_load"):
+                assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), (policy, rate, f)
