@@ -349,6 +349,8 @@ def reference_arm(args, rank, world):
     import paper_2504_15303_b200  # noqa: F401 (workloads for the inputs; no engine call)
     P = 5**16
     R = args.traces * args.q
+    if not (REF_DIR / "hetserve" / "__init__.py").exists():
+        return port_reference_arm(args, P, R)  # the reference was not vendored: its C restatement
     tables = reference_tables(args.search_q)
     pool = RefPool(args.rate, args.search_q)
     cores = pool.cores
@@ -375,6 +377,25 @@ def reference_arm(args, rank, world):
                       "requests_per_s": statistics.median(x["requests_per_s"] for x in vals)},
     }
     print(json.dumps(line), flush=True)
+
+
+def port_reference_arm(args, P: int, R: int):
+    """--impl reference without baseline/_ref: the C restatement (kind "port")."""
+    vals = [port_baseline(args.cpu_seconds, P, R, args.q, args.rate) for _ in range(args.warmup + args.steps)]
+    vals = vals[args.warmup:]
+    v = statistics.median(x["value"] for x in vals)
+    last = vals[-1]
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": (P + R) / v * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD.format(traces=args.traces, q=args.q, rate=args.rate), "candidates": P,
+                   "requests": R, "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port", "sample": last["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "breakdown": {"configs_per_s": last["configs_per_s"], "requests_per_s": last["requests_per_s"]},
+        "note": "baseline/_ref absent (python tools/vendor_reference.py): the reference's C restatement instead"}),
+        flush=True)
 
 
 def reference_tables(q_search: int):
@@ -606,7 +627,9 @@ def engine_arm(args, rank, world, local_rank):
         c5 = config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, params)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not (REF_DIR / "hetserve" / "__init__.py").exists():
+        cpu = port_baseline(args.cpu_seconds, P, R_total, args.q, args.rate)  # reference not vendored
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         pool = RefPool(args.rate, args.search_q)
         try:
             cpu = reference_baseline(pool, P, R_total, tables, q_trace=args.q, n_traces=8,
