@@ -302,6 +302,14 @@ int hs_search_rank(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees,
 int hs_search_topk(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees, int32_t n_machines, int64_t k,
                    int32_t shard, int32_t n_shards, hs_cand* out, int64_t* n_out, int64_t* n_feasible);
 
+/* The ranking streamed: the best k feasible candidates ranked AFTER the
+ * candidate (after_total, after_index) in planner.py:227 order (total desc,
+ * index asc) -- repeated calls with the last result as the boundary walk the
+ * whole ranking of any space (hs_search_rank materialises at most 2^26).
+ * after_index < 0: from the top.  *n_feasible = all feasible candidates. */
+int hs_search_topk_after(hs_ctx* ctx, const hs_entry* table, const int32_t* n_degrees, int32_t n_machines, int64_t k,
+                         double after_total, int64_t after_index, hs_cand* out, int64_t* n_out, int64_t* n_feasible);
+
 /* ---- batched scheduler replay ------------------------------------------ */
 /* Replay every trace of the batch on the same instance set.  assign
  * ([total requests], may be NULL) receives the chosen instance per request

@@ -145,7 +145,7 @@ EXPORTS = (
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
     "hs_replay_seeded", "hs_pcg64_seed", "hs_pcg64_seed_u64", "hs_rng_generate",
     "hs_sched_create", "hs_sched_destroy", "hs_sched_evaluate", "hs_sched_choose", "hs_sched_complete",
-    "hs_sched_snapshot", "hs_plan_instance", "hs_sched_get_state", "hs_sched_set_state", "hs_sched_set_instance", "hs_exp_batch",
+    "hs_sched_snapshot", "hs_plan_instance", "hs_sched_get_state", "hs_sched_set_state", "hs_sched_set_instance", "hs_exp_batch", "hs_search_topk_after",
 )
 
 _lib = None
@@ -199,6 +199,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_sched_set_state": ([vp, i32, dbl, i64, i64, i64], C.c_int),
             "hs_sched_set_instance": ([vp, i32, vp], C.c_int),
             "hs_exp_batch": ([vp, vp, i64, vp, vp], C.c_int),
+            "hs_search_topk_after": ([vp, vp, vp, i32, i64, dbl, i64, vp, vp, vp], C.c_int),
             "hs_plan_instance": ([vp, dbl, i64, vp, vp, vp, i64, vp, vp, vp, vp], C.c_int),
             "hs_rng_generate": ([vp, vp, i32, vp, vp, i32, vp, vp], C.c_int),
         }
@@ -416,6 +417,18 @@ class Engine:
         rc = self.lib.hs_search_topk(self.handle, _ptr(t), _ptr(np.ascontiguousarray(nd, np.int32)), len(nd), int(k),
                                      int(shard), int(n_shards), _ptr(out), C.byref(n), C.byref(nf))
         self.check(rc, "hs_search_topk")
+        return out[: n.value], int(nf.value)
+
+    def search_topk_after(self, table: np.ndarray, nd: np.ndarray, k: int, after=None):
+        """hs_search_topk_after: the k best candidates ranked after `after` = (total, index)."""
+        out = np.zeros(max(k, 1), dtype=CAND_DTYPE)
+        n = C.c_int64()
+        nf = C.c_int64()
+        t = np.ascontiguousarray(table.reshape(-1))
+        at, ai = (0.0, -1) if after is None else (float(after[0]), int(after[1]))
+        rc = self.lib.hs_search_topk_after(self.handle, _ptr(t), _ptr(np.ascontiguousarray(nd, np.int32)), len(nd),
+                                           int(k), at, ai, _ptr(out), C.byref(n), C.byref(nf))
+        self.check(rc, "hs_search_topk_after")
         return out[: n.value], int(nf.value)
 
     # ---------------------------------------------------------------- replay

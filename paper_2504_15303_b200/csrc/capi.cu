@@ -757,8 +757,28 @@ int hs_search_rank(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
   return HS_OK;
 }
 
+namespace {
+int search_topk_impl(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t M, int64_t k, int32_t shard,
+                     int32_t n_shards, bool has_after, double after_total, int64_t after_index, hs_cand* out,
+                     int64_t* n_out, int64_t* n_feasible);
+}
+
 int hs_search_topk(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t M, int64_t k, int32_t shard,
                    int32_t n_shards, hs_cand* out, int64_t* n_out, int64_t* n_feasible) {
+  return search_topk_impl(c, table, nd, M, k, shard, n_shards, false, 0.0, -1, out, n_out, n_feasible);
+}
+
+int hs_search_topk_after(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t M, int64_t k,
+                         double after_total, int64_t after_index, hs_cand* out, int64_t* n_out,
+                         int64_t* n_feasible) {
+  return search_topk_impl(c, table, nd, M, k, 0, 1, after_index >= 0, after_total, after_index, out, n_out,
+                          n_feasible);
+}
+
+namespace {
+int search_topk_impl(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t M, int64_t k, int32_t shard,
+                     int32_t n_shards, bool has_after, double after_total, int64_t after_index, hs_cand* out,
+                     int64_t* n_out, int64_t* n_feasible) {
   if (!c || !table || !nd || !out || !n_out || !n_feasible) return fail(HS_ERR_ARG, "null argument");
   if (M < 1 || M > HS_MAX_MACHINES) return fail(HS_ERR_ARG, "n_machines out of range");
   if (k < 0 || n_shards < 1 || shard < 0 || shard >= n_shards) return fail(HS_ERR_ARG, "bad k / shard");
@@ -794,8 +814,16 @@ int hs_search_topk(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t 
   const int64_t ib = items * shard / n_shards, ie = items * (shard + 1) / n_shards;
   const int64_t nf = (ie - ib) * DL;
   *n_feasible = nf;
-  const int64_t K = k < nf ? k : nf;
+  int64_t K = k < nf ? k : nf;
   if (K == 0) return HS_OK;
+  uint64_t bkey = ~0ull;  // no boundary: every key is below it
+  if (has_after) {
+    double x = after_total;
+    if (x == 0.0) x = 0.0;  // -0.0 and 0.0 tie
+    const uint64_t u = (uint64_t)*reinterpret_cast<const int64_t*>(&x);
+    bkey = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+  }
+  const int64_t bidx = has_after ? after_index : -1;
   const int64_t CAP = (int64_t)1 << 20;
   unsigned long long *d_hist, *d_cnt;
   uint64_t *d_key, *d_key2;
@@ -817,11 +845,20 @@ int hs_search_topk(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t 
   for (;; shift -= 12) {
     HS_CUDA(cudaMemsetAsync(d_hist, 0, 4096 * sizeof(unsigned long long), c->stream));
     HS_CUDA(hs::launch_topk_pass(fs, !uploaded, 0, ib, ie, shift, prefix, 0, d_hist, d_cnt, d_key, d_idx, CAP, blocks,
-                                 c->stream));
+                                 c->stream, bkey, bidx));
     uploaded = true;
     c->launches += 1;
     HS_CUDA(cudaMemcpyAsync(h.data(), d_hist, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaStreamSynchronize(c->stream));
+    if (shift == 52 && has_after) {  // candidates after the boundary: fewer than k near the end
+      int64_t left = 0;
+      for (int bb = 0; bb < 4096; ++bb) left += (int64_t)h[bb];
+      if (left < need) need = K = left;
+      if (K == 0) {
+        if ((rc = end_timing(c))) return rc;
+        return HS_OK;
+      }
+    }
     int bsel = -1;
     int64_t cum = 0;
     for (int bb = 4095; bb >= 0; --bb) {
@@ -840,7 +877,7 @@ int hs_search_topk(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t 
   }
   HS_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), c->stream));
   HS_CUDA(hs::launch_topk_pass(fs, false, 1, ib, ie, shift, prefix, thr, d_hist, d_cnt, d_key, d_idx, CAP, blocks,
-                               c->stream));
+                               c->stream, bkey, bidx));
   c->launches += 1;
   unsigned long long got = 0;
   HS_CUDA(cudaMemcpyAsync(&got, d_cnt, sizeof(got), cudaMemcpyDeviceToHost, c->stream));
@@ -876,6 +913,7 @@ int hs_search_topk(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_t 
   *n_out = K;
   return HS_OK;
 }
+}  // namespace
 
 namespace {
 

@@ -90,7 +90,7 @@ cudaError_t launch_search_score(const SpaceDesc& sd, int32_t m_real_offset, int6
 cudaError_t launch_topk_pass(const FeasSpace& fs, bool upload, int mode, int64_t item_begin, int64_t item_end,
                              int shift, uint64_t prefix, uint64_t thr, unsigned long long* d_hist,
                              unsigned long long* d_cnt, uint64_t* d_key, int64_t* d_idx, int64_t cap, int blocks,
-                             cudaStream_t st);
+                             cudaStream_t st, uint64_t bkey = ~0ull, int64_t bidx = -1);
 cudaError_t launch_invert_keys(uint64_t* d_key, int64_t n, cudaStream_t st);
 cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st);
 cudaError_t launch_min_need_2d(const int32_t* d_I, const int32_t* d_O, int64_t rows, int64_t width, int64_t pitch,

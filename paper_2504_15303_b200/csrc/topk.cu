@@ -29,12 +29,15 @@ __device__ __forceinline__ uint64_t key_of(double x) {
 }
 
 // mode 0: histogram of key digit (key >> shift) & 4095 among keys whose bits
-// above shift+12 equal `prefix`; mode 1: collect keys >= thr.
+// above shift+12 equal `prefix`; mode 1: collect keys >= thr.  Only
+// candidates ranked after the boundary (bkey, bidx) take part -- key < bkey,
+// or key == bkey and index > bidx (planner.py:227 order: total desc, index
+// asc) -- so successive calls stream the ranking chunk by chunk.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_topk_pass(int64_t item_begin, int64_t item_end, int64_t chunk, int shift,
                                                    uint64_t prefix, uint64_t thr, unsigned long long* hist,
                                                    unsigned long long* cnt, uint64_t* out_key, int64_t* out_idx,
-                                                   int64_t cap) {
+                                                   int64_t cap, uint64_t bkey, int64_t bidx) {
   __shared__ unsigned int sh[MODE == 0 ? 4096 : 1];
   __shared__ double sC[kMaxM * HS_MAX_DEGREES];
   const int M = c_feas.M;
@@ -73,6 +76,7 @@ __global__ void __launch_bounds__(256) k_topk_pass(int64_t item_begin, int64_t i
     for (; it < it_end; ++it) {
       for (int d = 0; d < DL; ++d) {
         const uint64_t key = key_of(__dadd_rn(s, CL[d]));
+        if (key > bkey || (key == bkey && sidx + (int64_t)origL[d] * strideL <= bidx)) continue;  // not after
         if (MODE == 0) {
           if (shift + 12 >= 64 || (key >> (shift + 12)) == prefix) atomicAdd(&sh[(key >> shift) & 4095u], 1u);
         } else if (key >= thr) {
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(256) k_topk_pass(int64_t item_begin, int64_t i
 cudaError_t launch_topk_pass(const FeasSpace& fs, bool upload, int mode, int64_t item_begin, int64_t item_end,
                              int shift, uint64_t prefix, uint64_t thr, unsigned long long* d_hist,
                              unsigned long long* d_cnt, uint64_t* d_key, int64_t* d_idx, int64_t cap, int blocks,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint64_t bkey, int64_t bidx) {
   cudaError_t e;
   if (upload) {
     e = cudaMemcpyToSymbolAsync(c_feas, &fs, sizeof(FeasSpace), 0, cudaMemcpyHostToDevice, st);
@@ -128,10 +132,10 @@ cudaError_t launch_topk_pass(const FeasSpace& fs, bool upload, int mode, int64_t
   if (chunk < 1) chunk = 1;
   if (mode == 0)
     k_topk_pass<0><<<blocks, threads, 0, st>>>(item_begin, item_end, chunk, shift, prefix, thr, d_hist, d_cnt, d_key,
-                                               d_idx, cap);
+                                               d_idx, cap, bkey, bidx);
   else
     k_topk_pass<1><<<blocks, threads, 0, st>>>(item_begin, item_end, chunk, shift, prefix, thr, d_hist, d_cnt, d_key,
-                                               d_idx, cap);
+                                               d_idx, cap, bkey, bidx);
   return cudaGetLastError();
 }
 

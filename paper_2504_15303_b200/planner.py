@@ -433,3 +433,95 @@ def best_config(tables: SearchTables, index: int) -> ThroughputEstimate:
 def deployment_of(tables: SearchTables, index: int) -> DeploymentConfig:
     """The DeploymentConfig of candidate `index` (itertools.product order)."""
     return _config_for(tables, tables.digits(index))
+
+
+# ------------------------------------------------ streamed ranking / report
+def iter_ranked(tables: SearchTables, chunk: int = 1 << 16, engine=None):
+    """planner.py:227's ranking of a space of any size, streamed best-first
+    in chunks of (total, index) (hs_search_topk_after: each chunk is the top
+    of what ranks after the previous chunk's last candidate).  Only feasible
+    candidates are ranked (planner.py:225-226)."""
+    eng = engine or nat.engine_for()
+    after = None
+    while True:
+        cands, _nf = eng.search_topk_after(tables.entries, tables.n_degrees, chunk, after)
+        if len(cands) == 0:
+            return
+        yield cands
+        after = (float(cands["total"][-1]), int(cands["index"][-1]))
+
+
+def iter_infeasible(tables: SearchTables, chunk: int = 1 << 20):
+    """The infeasible candidates in product order (planner.py:216-226) with the
+    reason search_optimal_config records for each (the first failing
+    machine's exception, planner.py:152-166), in chunks of (indices, first
+    failing machine, its digit) from the per-(machine, degree) statuses."""
+    nd = np.asarray(tables.n_degrees, np.int64)
+    ok = tables.entries["status"] == nat.ENTRY_OK  # [M, HS_MAX_DEGREES]
+    P = tables.space_size
+    M = len(nd)
+    for lo in range(0, P, chunk):
+        idx = np.arange(lo, min(P, lo + chunk), dtype=np.int64)
+        digs = np.empty((len(idx), M), np.int64)
+        x = idx.copy()
+        for m in range(M - 1, -1, -1):
+            digs[:, m] = x % nd[m]
+            x //= nd[m]
+        bad = ~ok[np.arange(M)[None, :], digs]
+        anyb = bad.any(axis=1)
+        first = np.argmax(bad, axis=1)
+        sel = np.nonzero(anyb)[0]
+        if len(sel):
+            yield idx[sel], first[sel], digs[sel, first[sel]]
+
+
+def write_plan_report(tables: SearchTables, out, engine=None, chunk: int = 1 << 16) -> int:
+    """`hetserve plan --out` (cli.py:70-109: one json.dumps(sort_keys=True)
+    line per _plan_records record, ranked then infeasible) streamed from the
+    device ranking, for spaces too large to materialise as a SearchOutcome.
+    `out` is a binary file object; returns the number of records."""
+    import json
+
+    fatal = _fatal_zero_division(tables)
+    if fatal is not None:
+        raise fatal
+    names = tables.names
+    counts = [m.accelerator_count for m in tables.cluster.machines]
+    pm = [[{"machine": names[i], "tp_degree": t, "instance_count": int(tables.entries[i, d]["instance_count"]),
+            "instance_tokens_per_sec": float(tables.entries[i, d]["rate"]),
+            "machine_tokens_per_sec": float(tables.entries[i, d]["contribution"]),
+            "slack_bytes": float(tables.entries[i, d]["slack"])}
+           for d, t in enumerate(tables.degrees[i])] for i in range(len(names))]
+    del counts
+    nd = [int(x) for x in tables.n_degrees]
+
+    def digits_of(idx: int) -> list:
+        o = [0] * len(nd)
+        for i in range(len(nd) - 1, -1, -1):
+            idx, o[i] = divmod(idx, nd[i])
+        return o
+
+    n = 0
+    for cands in iter_ranked(tables, chunk=chunk, engine=engine):
+        lines = []
+        for total, idx in zip(cands["total"].tolist(), cands["index"].tolist()):
+            dg = digits_of(idx)
+            n += 1
+            rec = {"rank": n, "config": {names[i]: tables.degrees[i][d] for i, d in enumerate(dg)},
+                   "system_tokens_per_sec": total, "per_machine": [pm[i][d] for i, d in enumerate(dg)]}
+            lines.append(json.dumps(rec, sort_keys=True))
+        out.write(("\n".join(lines) + "\n").encode())
+    reasons = {}
+    for idx, first, fdig in iter_infeasible(tables):
+        lines = []
+        for c, i, d in zip(idx.tolist(), first.tolist(), fdig.tolist()):
+            key = (i, d)
+            if key not in reasons:
+                reasons[key] = str(_entry_exception(tables.cluster, tables.requests, names[i], tables.degrees[i][d],
+                                                    tables.entries[i, d]))
+            dg = digits_of(c)
+            rec = {"config": {names[k]: tables.degrees[k][x] for k, x in enumerate(dg)}, "infeasible": reasons[key]}
+            lines.append(json.dumps(rec, sort_keys=True))
+            n += 1
+        out.write(("\n".join(lines) + "\n").encode())
+    return n

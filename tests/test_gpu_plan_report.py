@@ -74,3 +74,32 @@ def test_plan_report_bytes_match_reference(ref, which):
     assert text(got).encode() == text(want).encode()
     assert got == want
     assert len(want.ranked) > 0 and (which == "config1" or len(want.infeasible) > 0)
+
+
+def test_streamed_plan_report_equals_materialised_1m_candidates(ref, tmp_path):
+    """The streamed report writer (planner.write_plan_report: device ranking in
+    chunks through hs_search_topk_after, infeasible list in product order) over
+    a 4^10 = 1,048,576-candidate space with many exact ties (identical
+    machines) gives the bytes of the reference's own report writer
+    (cli._plan_records) over the materialised SearchOutcome."""
+    from paper_2504_15303_b200 import planner, refbind
+
+    cli = sys.modules["hetserve.cli"]
+    P = sys.modules["hetserve.planner"]
+    mems = [24, 32, 24, 32, 80, 24, 32, 24, 80, 32]  # repeated machines: exact ties in the ranking
+    prof = wl.ClusterProfile("ties", dict(wl.MODEL_13B), dict(wl.ENGINE), dict(wl.LIMITS),
+                             [(f"m{k}", 8, gb * 1_000_000_000, "v100") for k, gb in enumerate(mems)])
+    for k, (name, count, gb, _a) in enumerate(prof.machines):
+        for t in wl.enumerate_degrees(count):
+            prof.params[(name, t)] = wl.scaled_params(wl.RANK_BASE, t ** -wl.TP_ALPHA * (1.0 + 0.1 * (gb // 10**9 % 7)))
+    cluster, trace, params = _inputs(ref, prof, 16, seed=9)
+    ours = {name: fn for (mod, name), fn in refbind.bindings(ref).items() if mod is P}["search_optimal_config"]
+    outcome = ours(cluster, trace, params)
+    want = ("\n".join(json.dumps(r, sort_keys=True) for r in cli._plan_records(outcome)) + "\n").encode()
+    tables = planner.build_tables(cluster, trace, params)
+    path = tmp_path / "plan.jsonl"
+    with open(path, "wb") as fh:
+        n = planner.write_plan_report(tables, fh, chunk=4096)
+    assert n == outcome.candidates_visited == 4 ** 10
+    assert len(outcome.ranked) > 10_000 and len(outcome.infeasible) > 10_000
+    assert path.read_bytes() == want
