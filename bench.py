@@ -604,7 +604,12 @@ def engine_arm(args, rank, world, local_rank):
     # decided by its non-OK (machine, degree) entry): 1 DADD + 1 compare per
     # feasible candidate of this rank's range
     _t, _i, nfeas_local, _ms = planner.search_best(tables, lo, hi, engine=eng)
-    k2_fp64 = 2.0 * nfeas_local / (k2 / 1e3)
+    if dist:  # the search half's time is its slowest shard's
+        t2 = torch.tensor([k2], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t2, op=tdist.ReduceOp.MAX)
+        k2 = float(t2.item())
+    k2s = max(k2, 1e-6) / 1e3  # (a shard without feasible candidates launches nothing)
+    k2_fp64 = 2.0 * best[2] / k2s
     # K3 against the FP64 pipe with the reference-literal op count of SURVEY
     # section 8(d): OS scoring ~67 FP64 ops per instance per dispatch
     # (divides, floordiv, prefill, decode, exp, min-max) + ~15 per step event
@@ -656,8 +661,8 @@ def engine_arm(args, rank, world, local_rank):
                        "note": "every candidate is decided; K2 sums and compares only the feasible sub-product "
                                "(an infeasible candidate holds a non-OK (machine, degree) entry and cannot win)"},
             "breakdown": {"k1_table_ms": k1, "k2_search_ms": k2, "k3_replay_ms": k3,
-                          "configs_per_s": P / (k2 / 1e3) if world == 1 else (hi - lo) / (k2 / 1e3) * world,
-                          "feasible_scored_per_s": nfeas_local / (k2 / 1e3) * world,
+                          "configs_per_s": P / k2s,
+                          "feasible_scored_per_s": best[2] / k2s,
                           "requests_per_s_kernel": nreq / (k3 / 1e3) * world,
                           "step_events_per_request": n_steps_ev / max(nreq, 1),
                           "best_total": best[0], "best_index": best[1], "n_feasible": best[2],
@@ -667,8 +672,8 @@ def engine_arm(args, rank, world, local_rank):
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "k_replay",
                          "note": "replay is bound by dependent FP64 event chains, not bytes: see roofline_k3_fp64 "
                                  "and DESIGN.md"},
-            "roofline_k2": {"bound": "fp64", "achieved": k2_fp64, "peak": fp64_peak, "unit": "FP64 op/s",
-                            "frac": k2_fp64 / fp64_peak, "kernel": "k_search_best",
+            "roofline_k2": {"bound": "fp64", "achieved": k2_fp64, "peak": fp64_peak * world, "unit": "FP64 op/s",
+                            "frac": k2_fp64 / (fp64_peak * world), "kernel": "k_search_best",
                             "peak_source": "hs_probe_fp64 DADD throughput measured in this run",
                             "note": "2 FP64 ops (the left-to-right add and the compare, SURVEY.md 8d) per FEASIBLE "
                                     "candidate scored; a launch of a few microseconds is bound by launch latency"},
