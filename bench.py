@@ -759,7 +759,7 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
         res = hs.replay_candidates(t, params, top["index"][lo:hi], hs.PolicyConfig(), np.arange(n), off, I, O, O,
                                    engine=eng, want_assign=True)
         assert (res.result["error"] == 0).all()
-        return nf, k1, ms_topk, res.kernel_ms, n, top, res
+        return nf, k1, ms_topk, res.kernel_ms, n, top, res, t, lo, hi
 
     for _ in range(max(1, args.warmup - 1)):
         step()
@@ -769,7 +769,7 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
     kern, walls = [], []
     for _ in range(args.steps):
         w0 = time.perf_counter()
-        nf, k1, ms_topk, ms_rep, n, top, res = step()
+        nf, k1, ms_topk, ms_rep, n, top, res, t, lo, hi = step()
         walls.append((time.perf_counter() - w0) * 1e3)
         kern.append(k1 + ms_topk + ms_rep)
     ms_k = statistics.median(kern)
@@ -781,6 +781,22 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
     units = nf + kk * args.q
     nreq = n * args.q
     steps_per_req = float(res.result["n_steps"].sum()) / max(nreq, 1)
+    # instances per replayed deployment (SURVEY.md 8d's reference-literal FP64 count: N * 67 per
+    # dispatch + 15 per step event)
+    ent = t.entries
+    M = len(t.names)
+    nd_ = np.asarray(t.n_degrees, np.int64)
+    x = np.asarray(top["index"][lo:hi], np.int64).copy()
+    n_inst = np.zeros(len(x), np.int64)
+    for m in range(M - 1, -1, -1):
+        n_inst += ent["instance_count"][m, x % nd_[m]]
+        x //= nd_[m]
+    ops = float(n_inst.mean()) * 67 + 15 * steps_per_req if len(n_inst) else 0.0
+    fp64_peak = eng.probe_fp64()
+    traffic = None
+    pj = ROOT / "profiles" / "k3_config5_ncu.json"
+    if pj.exists():
+        traffic = json.loads(pj.read_text()).get("dram_bytes_per_request", 0.0) * nreq or None
     h2d = 2 * nreq * 4 + (n + 1) * 8
     d2h = nreq + n * res.metrics.shape[1] * nat.METRICS_DTYPE.itemsize + n * nat.RESULT_DTYPE.itemsize
     return {
@@ -793,7 +809,12 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
         "roofline": {"bound": "hbm", "achieved": BYTES_PER_DISPATCH * nreq / (ms_rep / 1e3) / 1e9,
                      "peak": json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6650.0)
                      if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0,
-                     "unit": "GB/s", "kernel": "k_replay (multi-deployment)", "traffic": None},
+                     "unit": "GB/s", "kernel": "k_replay (multi-deployment)", "traffic": traffic,
+                     "traffic_source": "profiles/k3_config5_ncu.json (ncu --set full, DRAM bytes per request)"},
+        "roofline_fp64": {"bound": "fp64", "achieved": ops * nreq / (ms_rep / 1e3), "peak": fp64_peak,
+                          "unit": "FP64 op/s", "frac": ops * nreq / (ms_rep / 1e3) / fp64_peak,
+                          "ops_per_dispatch": ops, "mean_instances": float(n_inst.mean()) if len(n_inst) else 0.0,
+                          "kernel": "k_replay (multi-deployment)"},
         "e2e": {"value": units / (ms_w / 1e3), "unit": UNIT, "ms_per_step": ms_w, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "note": "search_topk + replay_candidates with page-locked host traces (copies inside the call)"},

@@ -234,6 +234,10 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
   for (int j = 0; j < N; ++j)
     for (int k = 0; k < 8; ++k) negative |= inst[j].p[k] < 0.0;
   rc.flags = (pol->flags & HS_REPLAY_ORDER_KEYS) ? (1 | (negative ? 2 : 0)) : 0;
+  bool mono = std::getenv("HS_REPLAY_NO_MONO") == nullptr;  // (diagnostic A/B switch)
+  for (int j = 0; j < N; ++j)
+    for (int k = 4; k < 8; ++k) mono &= inst[j].p[k] >= 0.0;
+  if (mono) rc.flags |= 4;  // replay.cu kMono
   int nt = 0;
   std::vector<double> wts(N);
   for (int j = 0; j < N; ++j) {

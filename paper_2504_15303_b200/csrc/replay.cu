@@ -203,6 +203,7 @@ struct Cold {
 // ReplayConst.flags
 constexpr int32_t kOrderKeys = 1;  // depart = (time, heap key, per-lane sequence) triples
 constexpr int32_t kTrackMax = 2;   // step costs may be negative: every step is an event step
+constexpr int32_t kMono = 4;       // decode coefficients >= 0: a pure run's clock never decreases
 
 // One instance class of the deployment, staged in shared memory once per
 // trace group: lanes read their class by index from shared memory instead of
@@ -561,6 +562,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
         // may not run (extra additions are discarded).
         double c0 = price(cd), c1 = price(__dadd_rn(cd, 1.0)), c2 = price(__dadd_rn(cd, 2.0)),
                c3 = price(__dadd_rn(cd, 3.0));
+        const bool mono = (c_rep.flags & kMono) != 0;
         for (;;) {
 #ifdef HS_TIMERS
           if (lane == __ffs(__activemask()) - 1) tacc[9] += 1;
@@ -573,6 +575,18 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
           const double cd4 = __dadd_rn(cd, 4.0);
           const double n0 = price(cd4), n1 = price(__dadd_rn(cd, 5.0)), n2 = price(__dadd_rn(cd, 6.0)),
                        n3 = price(__dadd_rn(cd, 7.0));
+          // monotone clocks: t4 < lim implies t1, t2, t3 < lim, so one test
+          // admits the whole block; the per-step tests run on the block that exits
+          if (mono && k + 4 < kr && (drain || t4 < lim)) {
+            t_next = t4;
+            cd = cd4;
+            k += 4;
+            c0 = n0;
+            c1 = n1;
+            c2 = n2;
+            c3 = n3;
+            continue;
+          }
           // step i+1 runs iff step i ran, k+i < kr and t_i < lim
           const bool g1 = k + 1 < kr && (t1 < lim || drain);
           const bool g2 = g1 && k + 2 < kr && (t2 < lim || drain);
