@@ -369,8 +369,7 @@ def reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": (P + R) / v * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD.format(traces=args.traces, q=args.q, rate=args.rate),
-                   "candidates": P, "requests": R, "parallelism": f"{cores} host processes"},
+        "config": bench_config(args), "parallelism": f"{cores} host processes",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": last["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "breakdown": {"configs_per_s": statistics.median(x["configs_per_s"] for x in vals),
@@ -389,8 +388,7 @@ def port_reference_arm(args, P: int, R: int):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": (P + R) / v * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD.format(traces=args.traces, q=args.q, rate=args.rate), "candidates": P,
-                   "requests": R, "parallelism": "host threads"},
+        "config": bench_config(args), "parallelism": "host threads",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port", "sample": last["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "breakdown": {"configs_per_s": last["configs_per_s"], "requests_per_s": last["requests_per_s"]},
@@ -417,6 +415,13 @@ def reference_tables(q_search: int):
 
 WORKLOAD = ("config3 search (5^16 candidates, 70B, 10k trace) + config4 replay ({traces} traces x {q} requests, "
             "32 instances, {rate} req/s, OS)")
+
+
+def bench_config(args) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": WORKLOAD.format(traces=args.traces, q=args.q, rate=args.rate), "candidates": 5**16,
+            "requests": args.traces * args.q,
+            "l2": "inputs larger than L2 (replay inputs %.1f GB)" % (args.traces * args.q * 4 * 5 / 1e9)}
 
 
 # ------------------------------------------------------------------ engine
@@ -578,6 +583,7 @@ def engine_arm(args, rank, world, local_rank):
                "d2h_bytes_per_step": int(d2h * world), "ms_per_step": e2e_ms,
                # the two halves of the metric, each through its own public call (rank 0's wall clock)
                "configs_per_s": P / (sc_ms / 1e3), "requests_per_s": R_total / (rc_ms / 1e3),
+               "inputs": "host I/O lengths copied in; arrivals drawn on the device from per-trace seeds",
                "search_call_ms": sc_ms, "replay_call_ms": rc_ms,
                "replay_pipeline_ms": statistics.median(e2e_parts["replay_pipeline_ms"][-args.steps:])}
 
@@ -653,10 +659,7 @@ def engine_arm(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (gen-trace lognormal lengths + Poisson arrivals, numpy PCG64 streams drawn on the GPU)",
-            "config": {"workload": WORKLOAD.format(traces=args.traces, q=args.q, rate=args.rate),
-                       "candidates": P, "requests": R_total, "parallelism": f"shard{world}",
-                       "l2": "inputs larger than L2 (replay inputs %.1f GB)" % (I.nbytes * 5 * world / 1e9),
-                       "e2e_inputs": "host I/O lengths copied in; arrivals drawn on the device from per-trace seeds"},
+            "config": bench_config(args), "parallelism": f"shard{world}",
             "search": {"candidates_visited": P, "feasible_scored": best[2],
                        "note": "every candidate is decided; K2 sums and compares only the feasible sub-product "
                                "(an infeasible candidate holds a non-OK (machine, degree) entry and cannot win)"},
