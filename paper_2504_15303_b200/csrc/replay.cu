@@ -572,40 +572,31 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
           const double t2 = __dadd_rn(t1, c1);
           const double t3 = __dadd_rn(t2, c2);
           const double t4 = __dadd_rn(t3, c3);
-          const double cd4 = __dadd_rn(cd, 4.0);
-          const double n0 = price(cd4), n1 = price(__dadd_rn(cd, 5.0)), n2 = price(__dadd_rn(cd, 6.0)),
-                       n3 = price(__dadd_rn(cd, 7.0));
           // monotone clocks: t4 < lim implies t1, t2, t3 < lim, so one test
-          // admits the whole block; the per-step tests run on the block that exits
-          if (mono && k + 4 < kr && (drain || t4 < lim)) {
+          // admits the whole block; the per-step tests run on the block that
+          // exits.  The next block's prices are computed only once the block
+          // is admitted (the kernel is issue-bound: no prices wasted on exits)
+          const bool all4 = mono ? (k + 4 < kr && (drain || t4 < lim))
+                                 : (k + 4 < kr && (drain || (t1 < lim && t2 < lim && t3 < lim && t4 < lim)));
+          if (all4) {
             t_next = t4;
-            cd = cd4;
+            cd = __dadd_rn(cd, 4.0);
             k += 4;
-            c0 = n0;
-            c1 = n1;
-            c2 = n2;
-            c3 = n3;
+            c0 = price(cd);
+            c1 = price(__dadd_rn(cd, 1.0));
+            c2 = price(__dadd_rn(cd, 2.0));
+            c3 = price(__dadd_rn(cd, 3.0));
             continue;
           }
           // step i+1 runs iff step i ran, k+i < kr and t_i < lim
           const bool g1 = k + 1 < kr && (t1 < lim || drain);
           const bool g2 = g1 && k + 2 < kr && (t2 < lim || drain);
           const bool g3 = g2 && k + 3 < kr && (t3 < lim || drain);
-          const bool g4 = g3 && k + 4 < kr && (t4 < lim || drain);
-          if (!g4) {
-            const uint32_t n = 1u + (uint32_t)g1 + (uint32_t)g2 + (uint32_t)g3;
-            t_next = g3 ? t4 : (g2 ? t3 : (g1 ? t2 : t1));
-            cd = __dadd_rn(cd, (double)n);
-            k += n;
-            break;
-          }
-          t_next = t4;
-          cd = cd4;
-          k += 4;
-          c0 = n0;
-          c1 = n1;
-          c2 = n2;
-          c3 = n3;
+          const uint32_t n = 1u + (uint32_t)g1 + (uint32_t)g2 + (uint32_t)g3;
+          t_next = g3 ? t4 : (g2 ? t3 : (g1 ? t2 : t1));
+          cd = __dadd_rn(cd, (double)n);
+          k += n;
+          break;
         }
         n_steps += k - k0;
       }
