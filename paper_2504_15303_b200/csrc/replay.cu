@@ -881,7 +881,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
           sched = true;
           t_next = ta;
           blocked = false;
-          cold.segmax = -INFINITY;  // a new busy period
+          if (c_rep.flags & kTrackMax) cold.segmax = -INFINITY;  // a new busy period
         }
       }
       if (lane == al) my_assign = (uint8_t)chosen;
