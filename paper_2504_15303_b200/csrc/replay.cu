@@ -44,8 +44,9 @@ namespace hs {
 
 #ifdef HS_TIMERS
 // Diagnostic build only (-DHS_TIMERS): per-warp cycle counts of the replay
-// phases, summed over the launch: [advance, price, evaluate, mapping, commit].
-__device__ unsigned long long g_timers[16];
+// phases, summed over the launch: advance, price, evaluate, event-step parts,
+// pass counters, then min-max (16), commit (17), final drain (18), whole trace (19).
+__device__ unsigned long long g_timers[24];
 // accumulated in registers (tacc[]) and flushed once per lane at kernel end
 #define HS_T0(v) long long v = clock64()
 #define HS_T1(slot, v) \
@@ -341,7 +342,8 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
   uint32_t n_steps = 0;
   int64_t rr_next = 0;
 #ifdef HS_TIMERS
-  unsigned long long tacc[16] = {};
+  unsigned long long tacc[24] = {};
+  const long long t_all0 = clock64();
 #endif
   int32_t t_err = HS_TRACE_OK, t_err_inst = -1;
   int64_t t_err_req = -1;
@@ -843,6 +845,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
         }
       }
 
+      HS_T1(16, tm0);
       HS_T0(tc0);
       // ---- commit (scheduling.py:335-346) and enqueue (simulator.py:323-327)
       if (jj == chosen) {
@@ -885,11 +888,14 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
         }
       }
       if (lane == al) my_assign = (uint8_t)chosen;
+      HS_T1(17, tc0);
 
     }
     if (assign && wsub == 0 && lane < n_in && !failed) assign[o + base + lane] = my_assign;
   }
+  HS_T0(tdr0);
   if (!failed && !is_static && advance(0.0, true)) failed = true;
+  HS_T1(18, tdr0);
   if (!failed && is_static) {
     // run_static (simulator.py:229-247): each instance runs its assigned
     // requests (queue order = trace order) as greedy KV-feasible static
@@ -964,8 +970,9 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
 #ifdef HS_TIMERS
   // warp-level phases (slots 0-2, 6) were timed by every lane: count lane 0;
   // event-step parts (3-5, 7) are per lane
-  for (int sl = 0; sl < 16; ++sl) {
-    const bool warp_slot = sl <= 2 || sl == 6 || sl == 8 || sl == 12;
+  tacc[19] += (unsigned long long)(clock64() - t_all0);
+  for (int sl = 0; sl < 24; ++sl) {
+    const bool warp_slot = sl <= 2 || sl == 6 || sl == 8 || sl == 12 || sl >= 16;
     if (!warp_slot || lane == 0) atomicAdd(&g_timers[sl], tacc[sl]);
   }
 #endif
@@ -1100,9 +1107,9 @@ cudaError_t launch_min_need_2d(const int32_t* d_I, const int32_t* d_O, int64_t r
 // diagnostic export of the timers build (not part of the ABI header)
 extern "C" int hs_debug_timers(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
-  cudaError_t e = cudaMemcpyFromSymbol(out, hs::g_timers, sizeof(unsigned long long) * 16);
+  cudaError_t e = cudaMemcpyFromSymbol(out, hs::g_timers, sizeof(unsigned long long) * 24);
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[24] = {};
     cudaMemcpyToSymbol(hs::g_timers, z, sizeof(z));
   }
   return e == cudaSuccess ? 0 : 1;

@@ -64,7 +64,7 @@ def main():
         if hasattr(eng.lib, "hs_debug_timers"):
             import ctypes
             import numpy as np
-            buf = np.zeros(16, np.uint64)
+            buf = np.zeros(24, np.uint64)
             eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 1)
             eng.replay_device(inst, ps, T, d["off"], d["I"], d["O"], d["O"], d["T"], d["a"], d["m"], d["r"])
             eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 0)
