@@ -222,6 +222,12 @@ struct Xch {
   uint64_t a, b;
   int32_t c, d;
 };
+// Per-instance record of one dispatch (multi-warp traces, OS / MB): the
+// load's order key and load + w.
+struct DispRec {
+  uint64_t lk;
+  double own;
+};
 __device__ __forceinline__ void group_bar(int g, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(nthreads) : "memory");
 }
@@ -244,6 +250,11 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
   __shared__ Cold s_cold[kThreads];
   __shared__ HEnt s_heap[kThreads][kHS];
   __shared__ Xch s_x[G][W];
+  // W > 1, OS / MB: one published record per instance and one flag word per
+  // warp per dispatch, double-buffered by arrival parity, so a dispatch
+  // needs a single group barrier (every warp then reduces all W*32 records)
+  __shared__ DispRec s_disp[W > 1 ? 2 : 1][G][W > 1 ? W * 32 : 1];
+  __shared__ uint4 s_dflag[W > 1 ? 2 : 1][G][W];
   __shared__ uint32_t s_steps[G];
   extern __shared__ double s_cost[];  // [kWarps][32 * n_types] prices, then [G][n_types] TypeRec
   for (int k = threadIdx.x; k < 256; k += blockDim.x) s_tab[k] = kExpTab[k];
@@ -526,9 +537,38 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
     HS_LT1(5, tc0_);
   };
 
+  // The earliest failing step event of the trace group (heap order: time,
+  // then instance); false when no lane failed.
+  auto resolve_step_err = [&]() -> bool {
+    const unsigned eb = __ballot_sync(FULL, valid && lerr);
+    if (W == 1 && !eb) return false;
+    Xch mine{~0ull, 0, -1, -1};
+    if (eb) {
+      const uint64_t tk = (valid && lerr) ? okey(cold.err_t) : ~0ull;
+      const uint64_t mt = warp_min_u64(tk);
+      const int bl = __ffs(__ballot_sync(FULL, tk == mt)) - 1;
+      mine.a = mt;
+      mine.b = (uint64_t)(wsub * 32 + bl);
+      mine.c = __shfl_sync(FULL, cold.err, bl);
+      mine.d = __shfl_sync(FULL, cold.err_req, bl);
+    }
+    Xch all[W];
+    xchg(mine, all);
+    int best = -1;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      if (all[w].c >= 0 && (best < 0 || all[w].a < all[best].a)) best = w;
+    if (best < 0) return false;
+    t_err = all[best].c;
+    t_err_req = all[best].d;
+    t_err_inst = (int32_t)all[best].b;
+    t_err_val = from_okey(all[best].a);  // the failing step's time
+    return true;
+  };
+
   // Advance every lane's steps with t_next < t_limit (strict: steps at an
   // arrival's own time run after it), or every step when draining.
-  auto advance = [&](double t_limit, bool drain) -> bool {
+  auto advance = [&](double t_limit, bool drain, bool defer) -> bool {
     const double lim = drain ? INFINITY : t_limit;
     for (;;) {
       const bool want = valid && sched && (drain || t_next < t_limit) && !lerr;
@@ -607,34 +647,13 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
       HS_T1(6, tpu);
 #endif
     }
-    const unsigned eb = __ballot_sync(FULL, valid && lerr);
-    if (W == 1 && !eb) return false;
-    // the earliest failing step event wins (heap order: time, then instance)
-    Xch mine{~0ull, 0, -1, -1};
-    if (eb) {
-      const uint64_t tk = (valid && lerr) ? okey(cold.err_t) : ~0ull;
-      const uint64_t mt = warp_min_u64(tk);
-      const int bl = __ffs(__ballot_sync(FULL, tk == mt)) - 1;
-      mine.a = mt;
-      mine.b = (uint64_t)(wsub * 32 + bl);
-      mine.c = __shfl_sync(FULL, cold.err, bl);
-      mine.d = __shfl_sync(FULL, cold.err_req, bl);
-    }
-    Xch all[W];
-    xchg(mine, all);
-    int best = -1;
-#pragma unroll
-    for (int w = 0; w < W; ++w)
-      if (all[w].c >= 0 && (best < 0 || all[w].a < all[best].a)) best = w;
-    if (best < 0) return false;
-    t_err = all[best].c;
-    t_err_req = all[best].d;
-    t_err_inst = (int32_t)all[best].b;
-    t_err_val = from_okey(all[best].a);  // the failing step's time
-    return true;
+    // defer: a multi-warp dispatch folds the error check into its exchange
+    return defer ? false : resolve_step_err();
   };
 
   const bool is_static = c_rep.mode == 1;
+  // classes held by this warp's lanes (HS_MAX_CLASSES <= 32)
+  const unsigned warp_classes = __reduce_or_sync(FULL, valid ? 1u << ty : 0u);
   bool failed = false;
   uint8_t my_assign = 0;
   for (int64_t base = 0; base < q && !failed; base += 32) {
@@ -684,19 +703,29 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
     __syncwarp();
     HS_T0(tp0);
     if (policy != HS_POLICY_MB) {
-      for (int pair0 = 0; pair0 < n_in * NT; pair0 += 32) {
-        const int pair = pair0 + lane;
-        const int al = pair / NT, tyk = pair - al * NT;
-        const int srcl = al < 32 ? al : 0;
-        const int64_t Ia = __shfl_sync(FULL, cI, srcl);
-        const int64_t Pa = __shfl_sync(FULL, cP, srcl);
-        if (pair < n_in * NT) {
-          const double fl = py_floordiv(types[tyk].budget, i2d(pt * (Ia + Pa)));
-          int64_t b = (int64_t)fl;
-          if (b < 1) b = 1;
-          const double* ctp = types[tyk].p;
-          const double tot = __dadd_rn(prefill_time(ctp, b, Ia), decode_time(ctp, b, Ia, Pa));
-          cost[pair] = (tot <= 0.0) ? -1.0 : __ddiv_rn(tot, i2d(b));
+      auto price_pair = [&](int tyk, int64_t Ia, int64_t Pa) {
+        const double fl = py_floordiv(types[tyk].budget, i2d(pt * (Ia + Pa)));
+        int64_t b = (int64_t)fl;
+        if (b < 1) b = 1;
+        const double* ctp = types[tyk].p;
+        const double tot = __dadd_rn(prefill_time(ctp, b, Ia), decode_time(ctp, b, Ia, Pa));
+        return (tot <= 0.0) ? -1.0 : __ddiv_rn(tot, i2d(b));
+      };
+      if (W > 1) {
+        // a warp of a multi-warp trace prices only the classes its own
+        // lanes hold: lane = arrival, one pass per class
+        for (unsigned m = warp_classes; m; m &= m - 1) {
+          const int tyk = __ffs(m) - 1;
+          if (lane < n_in) cost[lane * NT + tyk] = price_pair(tyk, cI, cP);
+        }
+      } else {
+        for (int pair0 = 0; pair0 < n_in * NT; pair0 += 32) {
+          const int pair = pair0 + lane;
+          const int al = pair / NT, tyk = pair - al * NT;
+          const int srcl = al < 32 ? al : 0;
+          const int64_t Ia = __shfl_sync(FULL, cI, srcl);
+          const int64_t Pa = __shfl_sync(FULL, cP, srcl);
+          if (pair < n_in * NT) cost[pair] = price_pair(tyk, Ia, Pa);
         }
       }
       __syncwarp();
@@ -706,7 +735,10 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
       const int64_t a = base + al;
       const double ta = shfl_d(cT, al);
       HS_T0(ta0);
-      if (!is_static && advance(ta, false)) {
+      const bool eval_all = policy == HS_POLICY_OS || policy == HS_POLICY_MB;
+      // multi-warp OS / MB: the step-error check joins the dispatch's exchange
+      const bool fused = W > 1 && eval_all;
+      if (!is_static && advance(ta, false, fused)) {
         failed = true;
         break;
       }
@@ -717,7 +749,6 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
       const int64_t Pa = __shfl_sync(FULL, cP, al);
       // ---- choose (scheduling.py:235-254)
       int chosen = -1;
-      const bool eval_all = policy == HS_POLICY_OS || policy == HS_POLICY_MB;
       if (!eval_all) {
         if (policy == HS_POLICY_SI) {
           chosen = 0;
@@ -763,7 +794,31 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
       HS_T0(tm0);
       const unsigned errb = __ballot_sync(FULL, need && (cerr || eerr));
       bool any_err = errb != 0;
-      if (W > 1) {
+      const DispRec* drec = nullptr;
+      if (fused) {
+        // publish (load key, load + w) and the warp's error / candidate
+        // masks; one barrier; every warp then sees the whole group
+        const int buf = (int)(a & 1);
+        const unsigned preb = __ballot_sync(FULL, need && !isinf(w));
+        const unsigned stepb = __ballot_sync(FULL, valid && lerr);
+        s_disp[buf][g][jj] = DispRec{valid ? okey(load) : 0ull, __dadd_rn(load, w)};
+        if (lane == 0) s_dflag[buf][g][wsub] = make_uint4(errb, stepb, preb, 0u);
+        group_bar(g, W * 32);
+        drec = s_disp[buf][g];
+        unsigned any_e = 0, any_s = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < W; ++w2) {
+          const uint4 f = s_dflag[buf][g][w2];
+          any_e |= f.x;
+          any_s |= f.y;
+        }
+        if (any_s) {  // a step before this arrival failed: that error wins
+          resolve_step_err();
+          failed = true;
+          break;
+        }
+        any_err = any_e != 0;
+      } else if (W > 1) {
         Xch all[W];
         xchg(Xch{0, 0, errb ? 1 : 0, 0}, all);
         any_err = false;
@@ -803,6 +858,42 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
         // rounding is monotone, L_s + w_s >= L_s, so the max over j != s may
         // include s itself: peak_s = max(L_s + w_s, max_j L_j) -- one max
         // reduction instead of the top-2 of the loads.
+        if (fused) {
+          // the whole group's reduction from the published records, in
+          // every warp: max load, then the lowest instance of minimum peak
+          uint64_t lm = 0;
+#pragma unroll
+          for (int w2 = 0; w2 < W; ++w2) {
+            const uint64_t lk = drec[w2 * 32 + lane].lk;
+            lm = lk > lm ? lk : lm;
+          }
+          const uint64_t m1 = warp_max_u64(lm);
+          const double top = from_okey(m1);
+          uint64_t pk[W];
+          uint64_t pmin = ~0ull;
+#pragma unroll
+          for (int w2 = 0; w2 < W; ++w2) {
+            const double own = drec[w2 * 32 + lane].own;
+            const double peak = own > top ? own : top;
+            const bool cand = ((s_dflag[a & 1][g][w2].z >> lane) & 1u) && peak < INFINITY;
+            pk[w2] = cand ? okey(peak) : ~0ull;
+            pmin = pk[w2] < pmin ? pk[w2] : pmin;
+          }
+          const uint64_t mp = warp_min_u64(pmin);
+          unsigned my_idx = 0xffffffffu;
+#pragma unroll
+          for (int w2 = W - 1; w2 >= 0; --w2)
+            if (pk[w2] != ~0ull && pk[w2] == mp) my_idx = (unsigned)(w2 * 32 + lane);
+          const unsigned ci = __reduce_min_sync(FULL, my_idx);
+          if (ci == 0xffffffffu) {
+            t_err = HS_TRACE_NO_INSTANCE;
+            t_err_req = a;
+            t_err_inst = -1;
+            failed = true;
+            break;
+          }
+          chosen = (int)ci;
+        } else {
         uint64_t m1 = warp_max_u64(valid ? okey(load) : 0ull);
         if (W > 1) {
           Xch all[W];
@@ -842,6 +933,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
             break;
           }
           chosen = (int)all[bw].b;
+        }
         }
       }
 
@@ -894,7 +986,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
     if (assign && wsub == 0 && lane < n_in && !failed) assign[o + base + lane] = my_assign;
   }
   HS_T0(tdr0);
-  if (!failed && !is_static && advance(0.0, true)) failed = true;
+  if (!failed && !is_static && advance(0.0, true, false)) failed = true;
   HS_T1(18, tdr0);
   if (!failed && is_static) {
     // run_static (simulator.py:229-247): each instance runs its assigned

@@ -33,10 +33,14 @@ def ref():
     sys.path.remove(str(REF))
 
 
-def _scenario(ref, rng: random.Random, case: int):
-    n_mach = rng.randint(1, 3)
-    machines = tuple(ref.MachineSpec(f"m{i}", rng.choice([1, 2, 4]), rng.choice([200_000, 400_000, 900_000]),
-                                     "t") for i in range(n_mach))
+def _scenario(ref, rng: random.Random, case: int, wide: bool = False):
+    # wide: 5-12 machines of 4 or 8 GPUs, so deployments of 33-96 instances
+    # (2-3 warps per trace) exercise the multi-warp dispatch and its errors
+    n_mach = rng.randint(5, 12) if wide else rng.randint(1, 3)
+    # wide: small memories too (6,000 B holds ~180 tokens: instances fill up)
+    mems = [6_000, 20_000, 200_000] if wide else [200_000, 400_000, 900_000]
+    machines = tuple(ref.MachineSpec(f"m{i}", rng.choice([4, 8] if wide else [1, 2, 4]), rng.choice(mems), "t")
+                     for i in range(n_mach))
     model = ref.ModelSpec(layers=2, hidden_dim=4, param_count=100, bytes_per_param=2)  # 32 B/token
     cluster = ref.ClusterSpec(model=model, engine=ref.EngineOverheads(1.0, 0), machines=machines,
                               limits=ref.WorkloadLimits(max_input_len=64, max_output_len=64))
@@ -48,10 +52,13 @@ def _scenario(ref, rng: random.Random, case: int):
                  rng.uniform(1e-7, 1e-5), rng.uniform(1e-5, 1e-3), rng.uniform(1e-7, 1e-5), rng.uniform(1e-4, 1e-3)]
             if kind == 1:  # negative decode terms: step costs can go negative
                 p[7] = -rng.uniform(1e-3, 2e-2)  # short steps of small batches cost < 0
+                if wide and rng.random() < 0.3:  # per-request costs <= 0 for some classes
+                    p[1], p[7] = 0.0, -rng.uniform(0.05, 0.5)
             elif kind == 2:  # constant-only prefill, zero decode: many steps at one time
                 p = [0.0, rng.choice([1.0, 0.5]), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0]
             params[(m.name, t)] = ref.LatencyParams(*p)
-    degrees = {m.name: rng.choice(ref.enumerate_tp_degrees(m)) for m in machines}
+    degrees = {m.name: (1 if wide and rng.random() < 0.7 else rng.choice(ref.enumerate_tp_degrees(m)))
+               for m in machines}
     config = ref.deployment_for(machines, degrees)
     q = rng.randint(20, 250)
     ids = [f"r{k}" for k in range(q)]
@@ -64,7 +71,9 @@ def _scenario(ref, rng: random.Random, case: int):
     policy_name = rng.choice(["OS", "OS", "RR", "WRR", "SI", "MB"])
     n_inst = sum(p.instance_count for p in config.per_machine)
     wrr = tuple(float(rng.randint(1, 4)) for _ in range(n_inst)) if policy_name == "WRR" else None
-    policy = ref.PolicyConfig(policy=policy_name, theta=rng.choice([0.5, 2.0]), wrr_weights=wrr)
+    # theta 2000: exp(theta * usage) overflows once an instance is ~36 % full
+    policy = ref.PolicyConfig(policy=policy_name, theta=rng.choice([0.5, 2.0, 2000.0] if wide else [0.5, 2.0]),
+                              wrr_weights=wrr)
     mode = "static" if rng.random() < 0.2 else "continuous"
     rate = math.inf if (mode == "static" or rng.random() < 0.3) else rng.choice([5.0, 40.0, 400.0])
     return ref.simulator.Scenario(cluster=cluster, config=config, trace=trace, arrival_rate=rate, policy=policy,
@@ -98,6 +107,34 @@ def test_fuzzed_scenarios_match_live_reference(ref):
         n_err += want[0] == "err"
         n_neg += case % 4 == 1 and want[0] == "ok"
     assert n_dup > 40 and n_err > 10 and n_neg > 20, (n_dup, n_err, n_neg)
+
+
+def test_fuzzed_wide_scenarios_match_live_reference(ref):
+    """As above on deployments of 33-96 instances (multi-warp traces: the
+    fused one-barrier OS / MB dispatch, the exchanged SI / RR / WRR choice,
+    and their error paths)."""
+    from paper_2504_15303_b200 import refbind
+
+    binding = refbind.bindings(ref)
+    S = sys.modules["hetserve.simulator"]
+    ours = {name: fn for (mod, name), fn in binding.items() if mod is S}
+    n_err = n_wide = 0
+    kinds = set()
+    for case in range(1000, 1160):
+        rng = random.Random(case)
+        sc = _scenario(ref, rng, case, wide=True)
+        n_inst = sum(p.instance_count for p in sc.config.per_machine)
+        run_ref = S.run_static if sc.mode == "static" else S.run_continuous
+        run_gpu = ours["run_static"] if sc.mode == "static" else ours["run_continuous"]
+        want = _outcome(run_ref, sc)
+        got = _outcome(run_gpu, sc)
+        assert got == want, (case, n_inst, sc.mode, sc.policy.policy, sc.arrival_rate,
+                             want[1] if want[0] == "err" else "", got[1] if got[0] == "err" else "")
+        n_wide += n_inst > 32
+        if want[0] == "err":
+            n_err += 1
+            kinds.add(want[1][0])
+    assert n_wide > 100 and n_err > 10, (n_wide, n_err, kinds)
 
 
 def test_run_policy_comparison_matches_live_reference(ref):
