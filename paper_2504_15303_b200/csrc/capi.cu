@@ -267,7 +267,28 @@ int make_const(const hs_instance* inst, const hs_policy* pol, bool has_arrival, 
 // floor(budget / (per_token * min(I+O))) requests fit an instance at once.
 // n_max: the widest deployment of the launch (it picks the kernel's warps per
 // trace, hence how many heap entries per lane live in shared memory).
-void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q, int n_max = 0) {
+//
+// Multi-warp traces whose launch knows every output length (max_out >= 0)
+// get a retirement calendar instead: 2^cal_bits buckets (> max O, so the
+// active retirement steps never share a bucket) of 8 B plus the bucket
+// bitmap, per instance, whatever the active-set bound.
+int cal_bits_for(int n_max, int32_t max_out) {
+  if ((n_max + 31) / 32 < 2 || max_out < 0) return 0;
+  int b = 6;
+  while (b <= hs::kMaxCalBits && (1 << b) <= max_out) ++b;  // 2^b > max(O, 1)
+  return b <= hs::kMaxCalBits ? b : 0;
+}
+
+void size_heaps(hs::ReplayConst& rc, const hs_instance* inst, int32_t min_need, int64_t max_q, int n_max = 0,
+                int cal_bits = 0) {
+  rc.cal_bits = cal_bits;
+  if (cal_bits > 0) {
+    const int64_t B = int64_t(1) << cal_bits;
+    const int64_t per = (B * 8 + (B / 64) * 8 + hs::kHEntBytes - 1) / hs::kHEntBytes;  // in heap entries
+    for (int j = 0; j <= rc.N; ++j) rc.heap_off[j] = j * per;
+    rc.heap_stride = (rc.N * per + 15) / 16 * 16;
+    return;
+  }
   const int shared = hs::replay_heap_prefix(((n_max > 0 ? n_max : rc.N) + 31) / 32);
   if (min_need < 1) min_need = 1;
   int64_t acc = 0;
@@ -308,16 +329,18 @@ int replay_impl(hs_ctx* c, const hs_instance* inst, const hs_policy* pol, int64_
   if ((rcode = check_offsets(h_off, T, &max_q))) return rcode;
   const int64_t total_q = h_off[T] - h_off[0];
   int32_t* d_min = nullptr;
-  if ((rcode = ensure_t(c, S_MINNEED, 1, &d_min))) return rcode;
+  if ((rcode = ensure_t(c, S_MINNEED, 2, &d_min))) return rcode;
   HS_CUDA(cudaMemsetAsync(d_min, 0x7f, sizeof(int32_t), c->stream));
+  HS_CUDA(cudaMemsetAsync(d_min + 1, 0, sizeof(int32_t), c->stream));
   if (total_q > 0) {
-    HS_CUDA(hs::launch_min_need(d_I + h_off[0], d_O + h_off[0], total_q, d_min, c->stream));
+    HS_CUDA(hs::launch_min_need(d_I + h_off[0], d_O + h_off[0], total_q, d_min, c->stream, d_min + 1));
     c->launches += 1;
   }
-  int32_t min_need = 0;
-  HS_CUDA(cudaMemcpyAsync(&min_need, d_min, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  int32_t need_stats[2] = {0, 0};  // min(I + O), max(O)
+  HS_CUDA(cudaMemcpyAsync(need_stats, d_min, sizeof(need_stats), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  size_heaps(rc, inst, min_need, max_q);
+  const int32_t min_need = need_stats[0];
+  size_heaps(rc, inst, min_need, max_q, 0, cal_bits_for(rc.N, need_stats[1]));
   void* d_qrec;
   if ((rcode = ensure(c, S_WREC, (size_t)(h_off[T] > 0 ? h_off[T] : 1) * hs::kQRecBytes, &d_qrec))) return rcode;
   const size_t per_trace = (size_t)rc.heap_stride * hs::kHEntBytes;
@@ -1378,7 +1401,7 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
       (rc = ensure_t(c, S_RESULT, (size_t)(T > 0 ? T : 1), &dR)) || (rc = ensure(c, S_WREC, tq * hs::kQRecBytes, &dQ)) ||
       (rc = ensure(c, S_DEPS, sizeof(hs::ReplayConst) * n_dep, &dDeps)) ||
       (rc = ensure_t(c, S_TDEP, (size_t)(T > 0 ? T : 1), &dTD)) ||
-      (rc = ensure_t(c, S_THEAP, (size_t)(T > 0 ? T : 1), &dTH)) || (rc = ensure_t(c, S_MINNEED, 1, &dMin)))
+      (rc = ensure_t(c, S_THEAP, (size_t)(T > 0 ? T : 1), &dTH)) || (rc = ensure_t(c, S_MINNEED, 2, &dMin)))
     return rc;
   if (b->arrival && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
   if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
@@ -1394,14 +1417,18 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
     if (dT) HS_CUDA(cudaMemcpyAsync(dT, b->arrival, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
   }
   HS_CUDA(cudaMemsetAsync(dMin, 0x7f, sizeof(int32_t), c->stream));
+  HS_CUDA(cudaMemsetAsync(dMin + 1, 0, sizeof(int32_t), c->stream));
   if (total > 0) {
-    HS_CUDA(hs::launch_min_need(dI, dO, total, dMin, c->stream));
+    HS_CUDA(hs::launch_min_need(dI, dO, total, dMin, c->stream, dMin + 1));
     c->launches += 1;
   }
-  int32_t min_need = 0;
-  HS_CUDA(cudaMemcpyAsync(&min_need, dMin, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  int32_t need_stats[2] = {0, 0};  // min(I + O), max(O)
+  HS_CUDA(cudaMemcpyAsync(need_stats, dMin, sizeof(need_stats), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  for (int32_t d = 0; d < n_dep; ++d) size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q, n_max);
+  const int32_t min_need = need_stats[0];
+  const int cal_bits = cal_bits_for(n_max, need_stats[1]);
+  for (int32_t d = 0; d < n_dep; ++d)
+    size_heaps(deps[d], instances + inst_offsets[d], min_need, max_q, n_max, cal_bits);
   std::vector<int64_t> theap((size_t)(T > 0 ? T : 1));
   int64_t hacc = 0;
   for (int64_t t = 0; t < T; ++t) {

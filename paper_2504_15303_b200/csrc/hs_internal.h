@@ -57,6 +57,7 @@ struct ReplayConst {
   int32_t has_arrival;
   int32_t mode;  // 0 continuous (simulator.py:272), 1 static (simulator.py:206)
   int32_t flags;  // replay.cu kOrderKeys | kTrackMax
+  int32_t cal_bits;  // > 0: multi-warp traces keep retirements in a calendar of 2^cal_bits steps
   double theta;
   int64_t per_token;
   double wrr_total;
@@ -92,7 +93,9 @@ cudaError_t launch_topk_pass(const FeasSpace& fs, bool upload, int mode, int64_t
                              unsigned long long* d_cnt, uint64_t* d_key, int64_t* d_idx, int64_t cap, int blocks,
                              cudaStream_t st, uint64_t bkey = ~0ull, int64_t bidx = -1);
 cudaError_t launch_invert_keys(uint64_t* d_key, int64_t n, cudaStream_t st);
-cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st);
+// d_out: min(I + O); d_max_out (optional): max(O)
+cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st,
+                            int32_t* d_max_out = nullptr);
 cudaError_t launch_min_need_2d(const int32_t* d_I, const int32_t* d_O, int64_t rows, int64_t width, int64_t pitch,
                                int32_t* d_out, cudaStream_t st);
 // deps / trace_dep / trace_heap: per-trace deployments (config 5); when
@@ -105,6 +108,10 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           int n_max = 0, int max_types = 0, const uint32_t* d_progress = nullptr,
                           int phase_len = 0);
 constexpr int kQRecBytes = 24;  // replay.cu QRec
+// retirement calendar (multi-warp traces): 2^cal_bits buckets, cal_bits <= kMaxCalBits
+// (the summary bitmap is kCalSumWords 64-bit words per lane)
+constexpr int kMaxCalBits = 14;
+constexpr int kCalSumWords = 1 << (kMaxCalBits - 12);
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
 // heap entries per lane kept in shared memory by a trace of w warps (replay.cu kHS)
 __host__ __device__ constexpr int replay_heap_prefix(int w) { return w > 4 ? 4 : 16; }

@@ -232,7 +232,7 @@ __device__ __forceinline__ void group_bar(int g, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(nthreads) : "memory");
 }
 
-template <int W, bool MULTI>
+template <int W, bool MULTI, bool CAL>
 __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
                                   W == 1 ? HS_REPLAY_MIN_BLOCKS : (W > kWarps ? 1 : HS_REPLAY_MIN_BLOCKS_MULTI))
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
@@ -248,6 +248,8 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
   using Heap = HeapT<kHS>;
   __shared__ uint64_t s_tab[256];
   __shared__ Cold s_cold[kThreads];
+  // CAL: per-lane summary of the calendar's bucket bitmap (bit i: word i non-empty)
+  __shared__ uint64_t s_csum[CAL ? kThreads : 1][kCalSumWords];
   __shared__ HEnt s_heap[kThreads][kHS];
   __shared__ Xch s_x[G][W];
   // W > 1, OS / MB: one published record per instance and one flag word per
@@ -326,6 +328,24 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
   const Heap heap{s_heap[threadIdx.x], reinterpret_cast<HEnt*>(heap_all) + hbase + c_rep.heap_off[j]};
   const int64_t cap_tok = trec.cap_tok;  // floor(floor(budget) / per_token)
   const int32_t cap = (int32_t)(c_rep.heap_off[j + 1] - c_rep.heap_off[j]) + kHS;
+  // CAL: the retirement calendar replaces the heap -- a ring of B = 2^cal_bits
+  // buckets indexed by retirement step (B > every output length, so the
+  // active steps (k, k + max O] never collide), each a list of requests in
+  // admission order (= request order, the heap's tie-break) linked through
+  // the retired queue records (QRec.next; QRec.nI holds I - k_admit), plus a
+  // two-level bitmap of non-empty buckets: words in global memory after the
+  // buckets, their summary in shared memory.
+  const uint32_t cmask = CAL ? (1u << c_rep.cal_bits) - 1u : 0u;
+  int2* const cal = reinterpret_cast<int2*>(reinterpret_cast<HEnt*>(heap_all) + hbase + c_rep.heap_off[j]);
+  uint64_t* const csum = s_csum[CAL ? threadIdx.x : 0];
+  int32_t topnext = -1;  // CAL: the next request of the top bucket's list
+  if (CAL) {
+    uint64_t* cb = reinterpret_cast<uint64_t*>(cal + cmask + 1);
+    if (valid)
+      for (uint32_t i = 0; i <= (cmask >> 6); ++i) cb[i] = 0ull;
+#pragma unroll
+    for (int i = 0; i < kCalSumWords; ++i) csum[i] = 0ull;
+  }
 
   // hot per-lane state (registers)
   double load = 0.0, ex = 1.0;
@@ -376,6 +396,51 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
 #define HS_LT0(v)
 #define HS_LT1(slot, v)
 #endif
+  // ---- CAL helpers
+  // the head of a bucket (retirement step s_) becomes the top: its payload
+  auto cal_set_top = [&](uint32_t s_, int32_t r2) {
+    topkey = ((uint64_t)s_ << 32) | (uint32_t)r2;
+    topI = I[r2];
+    topO = O[r2];
+    const QRec q2 = R[r2];
+    topP = q2.P;
+    topW = q2.W;
+    topnext = q2.next;
+  };
+  // bucket of step s_ emptied: clear its bit; returns the bitmap word
+  auto cal_clear = [&](uint32_t s_) -> uint64_t {
+    uint64_t* cb = reinterpret_cast<uint64_t*>(cal + cmask + 1);
+    const uint32_t b = s_ & cmask, wi = b >> 6;
+    const uint64_t w = cb[wi] & ~(1ull << (b & 63));
+    cb[wi] = w;
+    if (!w) csum[wi >> 6] &= ~(1ull << (wi & 63));
+    return w;
+  };
+  // the first non-empty bucket at or after step p, circularly (every active
+  // step lies in [p, p + B)); w0 = the bitmap word holding p's bucket
+  auto cal_next = [&](uint32_t p, uint64_t w0) {
+    const uint64_t* cb = reinterpret_cast<const uint64_t*>(cal + cmask + 1);
+    const uint32_t b0 = p & cmask, wi0 = b0 >> 6;
+    uint64_t w = w0 & (~0ull << (b0 & 63));
+    uint32_t wi = wi0;
+    if (!w) {
+      // summary bits after wi0, then around to wi0 itself (its bits below b0)
+      const uint32_t ns = (((cmask >> 6) + 1) + 63) >> 6;
+      const uint32_t s0 = wi0 >> 6, bw = wi0 & 63;
+      wi = 0xffffffffu;
+      for (uint32_t t = 0; t <= ns && wi == 0xffffffffu; ++t) {
+        const uint32_t si = (s0 + t) & (ns - 1);  // ns is a power of two
+        uint64_t m = csum[si];
+        if (t == 0) m &= bw == 63 ? 0ull : (~0ull << (bw + 1));
+        else if (t == ns) m &= bw == 63 ? ~0ull : ((2ull << bw) - 1ull);
+        if (m) wi = si * 64 + (uint32_t)(__ffsll((long long)m) - 1);
+      }
+      w = cb[wi];
+    }
+    const uint32_t b = (wi << 6) + (uint32_t)(__ffsll((long long)w) - 1);
+    cal_set_top(p + ((b - b0) & cmask), cal[b].x);
+  };
+
   auto event_step = [&]() {
     const double t = t_next;
     sched = false;
@@ -397,14 +462,28 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
       const int32_t r = (int32_t)(topkey & 0xffffffffu);
       const int64_t Ir = topI, Or = topO, Pr = topP;
       const double wr = topW;
-      heap.pop(nact);
-      if (nact > 0) {
-        topkey = heap.s[0].key;  // the root always lives in shared memory
-        const int32_t r2 = (int32_t)(topkey & 0xffffffffu);
-        topI = I[r2];
-        topO = O[r2];
-        topP = R[r2].P;
-        topW = R[r2].W;
+      if (CAL) {
+        --nact;
+        if (topnext >= 0) {  // the bucket's list goes on (same step)
+          cal_set_top(k, topnext);
+        } else {
+          const uint64_t wk = cal_clear(k);
+          if (nact > 0) {
+            const uint32_t p = k + 1;
+            const uint32_t wp = (p & cmask) >> 6;
+            cal_next(p, wp == ((k & cmask) >> 6) ? wk : reinterpret_cast<const uint64_t*>(cal + cmask + 1)[wp]);
+          }
+        }
+      } else {
+        heap.pop(nact);
+        if (nact > 0) {
+          topkey = heap.s[0].key;  // the root always lives in shared memory
+          const int32_t r2 = (int32_t)(topkey & 0xffffffffu);
+          topI = I[r2];
+          topO = O[r2];
+          topP = R[r2].P;
+          topW = R[r2].W;
+        }
       }
       reserved -= Ir + Or;
       cold.completion = t;
@@ -448,7 +527,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
         }
         break;
       }
-      if (nact >= cap || k > 0x7fffffffu) {
+      if ((!CAL && nact >= cap) || k > 0x7fffffffu) {
         set_err(HS_TRACE_CAPACITY, qhead, t);
         return;
       }
@@ -471,16 +550,39 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
       reserved += need;
       if (Ir > max_i_new) max_i_new = Ir;
       ++newly;
-      const uint64_t key = ((uint64_t)(k + (uint32_t)(Or > 1 ? Or : 1)) << 32) | (uint32_t)r;
+      const uint32_t sstep = k + (uint32_t)(Or > 1 ? Or : 1);
+      const uint64_t key = ((uint64_t)sstep << 32) | (uint32_t)r;
       if (nact == 0 || key < topkey) {
         topkey = key;
         topI = (int32_t)Ir;
         topO = (int32_t)Or;
         topP = (int32_t)Pr;
         topW = wr;
+        topnext = -1;
       }
       const int64_t mk = Ir - (int64_t)k;
-      heap.push(nact, HEnt{key, mk});
+      if (CAL) {
+        // append r to bucket sstep: its queue record becomes the list node
+        uint64_t* cb = reinterpret_cast<uint64_t*>(cal + cmask + 1);
+        const uint32_t b = sstep & cmask, wi = b >> 6;
+        const uint64_t bit = 1ull << (b & 63);
+        const uint64_t w = cb[wi];
+        R[r].next = -1;
+        R[r].nI = (int32_t)mk;
+        if (w & bit) {
+          const int32_t tl = cal[b].y;
+          R[tl].next = r;
+          cal[b].y = r;
+          if (tl == (int32_t)(uint32_t)topkey) topnext = r;  // appended right behind the top
+        } else {
+          cal[b] = make_int2(r, r);
+          cb[wi] = w | bit;
+          csum[wi >> 6] |= 1ull << (wi & 63);
+        }
+        ++nact;
+      } else {
+        heap.push(nact, HEnt{key, mk});
+      }
       if (mk > cur_max) {
         cur_max = mk;
         cold.cnt_max = 1;
@@ -509,14 +611,32 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
       tacc[10] += 1;
       tacc[11] += nact;
 #endif
-      for (int32_t h = 0; h < nact; ++h) {
-        const int64_t mk = heap.get(h, nact).mk;
+      auto count = [&](int64_t mk) {
         if (mk > m) {
           m = mk;
           cm = 1;
         } else if (mk == m) {
           ++cm;
         }
+      };
+      if (CAL) {  // every active request: the non-empty buckets' lists
+        const uint64_t* cb = reinterpret_cast<const uint64_t*>(cal + cmask + 1);
+        const uint32_t ns = (((cmask >> 6) + 1) + 63) >> 6;
+        for (uint32_t si = 0; si < ns; ++si) {
+          for (uint64_t sm = csum[si]; sm; sm &= sm - 1) {
+            const uint32_t wi = si * 64 + (uint32_t)(__ffsll((long long)sm) - 1);
+            for (uint64_t w = cb[wi]; w; w &= w - 1) {
+              const uint32_t b = (wi << 6) + (uint32_t)(__ffsll((long long)w) - 1);
+              for (int32_t rr = cal[b].x; rr >= 0;) {
+                const QRec qq = R[rr];
+                count(qq.nI);
+                rr = qq.next;
+              }
+            }
+          }
+        }
+      } else {
+        for (int32_t h = 0; h < nact; ++h) count(heap.get(h, nact).mk);
       }
       cur_max = m;
       cold.cnt_max = cm;
@@ -780,6 +900,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
           cst = cost[al * NT + ty];
           cerr = cst < 0.0;
         }
+        HS_T0(tx0);
         if (dirty) {  // capacity.py:98-106 kv_usage, scheduling.py:154 exp
           const double usage = __ddiv_rn(i2d(pt * (run_i + run_p)), budget);
           bool of;
@@ -789,6 +910,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
         }
         eerr = ex_over;
         w = __dmul_rn(cst, ex);
+        HS_T1(21, tx0);
       }
       HS_T1(2, te0);
       HS_T0(tm0);
@@ -803,7 +925,9 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
         const unsigned stepb = __ballot_sync(FULL, valid && lerr);
         s_disp[buf][g][jj] = DispRec{valid ? okey(load) : 0ull, __dadd_rn(load, w)};
         if (lane == 0) s_dflag[buf][g][wsub] = make_uint4(errb, stepb, preb, 0u);
+        HS_T0(tb0);
         group_bar(g, W * 32);
+        HS_T1(20, tb0);
         drec = s_disp[buf][g];
         unsigned any_e = 0, any_s = 0;
 #pragma unroll
@@ -1096,7 +1220,7 @@ __global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
   }
 }
 
-template <int W, bool MULTI>
+template <int W, bool MULTI, bool CAL>
 cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                      const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign, double* d_depart,
                      hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec, uint64_t* d_heap,
@@ -1108,10 +1232,10 @@ cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
   const size_t smem = (size_t)warps * 32 * max_types * sizeof(double) + (size_t)G * max_types * sizeof(TypeRec);
   // static (heaps, per-lane state) + dynamic (price buffer) may exceed the
   // 48 KB default: opt in for the dynamic part every time
-  cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI, CAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const unsigned blocks = (unsigned)((n_traces + G - 1) / G);
-  k_replay<W, MULTI><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
+  k_replay<W, MULTI, CAL><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
                                                 d_result, static_cast<QRec*>(d_qrec), d_heap, d_deps, d_trace_dep,
                                                 d_trace_heap, n_max, max_types, d_progress, phase_len, rc);
   return cudaGetLastError();
@@ -1128,11 +1252,22 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
   if (max_types <= 0) max_types = rc.n_types;
   const int W = (n_max + 31) / 32;
 #define HS_LW(w, m)                                                                                              \
-  launch_w<w, m>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result, d_qrec, d_heap, \
-                 st, d_deps, d_trace_dep, d_trace_heap, n_max, max_types, d_progress, phase_len)
+  (cal ? launch_w<w, m, true>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result,  \
+                              d_qrec, d_heap, st, d_deps, d_trace_dep, d_trace_heap, n_max, max_types, d_progress,  \
+                              phase_len)                                                                           \
+       : launch_w<w, m, false>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics, d_result, d_qrec, d_heap, \
+                 st, d_deps, d_trace_dep, d_trace_heap, n_max, max_types, d_progress, phase_len))
   const bool multi = d_deps != nullptr;
+  const bool cal = rc.cal_bits > 0;
   switch (W) {
-    case 1: return multi ? HS_LW(1, true) : HS_LW(1, false);
+    case 1:  // one-warp traces keep the shared-memory heap (calendars are for W > 1)
+      if (cal) return cudaErrorInvalidValue;
+      return multi ? launch_w<1, true, false>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart,
+                                              d_metrics, d_result, d_qrec, d_heap, st, d_deps, d_trace_dep,
+                                              d_trace_heap, n_max, max_types, d_progress, phase_len)
+                   : launch_w<1, false, false>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart,
+                                               d_metrics, d_result, d_qrec, d_heap, st, d_deps, d_trace_dep,
+                                               d_trace_heap, n_max, max_types, d_progress, phase_len);
     case 2: return multi ? HS_LW(2, true) : HS_LW(2, false);
     case 3: return multi ? HS_LW(3, true) : HS_LW(3, false);
     case 4: return multi ? HS_LW(4, true) : HS_LW(4, false);
@@ -1146,23 +1281,31 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
 }
 
 // min over all requests of (I + O): sizes the per-instance active-set heaps
-__global__ void k_min_need(const int32_t* __restrict__ I, const int32_t* __restrict__ O, int64_t n, int32_t* out) {
-  int32_t m = INT32_MAX;
+__global__ void k_min_need(const int32_t* __restrict__ I, const int32_t* __restrict__ O, int64_t n, int32_t* out,
+                           int32_t* max_out) {
+  int32_t m = INT32_MAX, mo = 0;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = (int64_t)I[k] + O[k];
+    const int32_t o = O[k];
+    const int64_t v = (int64_t)I[k] + o;
     const int32_t vv = v > INT32_MAX ? INT32_MAX : (int32_t)v;
     m = vv < m ? vv : m;
+    mo = o > mo ? o : mo;
   }
   m = __reduce_min_sync(FULL, (unsigned)m);
-  if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+  mo = (int32_t)__reduce_max_sync(FULL, (unsigned)mo);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, m);
+    if (max_out) atomicMax(max_out, mo);
+  }
 }
 
-cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st) {
+cudaError_t launch_min_need(const int32_t* d_I, const int32_t* d_O, int64_t n, int32_t* d_out, cudaStream_t st,
+                            int32_t* d_max_out) {
   if (n <= 0) return cudaSuccess;
   int blocks = (int)((n + 255) / 256);
   const int cap = sm_count() * 8;
   if (blocks > cap) blocks = cap;
-  k_min_need<<<blocks, 256, 0, st>>>(d_I, d_O, n, d_out);
+  k_min_need<<<blocks, 256, 0, st>>>(d_I, d_O, n, d_out, d_max_out);
   return cudaGetLastError();
 }
 

@@ -25,7 +25,7 @@ from paper_2504_15303_b200 import workloads as wl  # noqa: E402
 
 
 def main():
-    q = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000
+    q = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 100_000
     eng = nat.engine_for(0)
     cluster, reqs, params, _I, _O = bench.search_inputs(10_000)
     t = planner.build_tables(cluster, reqs, params, engine=eng)
@@ -60,7 +60,8 @@ def main():
         run(np.arange(1024), reps=1)
         eng.lib.hs_debug_timers(buf.ctypes.data_as(ctypes.c_void_p), 0)
         nw = int(((n_inst + 31) // 32).sum())
-        names = {0: "advance", 1: "price", 2: "evaluate", 16: "minmax", 17: "commit", 18: "drain", 19: "whole"}
+        names = {0: "advance", 1: "price", 2: "evaluate", 21: "  exp part (lanes that need it)", 16: "minmax",
+                 20: "  barrier wait", 17: "commit", 18: "drain", 19: "whole"}
         print("cycles per warp per request:", {v: round(float(buf[k]) / nw / q, 1) for k, v in names.items()})
         print("cycles per warp (whole trace): %.3g" % (float(buf[19]) / nw))
         calls = max(int(buf[7]), 1)
@@ -68,6 +69,9 @@ def main():
               "steps with nact>kHS %.3f, mean nact %.1f"
               % (calls, calls / (1024 * q), buf[3] / calls, buf[4] / calls, buf[5] / calls, buf[14] / calls,
                  buf[15] / calls))
+        print("rescans per event call %.4f (mean length %.1f)" % (buf[10] / calls, buf[11] / max(int(buf[10]), 1)))
+        if "--timers-only" in sys.argv:
+            return
     steps = res.result["n_steps"].astype(np.int64)
     W = (n_inst + 31) // 32
     print(f"full: {full_ms:.1f} ms; instances min/med/max {n_inst.min()}/{int(np.median(n_inst))}/{n_inst.max()}; "
