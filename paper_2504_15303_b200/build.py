@@ -31,15 +31,17 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, force: bool = False, timers: bool = False) -> pathlib.Path:
-    lib = PKG / "libhetserve_b200_timers.so" if timers else LIB
+def build(verbose: bool = False, force: bool = False, timers: bool = False, defines=(), out=None) -> pathlib.Path:
+    """defines / out: diagnostic variants (e.g. -DHS_REPLAY_MIN_BLOCKS_MULTI=5 into a
+    separate .so, loaded with HS_LIB=...); the product library takes neither."""
+    lib = pathlib.Path(out).resolve() if out else (PKG / "libhetserve_b200_timers.so" if timers else LIB)
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
     deps += list((PKG.parent / "include").glob("*.h"))
     if not force and lib.exists() and all(lib.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return lib
     flags = [*ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
-             "-Xptxas", "-v" if verbose else "-O3", *(["-DHS_TIMERS"] if timers else [])]
-    objdir = PKG / "build" / ("timers" if timers else "release")
+             "-Xptxas", "-v" if verbose else "-O3", *(["-DHS_TIMERS"] if timers else []), *defines]
+    objdir = PKG / "build" / (lib.stem if out else ("timers" if timers else "release"))
     objdir.mkdir(parents=True, exist_ok=True)
     # one nvcc per translation unit, in parallel, then one link
     cmds = [[nvcc(), *flags, "-c", str(CSRC / s), "-o", str(objdir / (s + ".o"))] for s in SOURCES]

@@ -57,7 +57,9 @@ __device__ unsigned long long g_timers[24];
 #endif
 
 constexpr int kWarps = 4;
-// Resident blocks per SM that __launch_bounds__ asks for.  One-warp traces
+// Resident blocks per SM that __launch_bounds__ asks for (of the block's real
+// size, replay_block_threads: a 3-warp trace is a 96-thread block; bounding it
+// as 128 threads cost config 5 8 %: 425 vs 393 ms).  One-warp traces
 // (N <= 32) are issue-bound and gain from occupancy: 4 blocks (128 registers)
 // beats 3 (168) by 17 % on config 4.  Multi-warp traces (W > 1) spill at 128
 // registers (60-150 B) and lose more to the spills than they gain from the
@@ -69,6 +71,8 @@ constexpr int kWarps = 4;
 #define HS_REPLAY_MIN_BLOCKS_MULTI 3
 #endif
 constexpr unsigned FULL = 0xffffffffu;
+// threads of a replay block: G trace groups of W warps (G = 4 / 2 / 1 for W = 1 / 2 / >= 3)
+__host__ __device__ constexpr int replay_block_threads(int W) { return W * (W == 1 ? 4 : (W == 2 ? 2 : 1)) * 32; }
 
 // Per-lane min-heap of retirement entries: key = departure step << 32 |
 // request (orders retirements as the reference's active list does) and
@@ -233,7 +237,7 @@ __device__ __forceinline__ void group_bar(int g, int nthreads) {
 }
 
 template <int W, bool MULTI, bool CAL>
-__global__ void __launch_bounds__((W > kWarps ? W : kWarps) * 32,
+__global__ void __launch_bounds__(replay_block_threads(W),
                                   W == 1 ? HS_REPLAY_MIN_BLOCKS : (W > kWarps ? 1 : HS_REPLAY_MIN_BLOCKS_MULTI))
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
