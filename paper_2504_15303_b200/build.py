@@ -20,7 +20,7 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhetserve_b200.so"
-SOURCES = ["capi.cu", "search.cu", "replay.cu", "topk.cu", "rng.cu", "scheduler.cpp"]
+SOURCES = ["capi.cu", "search.cu", "replay.cu", "topk.cu", "sort.cu", "rng.cu", "scheduler.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -11,8 +11,6 @@
 #include <string>
 #include <vector>
 
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
 
 #include "hs_device.cuh"
 #include "hs_internal.h"
@@ -752,16 +750,11 @@ int hs_search_rank(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
       (rc = ensure_t(c, S_KEYS2, (size_t)P, &keys2)) || (rc = ensure_t(c, S_IDX2, (size_t)P, &idx2)) ||
       (rc = ensure_t(c, S_RANKED, (size_t)P, &out)))
     return rc;
-  size_t tmp1 = 0, tmp2 = 0;
-  thrust::counting_iterator<int64_t> counting(0);
-  HS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp1, counting, flag, sel, nsel, P, c->stream));
-  HS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, keys, keys2, sel, idx2, (int)P, 0, 64, c->stream));
   void* tmp;
-  if ((rc = ensure(c, S_CUBTMP, tmp1 > tmp2 ? tmp1 : tmp2, &tmp))) return rc;
-  size_t tmpn = c->cap[S_CUBTMP];
+  if ((rc = ensure(c, S_CUBTMP, hs::sort_workspace_bytes(P), &tmp))) return rc;
   if ((rc = begin_timing(c))) return rc;
   HS_CUDA(hs::launch_search_score(sd, m_off, P, tot, fb, flag, c->stream));
-  HS_CUDA(cub::DeviceSelect::Flagged(tmp, tmpn, counting, flag, sel, nsel, P, c->stream));
+  HS_CUDA(hs::select_flagged(flag, P, sel, nsel, tmp, c->stream));
   const unsigned g = (unsigned)((P + 255) / 256);
   k_orderable_keys<<<g, 256, 0, c->stream>>>(tot, sel, nsel, keys);
   HS_CUDA(cudaGetLastError());
@@ -769,9 +762,10 @@ int hs_search_rank(hs_ctx* c, const hs_entry* table, const int32_t* n_degrees, i
   HS_CUDA(cudaMemcpyAsync(&h_nsel, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   if (h_nsel > 0) {
-    tmpn = c->cap[S_CUBTMP];
-    HS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmpn, keys, keys2, sel, idx2, (int)h_nsel, 0, 64, c->stream));
-    k_gather_ranked<<<g, 256, 0, c->stream>>>(tot, idx2, nsel, out);
+    // (key, index) pairs by key: ties keep the index order of the selection
+    HS_CUDA(hs::sort_pairs_u64(keys, reinterpret_cast<uint64_t*>(sel), keys2, reinterpret_cast<uint64_t*>(idx2),
+                               h_nsel, 0, 64, tmp, c->stream));
+    k_gather_ranked<<<g, 256, 0, c->stream>>>(tot, sel, nsel, out);
     HS_CUDA(cudaGetLastError());
   }
   c->launches += 5;
@@ -912,16 +906,13 @@ int search_topk_impl(hs_ctx* c, const hs_entry* table, const int32_t* nd, int32_
   if ((int64_t)got > CAP) return fail(HS_ERR_UNSUPPORTED, "more than 2^20 candidates tie at the top-k boundary");
   const int n = (int)got;
   // stable sorts: by index ascending, then by total descending (~key ascending)
-  size_t t1 = 0, t2 = 0;
-  HS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, d_idx, d_idx2, d_key, d_key2, n, 0, 64, c->stream));
-  HS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, d_key2, d_key, d_idx2, d_idx, n, 0, 64, c->stream));
   void* tmp;
-  if ((rc = ensure(c, S_CUBTMP, t1 > t2 ? t1 : t2, &tmp))) return rc;
-  size_t tn = c->cap[S_CUBTMP];
-  HS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tn, d_idx, d_idx2, d_key, d_key2, n, 0, 64, c->stream));
-  HS_CUDA(hs::launch_invert_keys(d_key2, n, c->stream));
-  tn = c->cap[S_CUBTMP];
-  HS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tn, d_key2, d_key, d_idx2, d_idx, n, 0, 64, c->stream));
+  if ((rc = ensure(c, S_CUBTMP, hs::sort_workspace_bytes(n), &tmp))) return rc;
+  HS_CUDA(hs::sort_pairs_u64(reinterpret_cast<uint64_t*>(d_idx), d_key, reinterpret_cast<uint64_t*>(d_idx2), d_key2,
+                             n, 0, 64, tmp, c->stream));
+  HS_CUDA(hs::launch_invert_keys(d_key, n, c->stream));
+  HS_CUDA(hs::sort_pairs_u64(d_key, reinterpret_cast<uint64_t*>(d_idx), d_key2, reinterpret_cast<uint64_t*>(d_idx2),
+                             n, 0, 64, tmp, c->stream));
   c->launches += 3;
   if ((rc = end_timing(c))) return rc;
   std::vector<uint64_t> hk((size_t)K);

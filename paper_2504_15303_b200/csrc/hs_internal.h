@@ -107,6 +107,15 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
                           const int32_t* d_trace_dep = nullptr, const int64_t* d_trace_heap = nullptr,
                           int n_max = 0, int max_types = 0, const uint32_t* d_progress = nullptr,
                           int phase_len = 0);
+// sort.cu: stable LSD radix sort of (key, value) pairs by key bits
+// [begin_bit, end_bit), in place (keys / vals; *_alt are scratch of n), and the
+// ordered indices of the set flags (*d_count = how many).  workspace:
+// sort_workspace_bytes(n).
+size_t sort_workspace_bytes(int64_t n);
+cudaError_t sort_pairs_u64(uint64_t* keys, uint64_t* vals, uint64_t* keys_alt, uint64_t* vals_alt, int64_t n,
+                           int begin_bit, int end_bit, void* workspace, cudaStream_t st);
+cudaError_t select_flagged(const uint8_t* flag, int64_t n, int64_t* out, int64_t* d_count, void* workspace,
+                           cudaStream_t st);
 constexpr int kQRecBytes = 24;  // replay.cu QRec
 // retirement calendar (multi-warp traces): 2^cal_bits buckets, cal_bits <= kMaxCalBits
 // (the summary bitmap is kCalSumWords 64-bit words per lane)

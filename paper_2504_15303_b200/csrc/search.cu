@@ -23,7 +23,6 @@
 //   ranking of small spaces (sorted afterwards with CUB).
 #include <cmath>
 
-#include <cub/cub.cuh>
 
 #include "hs_device.cuh"
 #include "hs_internal.h"

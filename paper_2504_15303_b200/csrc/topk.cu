@@ -13,7 +13,6 @@
 // totals (12-bit digits, one histogram pass per digit, stopping as soon as
 // the candidates at or above the current bucket fit the collect buffer),
 // then one collect pass and a stable device sort by (total desc, index asc).
-#include <cub/cub.cuh>
 
 #include "hs_device.cuh"
 #include "hs_internal.h"
