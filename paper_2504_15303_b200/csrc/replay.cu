@@ -37,6 +37,8 @@
 // mapping (scheduling.py:299-312) is O(log N): the max of the loads and an
 // argmin of peaks via REDUX on order-preserving 64-bit keys.
 #include "hs_device.cuh"
+#include <cstdlib>
+
 #include "hs_internal.h"
 
 namespace hs {
@@ -57,6 +59,8 @@ __device__ unsigned long long g_timers[24];
 #endif
 
 constexpr int kWarps = 4;
+// at most this many one-warp traces per SM run the pipelined pure loop
+constexpr int kPipeTracesPerSM = 8;
 // Resident blocks per SM that __launch_bounds__ asks for (of the block's real
 // size, replay_block_threads: a 3-warp trace is a 96-thread block; bounding it
 // as 128 threads cost config 5 8 %: 425 vs 393 ms).  One-warp traces
@@ -236,7 +240,7 @@ __device__ __forceinline__ void group_bar(int g, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(nthreads) : "memory");
 }
 
-template <int W, bool MULTI, bool CAL>
+template <int W, bool MULTI, bool CAL, bool PIPE>
 __global__ void __launch_bounds__(replay_block_threads(W),
                                   W == 1 ? HS_REPLAY_MIN_BLOCKS : (W > kWarps ? 1 : HS_REPLAY_MIN_BLOCKS_MULTI))
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
@@ -740,18 +744,34 @@ __global__ void __launch_bounds__(replay_block_threads(W),
           const double t4 = __dadd_rn(t3, c3);
           // monotone clocks: t4 < lim implies t1, t2, t3 < lim, so one test
           // admits the whole block; the per-step tests run on the block that
-          // exits.  The next block's prices are computed only once the block
-          // is admitted (the kernel is issue-bound: no prices wasted on exits)
+          // exits.  At full occupancy (issue-bound) the next block's prices are
+          // computed only once the block is admitted (none wasted on exits);
+          // PIPE (few traces per SM: latency-bound) computes them alongside
+          // this block's clock chain, off the dependent path.
+          double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
+          if (PIPE) {
+            n0 = price(__dadd_rn(cd, 4.0));
+            n1 = price(__dadd_rn(cd, 5.0));
+            n2 = price(__dadd_rn(cd, 6.0));
+            n3 = price(__dadd_rn(cd, 7.0));
+          }
           const bool all4 = mono ? (k + 4 < kr && (drain || t4 < lim))
                                  : (k + 4 < kr && (drain || (t1 < lim && t2 < lim && t3 < lim && t4 < lim)));
           if (all4) {
             t_next = t4;
             cd = __dadd_rn(cd, 4.0);
             k += 4;
-            c0 = price(cd);
-            c1 = price(__dadd_rn(cd, 1.0));
-            c2 = price(__dadd_rn(cd, 2.0));
-            c3 = price(__dadd_rn(cd, 3.0));
+            if (PIPE) {
+              c0 = n0;
+              c1 = n1;
+              c2 = n2;
+              c3 = n3;
+            } else {
+              c0 = price(cd);
+              c1 = price(__dadd_rn(cd, 1.0));
+              c2 = price(__dadd_rn(cd, 2.0));
+              c3 = price(__dadd_rn(cd, 3.0));
+            }
             continue;
           }
           // step i+1 runs iff step i ran, k+i < kr and t_i < lim
@@ -1224,7 +1244,7 @@ __global__ void __launch_bounds__(replay_block_threads(W),
   }
 }
 
-template <int W, bool MULTI, bool CAL>
+template <int W, bool MULTI, bool CAL, bool PIPE = false>
 cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
                      const int32_t* d_O, const int32_t* d_P, const double* d_arr, uint8_t* d_assign, double* d_depart,
                      hs_inst_metrics* d_metrics, hs_trace_result* d_result, void* d_qrec, uint64_t* d_heap,
@@ -1236,13 +1256,26 @@ cudaError_t launch_w(const ReplayConst& rc, int64_t n_traces, const int64_t* d_o
   const size_t smem = (size_t)warps * 32 * max_types * sizeof(double) + (size_t)G * max_types * sizeof(TypeRec);
   // static (heaps, per-lane state) + dynamic (price buffer) may exceed the
   // 48 KB default: opt in for the dynamic part every time
-  cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI, CAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_replay<W, MULTI, CAL, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const unsigned blocks = (unsigned)((n_traces + G - 1) / G);
-  k_replay<W, MULTI, CAL><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
+  k_replay<W, MULTI, CAL, PIPE><<<blocks, warps * 32, smem, st>>>(n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
                                                 d_result, static_cast<QRec*>(d_qrec), d_heap, d_deps, d_trace_dep,
                                                 d_trace_heap, n_max, max_types, d_progress, phase_len, rc);
   return cudaGetLastError();
+}
+
+// One-warp traces: the software-pipelined pure loop (next block's prices
+// computed alongside this block's clock chain) pays when few traces share an
+// SM (latency-bound); at full occupancy the kernel is issue-bound and the
+// admit-then-price loop wins.  HS_REPLAY_PIPE=0/1 forces either (A/B runs).
+static bool replay_pipelined(int64_t n_traces) {
+  static const int force = [] {
+    const char* e = std::getenv("HS_REPLAY_PIPE");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  return n_traces <= (int64_t)kPipeTracesPerSM * sm_count();
 }
 
 cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t* d_off, const int32_t* d_I,
@@ -1266,12 +1299,17 @@ cudaError_t launch_replay(const ReplayConst& rc, int64_t n_traces, const int64_t
   switch (W) {
     case 1:  // one-warp traces keep the shared-memory heap (calendars are for W > 1)
       if (cal) return cudaErrorInvalidValue;
-      return multi ? launch_w<1, true, false>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart,
-                                              d_metrics, d_result, d_qrec, d_heap, st, d_deps, d_trace_dep,
-                                              d_trace_heap, n_max, max_types, d_progress, phase_len)
-                   : launch_w<1, false, false>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart,
+      if (multi)
+        return launch_w<1, true, false>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
+                                        d_result, d_qrec, d_heap, st, d_deps, d_trace_dep, d_trace_heap, n_max,
+                                        max_types, d_progress, phase_len);
+      if (replay_pipelined(n_traces))
+        return launch_w<1, false, false, true>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart,
                                                d_metrics, d_result, d_qrec, d_heap, st, d_deps, d_trace_dep,
                                                d_trace_heap, n_max, max_types, d_progress, phase_len);
+      return launch_w<1, false, false>(rc, n_traces, d_off, d_I, d_O, d_P, d_arr, d_assign, d_depart, d_metrics,
+                                       d_result, d_qrec, d_heap, st, d_deps, d_trace_dep, d_trace_heap, n_max,
+                                       max_types, d_progress, phase_len);
     case 2: return multi ? HS_LW(2, true) : HS_LW(2, false);
     case 3: return multi ? HS_LW(3, true) : HS_LW(3, false);
     case 4: return multi ? HS_LW(4, true) : HS_LW(4, false);

@@ -15,8 +15,11 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("pipe", ["0", "1"])
 @pytest.mark.parametrize("n_inst", [32, 9])
-def test_replay_vs_oracle_all_policies(n_inst):
+def test_replay_vs_oracle_all_policies(n_inst, pipe):
+    """pipe: HS_REPLAY_PIPE forces either one-warp pure-step loop (the launch
+    picks by traces per SM: the pipelined one below 8 per SM)."""
     r = subprocess.run([sys.executable, str(ROOT / "tests" / "replay_check.py"), "40", "3000", str(n_inst)],
-                       env=dict(os.environ), capture_output=True, text=True, timeout=900)
+                       env=dict(os.environ, HS_REPLAY_PIPE=pipe), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
