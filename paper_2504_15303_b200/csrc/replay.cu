@@ -231,10 +231,9 @@ struct Xch {
   int32_t c, d;
 };
 // Per-instance record of one dispatch (multi-warp traces, OS / MB): the
-// load's order key and load + w.
+// load's order key and the candidate key of load + w (~0: not a candidate).
 struct DispRec {
-  uint64_t lk;
-  double own;
+  uint64_t lk, ko;
 };
 __device__ __forceinline__ void group_bar(int g, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(nthreads) : "memory");
@@ -945,10 +944,13 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         // publish (load key, load + w) and the warp's error / candidate
         // masks; one barrier; every warp then sees the whole group
         const int buf = (int)(a & 1);
-        const unsigned preb = __ballot_sync(FULL, need && !isinf(w));
         const unsigned stepb = __ballot_sync(FULL, valid && lerr);
-        s_disp[buf][g][jj] = DispRec{valid ? okey(load) : 0ull, __dadd_rn(load, w)};
-        if (lane == 0) s_dflag[buf][g][wsub] = make_uint4(errb, stepb, preb, 0u);
+        // candidate key of own = load + w: its peak is max(own, top), so a NaN
+        // own (never > top) ranks as the smallest key and +inf is no candidate
+        const double own = __dadd_rn(load, w);
+        const uint64_t ko = (need && !isinf(w)) ? (isnan(own) ? 0ull : (own < INFINITY ? okey(own) : ~0ull)) : ~0ull;
+        s_disp[buf][g][jj] = DispRec{valid ? okey(load) : 0ull, ko};
+        if (lane == 0) s_dflag[buf][g][wsub] = make_uint4(errb, stepb, 0u, 0u);
         HS_T0(tb0);
         group_bar(g, W * 32);
         HS_T1(20, tb0);
@@ -1008,31 +1010,30 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         // reduction instead of the top-2 of the loads.
         if (fused) {
           // the whole group's reduction from the published records, in
-          // every warp: max load, then the lowest instance of minimum peak
-          uint64_t lm = 0;
+          // every warp.  With M = max load key and K_s = candidate key, the
+          // peak key is max(K_s, M), so the minimum peak is max(min K, M) =:
+          // thr and the choice is the lowest instance with K_s <= thr: the
+          // max and the min reduce side by side, then one ballot per warp.
+          uint64_t lm = 0, km = ~0ull, ko[W];
 #pragma unroll
           for (int w2 = 0; w2 < W; ++w2) {
-            const uint64_t lk = drec[w2 * 32 + lane].lk;
-            lm = lk > lm ? lk : lm;
+            const DispRec e = drec[w2 * 32 + lane];
+            lm = e.lk > lm ? e.lk : lm;
+            km = e.ko < km ? e.ko : km;
+            ko[w2] = e.ko;
           }
           const uint64_t m1 = warp_max_u64(lm);
+          const uint64_t kmin = warp_min_u64(km);
           const double top = from_okey(m1);
-          uint64_t pk[W];
-          uint64_t pmin = ~0ull;
+          const uint64_t thr = kmin > m1 ? kmin : m1;
+          unsigned ci = 0xffffffffu;
+          if (top < INFINITY && kmin != ~0ull) {  // a NaN or +inf top leaves no candidate
 #pragma unroll
-          for (int w2 = 0; w2 < W; ++w2) {
-            const double own = drec[w2 * 32 + lane].own;
-            const double peak = own > top ? own : top;
-            const bool cand = ((s_dflag[a & 1][g][w2].z >> lane) & 1u) && peak < INFINITY;
-            pk[w2] = cand ? okey(peak) : ~0ull;
-            pmin = pk[w2] < pmin ? pk[w2] : pmin;
+            for (int w2 = W - 1; w2 >= 0; --w2) {
+              const unsigned b = __ballot_sync(FULL, ko[w2] <= thr);
+              if (b) ci = (unsigned)(w2 * 32 + __ffs(b) - 1);
+            }
           }
-          const uint64_t mp = warp_min_u64(pmin);
-          unsigned my_idx = 0xffffffffu;
-#pragma unroll
-          for (int w2 = W - 1; w2 >= 0; --w2)
-            if (pk[w2] != ~0ull && pk[w2] == mp) my_idx = (unsigned)(w2 * 32 + lane);
-          const unsigned ci = __reduce_min_sync(FULL, my_idx);
           if (ci == 0xffffffffu) {
             t_err = HS_TRACE_NO_INSTANCE;
             t_err_req = a;
@@ -1041,23 +1042,18 @@ __global__ void __launch_bounds__(replay_block_threads(W),
             break;
           }
           chosen = (int)ci;
-        } else {
-        uint64_t m1 = warp_max_u64(valid ? okey(load) : 0ull);
-        if (W > 1) {
-          Xch all[W];
-          xchg(Xch{m1, 0, 0, 0}, all);
-          m1 = all[0].a;
-#pragma unroll
-          for (int w = 1; w < W; ++w) m1 = all[w].a > m1 ? all[w].a : m1;
-        }
-        const double top = from_okey(m1);
-        const double own = __dadd_rn(load, w);
-        const double peak = own > top ? own : top;
-        const bool cand = need && !isinf(w) && peak < INFINITY;
-        const uint64_t pk = cand ? okey(peak) : ~0ull;
-        const uint64_t mp = warp_min_u64(pk);
-        const unsigned win = __ballot_sync(FULL, cand && pk == mp);
-        if (W == 1) {
+        } else {  // W == 1 (multi-warp OS / MB traces take the fused path)
+          // the same threshold form as above: the max-load and the
+          // min-candidate reductions are independent, then one ballot
+          const double own = __dadd_rn(load, w);
+          const uint64_t kown =
+              (need && !isinf(w)) ? (isnan(own) ? 0ull : (own < INFINITY ? okey(own) : ~0ull)) : ~0ull;
+          const uint64_t m1 = warp_max_u64(valid ? okey(load) : 0ull);
+          const uint64_t kmin = warp_min_u64(kown);
+          const double top = from_okey(m1);
+          const uint64_t thr = kmin > m1 ? kmin : m1;
+          const bool any = top < INFINITY && kmin != ~0ull;  // a NaN or +inf top leaves no candidate
+          const unsigned win = __ballot_sync(FULL, any && kown <= thr);
           if (!win) {
             t_err = HS_TRACE_NO_INSTANCE;
             t_err_req = a;
@@ -1066,22 +1062,6 @@ __global__ void __launch_bounds__(replay_block_threads(W),
             break;
           }
           chosen = __ffs(win) - 1;
-        } else {
-          Xch all[W];
-          xchg(Xch{win ? mp : ~0ull, (uint64_t)(wsub * 32 + __ffs(win) - 1), win ? 1 : 0, 0}, all);
-          int bw = -1;
-#pragma unroll
-          for (int w = 0; w < W; ++w)
-            if (all[w].c && (bw < 0 || all[w].a < all[bw].a)) bw = w;
-          if (bw < 0) {
-            t_err = HS_TRACE_NO_INSTANCE;
-            t_err_req = a;
-            t_err_inst = -1;
-            failed = true;
-            break;
-          }
-          chosen = (int)all[bw].b;
-        }
         }
       }
 
