@@ -493,6 +493,10 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         }
       }
       reserved -= Ir + Or;
+      if (W > 1) {  // multi-warp traces count at retirement: off the barrier-paced dispatch
+        cold.req_count += 1;
+        cold.tok_count += Ir + Or;
+      }
       cold.completion = t;
       if (DEP) {
         if (c_rep.flags & kOrderKeys) {
@@ -1075,10 +1079,15 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         dirty = true;
         // InstanceMetrics request / token counts (simulator.py:338-341): in a
         // replay that completes, every dispatched request retires exactly
-        // once, so they are accumulated here, off the retirement path (a
-        // failed trace reports an error instead of metrics)
-        cold.req_count += 1;
-        cold.tok_count += Ia + Oa;
+        // once, so one-warp traces (and static mode, which has no event
+        // steps) accumulate them here, off the retirement path; multi-warp
+        // continuous traces count at retirement instead, off the dispatch
+        // that their barrier paces (a failed trace reports an error instead
+        // of metrics)
+        if (W == 1 || is_static) {
+          cold.req_count += 1;
+          cold.tok_count += Ia + Oa;
+        }
         R[a].P = (int32_t)Pa;
         R[a].W = w;
         if (qhead < 0) {
