@@ -123,7 +123,10 @@ constexpr int kMaxCalBits = 14;
 constexpr int kCalSumWords = 1 << (kMaxCalBits - 12);
 constexpr int kHEntBytes = 16;  // replay.cu HEnt
 // heap entries per lane kept in shared memory by a trace of w warps (replay.cu kHS)
-__host__ __device__ constexpr int replay_heap_prefix(int w) { return w > 4 ? 4 : 16; }
+#ifndef HS_REPLAY_HEAP_PREFIX
+#define HS_REPLAY_HEAP_PREFIX 16
+#endif
+__host__ __device__ constexpr int replay_heap_prefix(int w) { return w > 4 ? 4 : HS_REPLAY_HEAP_PREFIX; }
 
 // Seeded streams (rng.cu): up to kMaxDists distributions drawn in order from
 // each stream; out[j] is indexed by the stream offsets.
