@@ -618,3 +618,57 @@ def test_wide_deployments_over_128_instances_vs_oracle(eng, n_machines):
             assert np.array_equal(res.result["n_steps"], r["n_steps"]), (policy, rate)
             for f in ("completion_time", "peak_kv_usage", "residual_load"):
                 assert np.array_equal(res.metrics[f].view(np.uint64), m[f].view(np.uint64)), (policy, rate, f)
+
+
+@pytest.mark.parametrize("max_out", [60, 5000, 12000, 20000])
+def test_retirement_calendar_ring_sizes_vs_oracle(eng, max_out):
+    """Multi-warp multi-deployment replays size the retirement calendar from the
+    launch's largest output length: 2^6 .. 2^14 buckets (one to four summary
+    words per lane), and beyond 2^14 - 1 the heap again.  48- and 27-instance
+    deployments (2 and 1 warps), OS / RR, finite rate and rate = inf, with a
+    few outputs as long as max_out, vs the oracle."""
+    prof = wl.config4()
+    types = list(wl.CONFIG4_TYPES)
+    machines = tuple(hs.MachineSpec(f"m{k}", 8, wl.TYPE_MEM_GB[types[k % 4]] * 1_000_000_000, types[k % 4])
+                     for k in range(6))
+    cluster = hs.ClusterSpec(model=hs.ModelSpec(**prof.model), engine=hs.EngineOverheads(**prof.engine),
+                             machines=machines, limits=hs.WorkloadLimits(**prof.limits))
+    params = {(m.name, t): hs.LatencyParams(*wl.scaled_params(wl.RANK_BASE, t ** -wl.TP_ALPHA *
+                                                               wl.TYPE_SCALE[m.accelerator_type]))
+              for m in machines for t in wl.enumerate_degrees(8)}
+    configs = [hs.deployment_for(machines, {m.name: 1 for m in machines}),
+               hs.deployment_for(machines, {m.name: (1 if k % 2 else 8) for k, m in enumerate(machines)})]
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+    sizes = [len(build_instances(cluster, c, params)) for c in configs]
+    assert sizes[0] == 48 and sizes[1] < 32
+    q, T = 1500, 4
+    Is, Os = [], []
+    for t in range(T):
+        I, O = wl.trace_lengths(q, seed=40 + t)
+        O = np.minimum(O, max_out).astype(np.int32)
+        O[np.random.default_rng(t).choice(q, 3, replace=False)] = max_out  # the longest retirements
+        Is.append(I)
+        Os.append(O)
+    I, O = np.concatenate(Is), np.concatenate(Os)
+    off = np.arange(T + 1, dtype=np.int64) * q
+    tdep = np.arange(T) % 2
+    per_token = hs.kv_bytes_per_token(cluster.model)
+    for policy in ("OS", "RR"):
+        pol = hs.PolicyConfig(policy=policy)
+        for rate in (400.0, math.inf):
+            A = None if math.isinf(rate) else np.concatenate([wl.arrivals(q, rate, seed=t) for t in range(T)])
+            res = hs.replay_deployments(cluster, configs, params, pol, tdep, off, I, O, O, arrival=A,
+                                        want_depart=True, engine=eng)
+            for t in range(T):
+                handles = build_instances(cluster, configs[tdep[t]], params)
+                n = len(handles)
+                sl = slice(off[t], off[t + 1])
+                a, d, m, r = orc.replay(engine_instances(handles, pol), _policy_struct(pol, n, per_token),
+                                        np.array([0, q], np.int64), I[sl], O[sl], O[sl],
+                                        None if A is None else A[sl])
+                assert int(res.result[t]["error"]) == int(r[0]["error"]), (policy, rate, t)
+                assert res.result[t]["n_steps"] == r[0]["n_steps"], (policy, rate, t)
+                assert np.array_equal(res.assign[sl], a), (policy, rate, t)
+                assert np.array_equal(res.depart[sl].view(np.uint64), d.view(np.uint64)), (policy, rate, t)
+                for f in ("completion_time", "peak_kv_usage", "residual_load"):
+                    assert np.array_equal(res.metrics[t, :n][f].view(np.uint64), m[0][f].view(np.uint64)), f
