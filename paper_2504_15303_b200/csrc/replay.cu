@@ -204,7 +204,7 @@ struct Cold {
   double completion, wcur, err_t;
   double segmax;  // HS_REPLAY_ORDER_KEYS: running max of step times since the lane last went idle
   int64_t tok_count;
-  int32_t req_count, cnt_max, err, err_req;
+  int32_t req_count, err, err_req;
   int32_t ty;    // instance class (read from here: a per-lane constant-bank index serialises)
   int32_t nret;  // HS_REPLAY_ORDER_KEYS: retirements so far (per-lane processing order)
 };
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(replay_block_threads(W),
   cold.err_t = 0.0;
   cold.tok_count = 0;
   cold.req_count = 0;
-  cold.cnt_max = 0;
+  int32_t cnt_max = 0;  // holders of cur_max among the active requests (a register: -1.2 % / -4.3 %)
   cold.err = HS_TRACE_OK;
   cold.err_req = -1;
   uint32_t n_steps = 0;
@@ -516,11 +516,11 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         return;
       }
       const int64_t ka = (int64_t)k - (Or > 1 ? Or : 1);
-      if (Ir - ka == cur_max && --cold.cnt_max == 0) max_dirty = true;
+      if (Ir - ka == cur_max && --cnt_max == 0) max_dirty = true;
     }
     if (nact == 0) {
       cur_max = INT64_MIN;
-      cold.cnt_max = 0;
+      cnt_max = 0;
       max_dirty = false;
     }
     HS_LT1(3, tr0);
@@ -596,10 +596,10 @@ __global__ void __launch_bounds__(replay_block_threads(W),
       }
       if (mk > cur_max) {
         cur_max = mk;
-        cold.cnt_max = 1;
+        cnt_max = 1;
         max_dirty = false;
       } else if (mk == cur_max) {
-        cold.cnt_max += 1;
+        cnt_max += 1;
       }
     }
     blocked = true;  // queue empty or its head does not fit: nothing changes until an event
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(replay_block_threads(W),
     }
     double c = 0.0;
     if (newly) c = __dadd_rn(c, prefill_time(tp, newly, max_i_new));
-    if (max_dirty || cold.cnt_max <= 0) {  // the last holder of the max retired: rescan
+    if (max_dirty || cnt_max <= 0) {  // the last holder of the max retired: rescan
       int64_t m = INT64_MIN;
       int32_t cm = 0;
 #ifdef HS_TIMERS
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         for (int32_t h = 0; h < nact; ++h) count(heap.get(h, nact).mk);
       }
       cur_max = m;
-      cold.cnt_max = cm;
+      cnt_max = cm;
       max_dirty = false;
     }
     const double db = i2d(nact);
