@@ -1404,7 +1404,11 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
   if (total > 0) {
     HS_CUDA(cudaMemcpyAsync(dI, b->input_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
     HS_CUDA(cudaMemcpyAsync(dO, b->output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
-    HS_CUDA(cudaMemcpyAsync(dP, b->pred_output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
+    // predictions identical to the outputs (oracle predictor): copy once
+    if (b->pred_output_len == b->output_len)
+      dP = dO;
+    else
+      HS_CUDA(cudaMemcpyAsync(dP, b->pred_output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
     if (dT) HS_CUDA(cudaMemcpyAsync(dT, b->arrival, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
   }
   HS_CUDA(cudaMemsetAsync(dMin, 0x7f, sizeof(int32_t), c->stream));
