@@ -254,6 +254,10 @@ int hs_probe_fp64(hs_ctx* ctx, double* dadd_per_s);
  * evaluate it for workload() (scheduling.py:154): y[i] = exp(x[i]) and
  * overflow[i] = 1 where math.exp raises OverflowError.  Host arrays. */
 int hs_exp_batch(hs_ctx* ctx, const double* x, int64_t n, double* y, uint8_t* overflow);
+/* CPython float floor division x // w as the replay kernels evaluate it for
+ * ideal_batch_size (scheduling.py:128: budget // (per_token * tokens)):
+ * y[i] = x[i] // w[i].  Host arrays. */
+int hs_floordiv_batch(hs_ctx* ctx, const double* x, const double* w, int64_t n, double* y);
 
 /* ---- deployment search ------------------------------------------------ */
 /* Fill table[i * HS_MAX_DEGREES + d] for d < n_degrees[i] (degree list =

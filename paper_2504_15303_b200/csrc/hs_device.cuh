@@ -61,8 +61,21 @@ __device__ __forceinline__ double decode_time(const double* p, int64_t b, int64_
 
 // CPython float floor division (Objects/floatobject.c _float_div_mod); here
 // both operands are positive (scheduling.py:128: budget > 0, bytes > 0).
+// fmod(x, y) for x >= 0, 0 < y < inf: x - n*y with n = trunc(x/y) is exactly
+// representable, q = trunc(fl(x/y)) is n or n +- 1 below 2^52, and one FMA
+// with the right q yields that remainder exactly (the library fmod is a
+// bit-serial loop); anything else takes the library path.
+__device__ __forceinline__ double exact_fmod(double vx, double wx) {
+  const double q = trunc(__ddiv_rn(vx, wx));
+  if (!(vx >= 0.0 && wx > 0.0 && wx < INFINITY && q < 4503599627370496.0)) return fmod(vx, wx);
+  double r = __fma_rn(-q, wx, vx);
+  if (r < 0.0) r = __fma_rn(-(q - 1.0), wx, vx);
+  else if (r >= wx) r = __fma_rn(-(q + 1.0), wx, vx);
+  return r;
+}
+
 __device__ __forceinline__ double py_floordiv(double vx, double wx) {
-  double mod = fmod(vx, wx);
+  double mod = exact_fmod(vx, wx);
   double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
   if (mod != 0.0) {
     if ((wx < 0) != (mod < 0)) {
