@@ -75,6 +75,20 @@ __device__ __forceinline__ double exact_fmod(double vx, double wx) {
 }
 
 __device__ __forceinline__ double py_floordiv(double vx, double wx) {
+  {
+    // x >= 0, 0 < w < inf, integer quotient n < 2^50: CPython's result is n.
+    // Its steps: mod = x - n*w (exact), div = fl(fl(x - mod) / w) with x - mod
+    // = n*w, so |div - n| <= n * (2u + u^2) <= 1/4 + 2^-56 (u = 2^-53), and
+    // floor(div) (+1 when div - floor(div) > 0.5) lands on n; n itself is
+    // trunc(fl(x/w)) corrected by the sign of one exact FMA remainder.
+    double q = trunc(__ddiv_rn(vx, wx));
+    if (vx >= 0.0 && wx > 0.0 && wx < INFINITY && q < 1125899906842624.0) {
+      const double r = __fma_rn(-q, wx, vx);
+      if (r < 0.0) q -= 1.0;
+      else if (r >= wx) q += 1.0;
+      return q;
+    }
+  }
   double mod = exact_fmod(vx, wx);
   double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
   if (mod != 0.0) {
