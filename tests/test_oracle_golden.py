@@ -4,8 +4,11 @@ tests/golden/*.json were produced by tests/golden/make_golden.py running the
 unmodified reference package; every float is compared bit for bit.
 """
 
+import json
 import math
+import pathlib
 import random
+import sys
 
 import numpy as np
 import pytest
@@ -157,3 +160,29 @@ def test_oracle_topk_is_head_of_reference_ranking(case):
     from paper_2504_15303_b200.planner import merge_topk
     merged = merge_topk(parts, k)
     assert merged["index"].tolist() == top["index"].tolist()
+
+
+FULLSCALE = json.loads((pathlib.Path(__file__).resolve().parent / "golden" / "fullscale_cases.json").read_text())["cases"]
+
+
+@pytest.mark.parametrize("case", FULLSCALE, ids=lambda c: f"t{c['trace']}-{c['policy']}-{c['mode']}-{c['rate']}")
+def test_oracle_fullscale_matches_reference(case):
+    """The C oracle on the bench's own 1e5-request traces against the
+    reference's outputs (tests/golden/make_fullscale.py): the bench-scale GPU
+    parity tests that use the oracle as checker rest on this pin."""
+    sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent / "golden"))
+    from make_fullscale import case_scenario
+    from paper_2504_15303_b200 import simulator as S
+    from paper_2504_15303_b200 import workloads as wl
+
+    rate = math.inf if case["rate"] == "inf" else float(case["rate"])
+    sc = case_scenario(hs, S, wl, (case["trace"], case["policy"], rate, case["mode"], case["predictor"]))
+    inst, pol, handles, I, O, P, T = H.replay_structs(sc)
+    assign, depart, metrics, result = orc.replay(inst, pol, np.array([0, len(I)], np.int64), I, O, P, T)
+    assert int(result[0]["error"]) == nat.TRACE_OK
+    want = case["metrics"]
+    got = H.metrics_digest(assign, depart, metrics[0], handles, sc.trace, T, want["policy"],
+                           static=sc.mode == "static")
+    for key in ("assign_head", "assign_sha", "makespan", "per_instance", "residual_loads", "depart_sha",
+                "times_sha", "times_head", "throughput", "spread"):
+        assert got[key] == want[key], key
