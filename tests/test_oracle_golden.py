@@ -186,3 +186,30 @@ def test_oracle_fullscale_matches_reference(case):
     for key in ("assign_head", "assign_sha", "makespan", "per_instance", "residual_loads", "depart_sha",
                 "times_sha", "times_head", "throughput", "spread"):
         assert got[key] == want[key], key
+
+
+C5 = json.loads((pathlib.Path(__file__).resolve().parent / "golden" / "fullscale_cases.json").read_text())["config5"]
+
+
+@pytest.mark.parametrize("c", C5, ids=lambda c: f"rank{c['rank']}")
+def test_oracle_config5_fullscale_matches_reference(c):
+    """Config-5 deployments (66-72 instances) on the 1e5-request trace at
+    rate = inf: the C oracle against the reference's run_continuous."""
+    import bench
+    from paper_2504_15303_b200 import workloads as wl
+    from paper_2504_15303_b200.simulator import _policy_struct, build_instances, engine_instances
+
+    cluster, _reqs, params, _I, _O = bench.search_inputs(16)
+    config = hs.deployment_for(cluster.machines, c["degrees"])
+    handles = build_instances(cluster, config, params)
+    assert len(handles) == c["instances"]
+    I1, O1 = wl.trace_lengths(c["q"], seed=0)
+    pol = hs.PolicyConfig()
+    assign, depart, metrics, result = orc.replay(
+        engine_instances(handles, pol), _policy_struct(pol, len(handles), hs.kv_bytes_per_token(cluster.model)),
+        np.array([0, c["q"]], np.int64), I1, O1, O1, None)
+    assert int(result[0]["error"]) == nat.TRACE_OK
+    trace = [hs.Request(f"r{k}", int(I1[k]), int(O1[k]), int(O1[k])) for k in range(c["q"])]
+    got = H.metrics_digest(assign, depart, metrics[0], handles, trace, None, "OS")
+    for key, want in c["metrics"].items():
+        assert got[key] == want, key
