@@ -405,11 +405,13 @@ __global__ void __launch_bounds__(replay_block_threads(W),
 #endif
   // ---- CAL helpers
   // the head of a bucket (retirement step s_) becomes the top: its payload
+  // (the pushed record holds O and I - k_admit, k_admit = s_ - max(O, 1):
+  // one record load, not three scattered ones)
   auto cal_set_top = [&](uint32_t s_, int32_t r2) {
     topkey = ((uint64_t)s_ << 32) | (uint32_t)r2;
-    topI = I[r2];
-    topO = O[r2];
     const QRec q2 = R[r2];
+    topO = q2.nO;
+    topI = (int32_t)((int64_t)q2.nI + (int64_t)s_ - (int64_t)(q2.nO > 1 ? q2.nO : 1));
     topP = q2.P;
     topW = q2.W;
     topnext = q2.next;
@@ -580,6 +582,7 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         const uint64_t w = cb[wi];
         R[r].next = -1;
         R[r].nI = (int32_t)mk;
+        R[r].nO = (int32_t)Or;
         if (w & bit) {
           const int32_t tl = cal[b].y;
           R[tl].next = r;
