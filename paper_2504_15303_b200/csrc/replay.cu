@@ -71,6 +71,11 @@ constexpr int kPipeTracesPerSM = 8;
 #ifndef HS_REPLAY_MIN_BLOCKS
 #define HS_REPLAY_MIN_BLOCKS 4
 #endif
+// the PIPE instantiation runs at most kPipeTracesPerSM traces (2 blocks) per SM,
+// so it may take up to 256 registers (it uses ~160, no spills: 1024 traces 265.8 -> 260.4 ms)
+#ifndef HS_REPLAY_PIPE_MIN_BLOCKS
+#define HS_REPLAY_PIPE_MIN_BLOCKS 2
+#endif
 #ifndef HS_REPLAY_MIN_BLOCKS_MULTI
 #define HS_REPLAY_MIN_BLOCKS_MULTI 3
 #endif
@@ -241,7 +246,8 @@ __device__ __forceinline__ void group_bar(int g, int nthreads) {
 
 template <int W, bool MULTI, bool CAL, bool PIPE>
 __global__ void __launch_bounds__(replay_block_threads(W),
-                                  W == 1 ? HS_REPLAY_MIN_BLOCKS : (W > kWarps ? 1 : HS_REPLAY_MIN_BLOCKS_MULTI))
+                                  W == 1 ? (PIPE ? HS_REPLAY_PIPE_MIN_BLOCKS : HS_REPLAY_MIN_BLOCKS)
+                                         : (W > kWarps ? 1 : HS_REPLAY_MIN_BLOCKS_MULTI))
     k_replay(int64_t n_traces, const int64_t* __restrict__ off, const int32_t* __restrict__ gI,
              const int32_t* __restrict__ gO, const int32_t* __restrict__ gP, const double* __restrict__ gT,
              uint8_t* __restrict__ assign, double* __restrict__ depart, hs_inst_metrics* __restrict__ metrics,
