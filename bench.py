@@ -723,9 +723,10 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
         if n not in tiles:
             ti = eng.host_array((max(n * args.q, 1),), np.int32)
             to = eng.host_array((max(n * args.q, 1),), np.int32)
+            ta = eng.host_array((max(n * args.q, 1),), np.uint8)  # assignments, written in place by the kernel
             ti[: n * args.q] = np.tile(I1, n)
             to[: n * args.q] = np.tile(O1, n)
-            tiles[n] = (ti[: n * args.q], to[: n * args.q])
+            tiles[n] = (ti[: n * args.q], to[: n * args.q], ta)
         return tiles[n]
 
     def step():
@@ -758,9 +759,9 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
         lo, hi = shard_range(len(top), rank, world)
         n = hi - lo
         off = np.arange(n + 1, dtype=np.int64) * args.q
-        I, O = tiled(n)
+        I, O, A = tiled(n)
         res = hs.replay_candidates(t, params, top["index"][lo:hi], hs.PolicyConfig(), np.arange(n), off, I, O, O,
-                                   engine=eng, want_assign=True)
+                                   engine=eng, want_assign=True, assign_out=A)
         assert (res.result["error"] == 0).all()
         return nf, k1, ms_topk, res.kernel_ms, n, top, res, t, lo, hi
 
@@ -820,7 +821,7 @@ def config5_measure(args, rank, world, local_rank, eng, ext, cluster, reqs, para
                           "kernel": "k_replay (multi-deployment)"},
         "e2e": {"value": units / (ms_w / 1e3), "unit": UNIT, "ms_per_step": ms_w, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "note": "search_topk + replay_candidates with page-locked host traces (copies inside the call)"},
+                "note": "search_topk + replay_candidates with page-locked host traces (copies inside the call) and a page-locked assignment buffer the kernel writes in place"},
         "top_indices": [int(x) for x in top["index"][:8]],
         "_units": units, "_P": 5**16, "_nreq": kk * args.q,
     }

@@ -328,7 +328,8 @@ int hs_replay(hs_ctx* ctx, const hs_instance* instances, const hs_policy* policy
  * replayed on its own trace).  Deployment d owns instances
  * [inst_offsets[d], inst_offsets[d+1]) (types numbered per deployment);
  * trace t runs deployment trace_deployment[t]; policy->n_instances is
- * ignored.  metrics is [n_traces][max instances over deployments]. */
+ * ignored.  metrics is [n_traces][max instances over deployments]; assign
+ * and depart as for hs_replay (a page-locked assign buffer is written in place). */
 int hs_replay_deployments(hs_ctx* ctx, const hs_instance* instances, const int32_t* inst_offsets,
                           int32_t n_deployments, const hs_policy* policy, const int32_t* trace_deployment,
                           const hs_trace_batch* batch, uint8_t* assign, double* depart, hs_inst_metrics* metrics,

@@ -309,15 +309,18 @@ class Engine:
 
     def replay_deployments(self, instances, inst_offsets: np.ndarray, policy: hs_policy, trace_dep: np.ndarray,
                            offsets: np.ndarray, I: np.ndarray, O: np.ndarray, P: np.ndarray,
-                           arrival: np.ndarray | None, want_assign: bool = True, want_depart: bool = False):
+                           arrival: np.ndarray | None, want_assign: bool = True, want_depart: bool = False,
+                           assign_out: np.ndarray | None = None, depart_out: np.ndarray | None = None):
+        """assign_out / depart_out: caller buffers (a page-locked assign_out,
+        e.g. host_array, is written by the kernel in place)."""
         T = len(offsets) - 1
         nd = len(inst_offsets) - 1
         n_max = int(np.max(np.diff(inst_offsets))) if nd else 0
         total = int(offsets[-1])
         batch = hs_trace_batch(T, offsets.ctypes.data, I.ctypes.data, O.ctypes.data, P.ctypes.data,
                                None if arrival is None else arrival.ctypes.data)
-        assign = np.zeros(max(total, 1), np.uint8) if want_assign else None
-        depart = np.zeros(max(total, 1), np.float64) if want_depart else None
+        assign = _out_buf(assign_out, total, np.uint8) if want_assign else None
+        depart = _out_buf(depart_out, total, np.float64) if want_depart else None
         metrics = np.zeros(max(T * n_max, 1), METRICS_DTYPE)
         result = np.zeros(max(T, 1), RESULT_DTYPE)
         io = np.ascontiguousarray(inst_offsets, np.int32)

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1388,6 +1389,17 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
   if (n_dep < 1) return fail(HS_ERR_ARG, "n_deployments must be >= 1");
   int rc;
   if ((rc = use_device(c))) return rc;
+  // HS_DEBUG_PHASES=1: host wall time of each phase on stderr (diagnostic)
+  static const bool dbg = std::getenv("HS_DEBUG_PHASES") != nullptr;
+  auto tp0 = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(c->stream);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hs_replay_deployments] %-12s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - tp0).count());
+    tp0 = t;
+  };
   const int64_t T = b->n_traces;
   const int64_t* off = b->offsets;
   if (T < 0 || off[0] != 0) return fail(HS_ERR_ARG, "bad offsets");
@@ -1424,7 +1436,13 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
       (rc = ensure_t(c, S_THEAP, (size_t)(T > 0 ? T : 1), &dTH)) || (rc = ensure_t(c, S_MINNEED, 2, &dMin)))
     return rc;
   if (b->arrival && (rc = ensure_t(c, S_T, tq, &dT))) return rc;
-  if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) return rc;
+  // a page-locked, device-mapped caller buffer takes the assignments directly
+  uint8_t* const zA = mapped_host(assign);
+  if (zA) {
+    dA = zA;
+  } else if (assign && (rc = ensure_t(c, S_ASSIGN, tq, &dA))) {
+    return rc;
+  }
   const size_t dep_w = (pol->flags & HS_REPLAY_ORDER_KEYS) ? 3 : 1;  // doubles per request in `depart`
   if (depart && (rc = ensure_t(c, S_DEPART, tq * dep_w, &dDep))) return rc;
   // requests that never retire (a failed trace) read back as NaN
@@ -1440,6 +1458,7 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
       HS_CUDA(cudaMemcpyAsync(dP, b->pred_output_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, c->stream));
     if (dT) HS_CUDA(cudaMemcpyAsync(dT, b->arrival, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
   }
+  phase("setup+copies");
   HS_CUDA(cudaMemsetAsync(dMin, 0x7f, sizeof(int32_t), c->stream));
   HS_CUDA(cudaMemsetAsync(dMin + 1, 0, sizeof(int32_t), c->stream));
   if (total > 0) {
@@ -1459,6 +1478,7 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
     theap[t] = hacc;
     hacc += deps[trace_dep[t]].heap_stride;
   }
+  phase("need+size");
   uint64_t* dHeap;
   if ((rc = ensure_t(c, S_HEAP, (size_t)(hacc > 0 ? hacc : 1) * 2, &dHeap))) return rc;
   HS_CUDA(cudaMemcpyAsync(dDeps, deps.data(), sizeof(hs::ReplayConst) * n_dep, cudaMemcpyHostToDevice, c->stream));
@@ -1469,14 +1489,16 @@ int hs_replay_deployments(hs_ctx* c, const hs_instance* instances, const int32_t
                             static_cast<const hs::ReplayConst*>(dDeps), dTD, dTH, n_max, max_types));
   c->launches += 1;
   if ((rc = end_timing(c))) return rc;
+  phase("kernel");
   if (T > 0) {
     HS_CUDA(cudaMemcpyAsync(metrics, dM, sizeof(hs_inst_metrics) * T * n_max, cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaMemcpyAsync(result, dR, sizeof(hs_trace_result) * T, cudaMemcpyDeviceToHost, c->stream));
   }
-  if (assign && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
+  if (assign && !zA && total > 0) HS_CUDA(cudaMemcpyAsync(assign, dA, total, cudaMemcpyDeviceToHost, c->stream));
   if (depart && total > 0)
     HS_CUDA(cudaMemcpyAsync(depart, dDep, sizeof(double) * dep_w * total, cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
+  phase("results");
   return HS_OK;
 }
 

@@ -404,10 +404,11 @@ def replay_traces(cluster, config, params, policy: PolicyConfig, offsets, input_
 
 def replay_deployments(cluster, configs, params, policy: PolicyConfig, trace_deployment, offsets, input_len,
                        output_len, pred_output_len, arrival=None, want_assign=True, want_depart=False, engine=None,
-                       static=False) -> ReplayBatchResult:
+                       static=False, assign_out=None, depart_out=None) -> ReplayBatchResult:
     """Replay trace t on deployment configs[trace_deployment[t]] (BASELINE
     config 5: every top-k deployment re-scored by a full simulation), all
-    traces in one launch.  metrics is [T, max instances]."""
+    traces in one launch.  metrics is [T, max instances].  assign_out /
+    depart_out: caller buffers, as for replay_traces."""
     per_token = kv_bytes_per_token(cluster.model)
     inst_all, offs = [], [0]
     for cfg in configs:
@@ -431,13 +432,14 @@ def replay_deployments(cluster, configs, params, policy: PolicyConfig, trace_dep
                                         np.ascontiguousarray(output_len, np.int32),
                                         np.ascontiguousarray(pred_output_len, np.int32),
                                         None if arrival is None else np.ascontiguousarray(arrival, np.float64),
-                                        want_assign=want_assign, want_depart=want_depart)
+                                        want_assign=want_assign, want_depart=want_depart, assign_out=assign_out,
+                                        depart_out=depart_out)
     return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)
 
 
 def replay_candidates(tables, params_by_machine_tp, indices, policy: PolicyConfig, trace_deployment, offsets,
                       input_len, output_len, pred_output_len, arrival=None, want_assign=True, want_depart=False,
-                      engine=None) -> ReplayBatchResult:
+                      engine=None, assign_out=None, depart_out=None) -> ReplayBatchResult:
     """BASELINE config 5 (search -> re-score): replay trace t on
     candidate indices[trace_deployment[t]] of a search's tables, every
     deployment in one launch.  The instance arrays are assembled straight from
@@ -500,5 +502,6 @@ def replay_candidates(tables, params_by_machine_tp, indices, policy: PolicyConfi
                                         np.ascontiguousarray(output_len, np.int32),
                                         np.ascontiguousarray(pred_output_len, np.int32),
                                         None if arrival is None else np.ascontiguousarray(arrival, np.float64),
-                                        want_assign=want_assign, want_depart=want_depart)
+                                        want_assign=want_assign, want_depart=want_depart, assign_out=assign_out,
+                                        depart_out=depart_out)
     return ReplayBatchResult(a, d, m, r, eng.last_kernel_ms)

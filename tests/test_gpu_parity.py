@@ -489,6 +489,31 @@ def test_replay_candidates_equals_object_path(eng):
         assert a.result.tobytes() == b.result.tobytes()
 
 
+def test_replay_candidates_assign_out_in_place(eng):
+    """A page-locked assign_out is written by the kernel in place (no copy
+    back) and equals the default (device buffer copied back) path."""
+    _case, _req, t = _config3_tables(eng)
+    top, _nf, _ = planner.search_topk(t, 24, engine=eng)
+    p3 = wl.config3()
+    params = {k: hs.LatencyParams(*v) for k, v in p3.params.items()}
+    q = 3000
+    I1, O1 = wl.trace_lengths(q, seed=11)
+    n = len(top)
+    off = np.arange(n + 1, dtype=np.int64) * q
+    I, O = np.tile(I1, n), np.tile(O1, n)
+    a = hs.replay_candidates(t, params, top["index"], hs.PolicyConfig(), np.arange(n), off, I, O, O, engine=eng)
+    buf = eng.host_array((n * q + 5,), np.uint8)
+    buf[:] = 0xAB
+    b = hs.replay_candidates(t, params, top["index"], hs.PolicyConfig(), np.arange(n), off, I, O, O, engine=eng,
+                             assign_out=buf)
+    assert np.array_equal(a.assign, b.assign) and np.array_equal(buf[: n * q], a.assign)
+    assert (buf[n * q:] == 0xAB).all()
+    assert a.metrics.tobytes() == b.metrics.tobytes() and a.result.tobytes() == b.result.tobytes()
+    with pytest.raises(ValueError):
+        hs.replay_candidates(t, params, top["index"], hs.PolicyConfig(), np.arange(n), off, I, O, O, engine=eng,
+                             assign_out=np.zeros(5, np.uint8))
+
+
 def _twin_cluster():
     """Two machines of one accelerator type: equal degrees make one instance
     class, different degrees two."""

@@ -16,6 +16,7 @@ q = 100_000; n = 1024
 I1, O1 = wl.trace_lengths(q, seed=0)
 ti = eng.host_array((n * q,), np.int32); to = eng.host_array((n * q,), np.int32)
 ti[:] = np.tile(I1, n); to[:] = np.tile(O1, n)
+ta = eng.host_array((n * q,), np.uint8)
 off = np.arange(n + 1, dtype=np.int64) * q
 orig = eng.replay_deployments
 acc = {}
@@ -25,5 +26,5 @@ eng.replay_deployments = timed
 for it in range(3):
     t0 = time.perf_counter(); t = planner.build_tables(cluster, reqs, params, engine=eng); t1 = time.perf_counter()
     top, nf, ms = planner.search_topk(t, 1024, engine=eng); t2 = time.perf_counter()
-    res = hs.replay_candidates(t, params, top["index"], hs.PolicyConfig(), np.arange(n), off, ti, to, to, engine=eng, want_assign=True); t3 = time.perf_counter()
+    res = hs.replay_candidates(t, params, top["index"], hs.PolicyConfig(), np.arange(n), off, ti, to, to, engine=eng, want_assign=True, assign_out=ta); t3 = time.perf_counter()
     print(f"build_tables {1e3*(t1-t0):.1f} ms  search_topk {1e3*(t2-t1):.1f} ms  replay_candidates {1e3*(t3-t2):.1f} ms (C call {acc['c_call']:.1f}, kernel {res.kernel_ms:.1f})")
