@@ -259,6 +259,12 @@ int hs_exp_batch(hs_ctx* ctx, const double* x, int64_t n, double* y, uint8_t* ov
  * y[i] = x[i] // w[i].  Host arrays. */
 int hs_floordiv_batch(hs_ctx* ctx, const double* x, const double* w, int64_t n, double* y);
 
+/* The IEEE quotient x / b as the replay kernels evaluate kv_usage
+ * (capacity.py:98-106: per_token * running_tokens / budget): from RN(1 / b)
+ * with one FMA correction.  y[i] = x[i] / b[i], b finite and positive.  Host
+ * arrays. */
+int hs_div_batch(hs_ctx* ctx, const double* x, const double* b, int64_t n, double* y);
+
 /* ---- deployment search ------------------------------------------------ */
 /* Fill table[i * HS_MAX_DEGREES + d] for d < n_degrees[i] (degree list =
  * core.py:363-371 enumerate_tp_degrees of machines[i]).  params is

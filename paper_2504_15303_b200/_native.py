@@ -145,7 +145,7 @@ EXPORTS = (
     "hs_device_synchronize", "hs_host_alloc", "hs_host_free", "hs_ctx_stream", "hs_probe_fp64",
     "hs_replay_seeded", "hs_pcg64_seed", "hs_pcg64_seed_u64", "hs_rng_generate",
     "hs_sched_create", "hs_sched_destroy", "hs_sched_evaluate", "hs_sched_choose", "hs_sched_complete",
-    "hs_sched_snapshot", "hs_plan_instance", "hs_sched_get_state", "hs_sched_set_state", "hs_sched_set_instance", "hs_exp_batch", "hs_floordiv_batch", "hs_search_topk_after",
+    "hs_sched_snapshot", "hs_plan_instance", "hs_sched_get_state", "hs_sched_set_state", "hs_sched_set_instance", "hs_exp_batch", "hs_floordiv_batch", "hs_div_batch", "hs_search_topk_after",
 )
 
 _lib = None
@@ -200,6 +200,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "hs_sched_set_instance": ([vp, i32, vp], C.c_int),
             "hs_exp_batch": ([vp, vp, i64, vp, vp], C.c_int),
             "hs_floordiv_batch": ([vp, vp, vp, i64, vp], C.c_int),
+            "hs_div_batch": ([vp, vp, vp, i64, vp], C.c_int),
             "hs_search_topk_after": ([vp, vp, vp, i32, i64, dbl, i64, vp, vp, vp], C.c_int),
             "hs_plan_instance": ([vp, dbl, i64, vp, vp, vp, i64, vp, vp, vp, vp], C.c_int),
             "hs_rng_generate": ([vp, vp, i32, vp, vp, i32, vp, vp], C.c_int),
@@ -354,6 +355,14 @@ class Engine:
         w = np.ascontiguousarray(w, np.float64)
         y = np.empty_like(x)
         self.check(self.lib.hs_floordiv_batch(self.handle, _ptr(x), _ptr(w), len(x), _ptr(y)), "hs_floordiv_batch")
+        return y
+
+    def div_batch(self, x: np.ndarray, b: np.ndarray):
+        """hs_div_batch: the IEEE quotient x / b as the replay kernels compute kv_usage."""
+        x = np.ascontiguousarray(x, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        y = np.empty_like(x)
+        self.check(self.lib.hs_div_batch(self.handle, _ptr(x), _ptr(b), len(x), _ptr(y)), "hs_div_batch")
         return y
 
     # --------------------------------------------------------------- streams

@@ -509,6 +509,33 @@ int hs_floordiv_batch(hs_ctx* c, const double* x, const double* w, int64_t n, do
   return HS_OK;
 }
 
+__global__ void k_div_batch(const double* __restrict__ x, const double* __restrict__ b, int64_t n,
+                            double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = hs::div_rn_by(x[i], b[i], __ddiv_rn(1.0, b[i]));
+}
+
+int hs_div_batch(hs_ctx* c, const double* x, const double* b, int64_t n, double* y) {
+  if (!c || n < 0 || (n > 0 && (!x || !b || !y))) return fail(HS_ERR_ARG, "null argument");
+  int rc;
+  if ((rc = use_device(c))) return rc;
+  if (n == 0) return HS_OK;
+  double *dx, *db, *dy;
+  if ((rc = ensure_t(c, S_TOTAL, (size_t)n, &dx)) || (rc = ensure_t(c, S_KEYS2, (size_t)n, &db)) ||
+      (rc = ensure_t(c, S_KEYS, (size_t)n, &dy)))
+    return rc;
+  HS_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  HS_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > hs::sm_count() * 16) blocks = hs::sm_count() * 16;
+  k_div_batch<<<(unsigned)blocks, 256, 0, c->stream>>>(dx, db, n, dy);
+  HS_CUDA(cudaGetLastError());
+  c->launches += 1;
+  HS_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HS_OK;
+}
+
 int hs_exp_batch(hs_ctx* c, const double* x, int64_t n, double* y, uint8_t* overflow) {
   if (!c || n < 0 || (n > 0 && (!x || !y || !overflow))) return fail(HS_ERR_ARG, "null argument");
   int rc;

@@ -74,6 +74,22 @@ __device__ __forceinline__ double exact_fmod(double vx, double wx) {
   return r;
 }
 
+// x / b rounded to nearest from r = RN(1 / b), for finite positive b and
+// finite x: q0 = RN(x r) lies within an ulp of x / b, the FMA residual
+// x - q0 b is then exact, and one correction RN(q0 + r (x - q0 b)) is the
+// correctly rounded quotient (Markstein's theorem for round-to-nearest) -- the
+// IEEE quotient CPython's `/` gives, without the reciprocal refinement of a
+// full division.  Pinned against numpy's x / b by tests/test_gpu_floordiv.py.
+__device__ __forceinline__ double div_rn_by(double x, double b, double r) {
+  const double q0 = __dmul_rn(x, r);
+  const double e = __fma_rn(-q0, b, x);
+  return __fma_rn(e, r, q0);
+}
+
+#ifndef HS_RECIP_DIV
+#define HS_RECIP_DIV 1
+#endif
+
 __device__ __forceinline__ double py_floordiv(double vx, double wx) {
   {
     // x >= 0, 0 < w < inf, integer quotient n < 2^50: CPython's result is n.

@@ -227,7 +227,9 @@ struct TypeRec {
   double p[8];
   double budget;
   int64_t cap_tok;  // floor(floor(budget) / per_token)
+  double rbudget;   // RN(1 / budget): kv_usage's division by one FMA correction (div_rn_by)
 };
+constexpr int kTypeRecWords = sizeof(TypeRec) / sizeof(double);
 
 // Cross-warp exchange for traces spanning W > 1 warps: one slot per warp of
 // the trace group, a named barrier per group (ids 1..4).
@@ -294,12 +296,13 @@ __global__ void __launch_bounds__(replay_block_threads(W),
   const int NTS = MULTI ? max_types : NT;
   double* cost = s_cost + (size_t)wib * 32 * NTS;
   TypeRec* types = reinterpret_cast<TypeRec*>(s_cost + (size_t)(W * G) * 32 * NTS) + (size_t)g * NTS;
-  for (int k = wsub * 32 + lane; k < NT * 10; k += W * 32) {
-    const int t = k / 10, f = k - t * 10;
+  for (int k = wsub * 32 + lane; k < NT * kTypeRecWords; k += W * 32) {
+    const int t = k / kTypeRecWords, f = k - t * kTypeRecWords;
     double* dst = reinterpret_cast<double*>(types + t) + f;
     if (f < 8) *dst = c_rep.type_p[t][f];
     else if (f == 8) *dst = c_rep.type_budget[t];
-    else *reinterpret_cast<int64_t*>(dst) = c_rep.type_cap_tokens[t];
+    else if (f == 9) *reinterpret_cast<int64_t*>(dst) = c_rep.type_cap_tokens[t];
+    else *dst = __ddiv_rn(1.0, c_rep.type_budget[t]);
   }
   if (W > 1) group_bar(g, W * 32);
   else __syncwarp();
@@ -938,7 +941,11 @@ __global__ void __launch_bounds__(replay_block_threads(W),
         }
         HS_T0(tx0);
         if (dirty) {  // capacity.py:98-106 kv_usage, scheduling.py:154 exp
+#if HS_RECIP_DIV
+          const double usage = div_rn_by(i2d(pt * (run_i + run_p)), budget, trec.rbudget);
+#else
           const double usage = __ddiv_rn(i2d(pt * (run_i + run_p)), budget);
+#endif
           bool of;
           ex = py_exp(__dmul_rn(theta, usage), s_tab, &of);
           ex_over = of;

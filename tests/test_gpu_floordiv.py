@@ -67,3 +67,53 @@ def test_floordiv_2e7_random_pairs_replay_range(eng):
     assert _same(got[sub], x[sub], w[sub]) == []
     assert np.array_equal(want[sub], np.array([a // b for a, b in zip(x[sub].tolist(), w[sub].tolist())]))
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+# ---- kv_usage's division (capacity.py:98-106): x / budget from RN(1 / budget)
+def _div_bits_equal(eng, x, b):
+    got = eng.div_batch(x, b)
+    want = x / b  # IEEE round-to-nearest quotient, the same as CPython's float `/`
+    bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+    return bad, got, want
+
+
+def test_div_replay_range_1e8(eng):
+    """1e8 random (x, budget) pairs over the replay's range: x = per_token *
+    running tokens (integers to 2^50), budgets from 1e6 to 1e13 bytes,
+    fractional and integral, in chunks of 1e7."""
+    rng = np.random.default_rng(77)
+    for c in range(10):
+        n = 10_000_000
+        x = np.floor(rng.uniform(0, 2.0 ** rng.integers(10, 51), n))
+        b = rng.uniform(1e6, 1e13, n)
+        b = np.where(rng.random(n) < 0.5, np.floor(b), b)
+        bad, got, want = _div_bits_equal(eng, x, b)
+        assert len(bad) == 0, (c, x[bad[:5]].tolist(), b[bad[:5]].tolist())
+
+
+def test_div_adversarial(eng):
+    """Divisors with all-ones and near-one mantissas, powers of two, exact
+    quotients and their neighbours, quotients at rounding ties of nearby
+    precision, full-range random doubles."""
+    rng = np.random.default_rng(5)
+    k = rng.integers(-40, 40, 20000)
+    ones = np.ldexp((2.0 ** 53 - 1) / 2.0 ** 52, k)  # 1.111...1 * 2^k
+    near1 = np.ldexp(1.0 + rng.integers(1, 1000, 20000) * 2.0 ** -52, k)
+    pow2 = np.ldexp(1.0, k)
+    b = np.concatenate([ones, near1, pow2, np.nextafter(ones, 0), np.nextafter(near1, np.inf)])
+    q = np.floor(rng.uniform(0, 2.0 ** 52, len(b)))
+    xs, bs = [], []
+    for d in (-1, 0, 1):
+        x = q * b
+        x = np.nextafter(x, np.inf) if d > 0 else (np.nextafter(x, 0) if d < 0 else x)
+        xs.append(x)
+        bs.append(b)
+    xs.append(np.floor(rng.uniform(0, 2.0 ** 50, len(b))))
+    bs.append(b)
+    xs.append(np.abs(rng.standard_normal(200000)) * 10.0 ** rng.integers(-100, 100, 200000))
+    bs.append(np.abs(rng.standard_normal(200000)) * 10.0 ** rng.integers(-100, 100, 200000) + 1e-300)
+    x, b = np.concatenate(xs), np.concatenate(bs)
+    ok = np.isfinite(x) & np.isfinite(b) & (b > 0) & np.isfinite(x / b) & (np.abs(x / b) > 1e-290) | (x == 0)
+    x, b = x[ok], b[ok]
+    bad, got, want = _div_bits_equal(eng, x, b)
+    assert len(bad) == 0, (x[bad[:5]].tolist(), b[bad[:5]].tolist(), got[bad[:5]].tolist(), want[bad[:5]].tolist())
